@@ -1,0 +1,93 @@
+/*
+ * shufflekit_b200.h -- C ABI of the B200-native MergeShuffle engine.
+ *
+ * Drop-in boundary for the reference's operator layer (shufflekit._kernels,
+ * the numba engine behind shufflekit.shufflers; paths relative to the
+ * reference's pkg/src/shufflekit/).  Every entry point is stream-ordered on the
+ * caller's CUDA stream (`stream` = cudaStream_t, NULL = legacy default),
+ * works on caller-owned DEVICE memory (except the *_host variants), permutes in
+ * place, and treats elements as opaque 4- or 8-byte words (elem_bytes in {4,8}).
+ * The result is bit-identical to the reference for the same seed / BitSource
+ * state, for any element type of that width.
+ *
+ * Return value: 0 on success, a negative SK_E* code on failure; sk_last_error()
+ * describes the last failure of the calling thread.  Internal scratch (O(n)
+ * ping-pong buffer, per-round plans) comes from the device's stream-ordered
+ * memory pool and is released before the call returns.
+ *
+ * Bit-source state vectors are the reference's 4-word state
+ * [sm64_state, bit_buffer, buffered_bits, bits_consumed]
+ * (_kernels.py:5-7, bitstream.py:125-130); *_io variants read the state before
+ * the call and write back the state after it, exactly as the reference's
+ * _state_vec/_sync round-trip does (_kernels.py:408-414).
+ */
+#ifndef SHUFFLEKIT_B200_H
+#define SHUFFLEKIT_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SK_OK 0
+#define SK_EINVAL (-1)   /* bad argument (reference raises ValueError) */
+#define SK_ECUDA (-2)    /* CUDA runtime error */
+#define SK_ENOMEM (-3)   /* device allocation failed */
+
+/* Replaces shufflers.merge_shuffle_parallel (shufflers.py:251-299) /
+ * _kernels.merge_shuffle_tasked (_kernels.py:540-543): the frozen substream
+ * schedule, leaf i keyed substream_seed(seed, i), round-r merge at block i keyed
+ * substream_seed(seed, r*q + i).  cutoff = 0 selects MERGE_CUTOFF_DEFAULT
+ * (65536, shufflers.py:29).  *bits_out (host, may be NULL) = ShuffleReport.bits;
+ * when non-NULL the call synchronizes the stream before returning. */
+int sk_merge_shuffle_parallel(void *data, int elem_bytes, uint64_t n, uint64_t cutoff, uint64_t seed,
+                              uint64_t *bits_out, void *stream);
+
+/* Same, on HOST memory: copies in, shuffles, copies out, synchronizes
+ * (the end-to-end path; pinned host memory gives full PCIe bandwidth). */
+int sk_merge_shuffle_parallel_host(void *host_data, int elem_bytes, uint64_t n, uint64_t cutoff, uint64_t seed,
+                                   uint64_t *bits_out, void *stream);
+
+/* `batch` independent arrays of `len` elements, back to back; array t is
+ * shuffled as merge_shuffle_parallel with BitSource(substream_seed(seed, t))
+ * (the per-trial key of _kernels.py:219-220 and cli.py:136).
+ * bits_out: host array of `batch` counts (may be NULL). */
+int sk_batched_shuffle(void *data, int elem_bytes, uint64_t batch, uint64_t len, uint64_t cutoff, uint64_t seed,
+                       uint64_t *bits_out, void *stream);
+
+/* Replaces _kernels.fy_range_inplace (_kernels.py:423-427) / fisher_yates
+ * (shufflers.py:145-155): Fisher-Yates on [lo, hi) from a mid-stream state. */
+int sk_fy_range(void *data, int elem_bytes, uint64_t lo, uint64_t hi, uint64_t state_io[4], void *stream);
+
+/* Replaces _kernels.merge_inplace (_kernels.py:430-434) / merge
+ * (shufflers.py:158-191): shuffled merge of [j,k) and [k,l). */
+int sk_merge_range(void *data, int elem_bytes, uint64_t j, uint64_t k, uint64_t l, uint64_t state_io[4],
+                   void *stream);
+
+/* Replaces _kernels.merge_shuffle_inplace (_kernels.py:437-441) /
+ * merge_shuffle (shufflers.py:194-217): the sequential single-stream variant.
+ * Inherently serial (every task's start offset depends on all earlier tasks);
+ * runs as one GPU thread. */
+int sk_merge_shuffle_seq(void *data, int elem_bytes, uint64_t n, uint64_t cutoff, uint64_t state_io[4],
+                         void *stream);
+
+/* Replaces _kernels.chi_counts (_kernels.py:489-526) for algo "fy" (0),
+ * "merge" (1) and "merge_parallel" (2); 2 <= n <= 20 ... counts_out: host
+ * array of n! int64 bins.  Synchronizes. */
+int sk_chi_counts(int algo, int n, uint64_t trials, uint64_t seed, uint64_t cutoff, int64_t *counts_out,
+                  void *stream);
+
+/* Diagnostics. */
+const char *sk_last_error(void);
+int sk_version(void);
+uint64_t sk_launch_count(void);       /* kernels launched by this library so far */
+void sk_profile_enable(int on);       /* record CUDA events around the data-path stages */
+/* stage times (ms, summed) and launch counts since enable: stage 0 leaf decode,
+ * 1 leaf apply, 2 merge rounds (window kernel + identity region + tail apply),
+ * 3 final copy; returns number of stages written.  Synchronizes. */
+int sk_profile_read(double *ms_out, uint64_t *launches_out, int max_stages);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,704 @@
+// engine.cu -- orchestration of the B200 MergeShuffle pipeline and the C ABI.
+//
+// Data path (caller stream):   leaf decode -> leaf apply -> round 1 .. round c
+//   (round = window gather kernel, identity region, tail gather/scatter),
+//   ping-ponging between the caller's buffer and one O(n) scratch buffer.
+// Plan path (side stream, data independent, overlaps the leaf stage):
+//   per round: superblock rank tables -> stop points / X -> window chains;
+//   then one launch decodes every pair's tail draws (all rounds at once),
+//   then per round: radix sort of tail targets -> (dst, src) tail plan.
+// Reference driver: shufflers.py:251-299 / _kernels.py:253-289.
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/shufflekit_b200.h"
+#include "sk_kernels.h"
+
+namespace sk {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static thread_local std::string g_err;
+static void set_err(const std::string& s) { g_err = s; }
+
+int num_sms() {
+  int dev = 0, v = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
+}
+
+struct CudaError {
+  int code;
+};
+
+#define CK(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      set_err(std::string(#expr) + ": " + cudaGetErrorString(e_));                            \
+      throw CudaError{e_ == cudaErrorMemoryAllocation ? SK_ENOMEM : SK_ECUDA};                \
+    }                                                                                         \
+  } while (0)
+
+// ------------------------------------------------------------------ profiling
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static constexpr int kStages = 5;
+struct ProfRec {
+  int stage;
+  cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_prof;
+static uint64_t g_prof_launch[kStages];
+
+struct StageTimer {
+  int stage;
+  cudaStream_t st;
+  cudaEvent_t a{}, b{};
+  uint64_t l0;
+  bool on;
+  StageTimer(int s, cudaStream_t stream) : stage(s), st(stream), l0(g_launches.load()), on(g_prof_on) {
+    if (on) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~StageTimer() {
+    if (on) {
+      cudaEventRecord(b, st);
+      std::lock_guard<std::mutex> lk(g_prof_mu);
+      g_prof.push_back({stage, a, b});
+      g_prof_launch[stage] += g_launches.load() - l0;
+    }
+  }
+};
+
+// ------------------------------------------------------------ device memory
+static void setup_pool_once() {
+  static std::once_flag f;
+  std::call_once(f, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+// All allocations of one call; freed stream-ordered on the data stream.
+struct Arena {
+  std::vector<void*> ptrs;
+  template <typename T>
+  T* alloc(size_t count, cudaStream_t st) {
+    if (count == 0) count = 1;
+    void* p = nullptr;
+    CK(cudaMallocAsync(&p, count * sizeof(T), st));
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  void release(cudaStream_t st) {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+    ptrs.clear();
+  }
+};
+
+static int plan_c(uint64_t n, uint64_t cutoff) {
+  int c = 0;
+  while ((n >> c) > cutoff) ++c;
+  return c;
+}
+
+struct LevelBufs {
+  LevelJob LJ;
+  uint64_t sbs = 0, npairs = 0;
+  uint32_t tpp = 0;
+  uint64_t* rank = nullptr;
+  PairPlan* plans = nullptr;
+  uint64_t* wins = nullptr;
+  uint32_t* nwin = nullptr;
+  // tails
+  uint64_t total = 0;
+  uint64_t* rec_key = nullptr;
+  uint32_t* rec_pair = nullptr;
+  uint64_t* skey = nullptr;
+  uint32_t* sval = nullptr;
+  uint32_t* ival = nullptr;
+  uint64_t* predx = nullptr;
+  uint8_t* keyed = nullptr;
+  uint64_t* dst = nullptr;
+  uint64_t* src = nullptr;
+  void* tmp = nullptr;
+  cudaEvent_t ev_tail{};
+};
+
+__global__ void set_tail_off_kernel(PairPlan* plans, const uint64_t* offs, uint64_t n) {
+  uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < n) plans[g].tail_off = offs[g];
+}
+
+// Order `ps` after everything queued on `st` so far (allocations, bit counters).
+static void fork_side(cudaStream_t st, cudaStream_t ps) {
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, st));
+  CK(cudaStreamWaitEvent(ps, ev, 0));
+  cudaEventDestroy(ev);
+}
+
+// Build every round's plan on `ps`; on return the window chains are queued
+// (ev_windows) and the tail plans are queued per round (lv[r].ev_tail).
+// Host-synchronizes once on the stop points (tail buffer sizing) -- the data
+// stream keeps running the leaf stage meanwhile.
+static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* d_bits, Arena& A, cudaStream_t ps,
+                        cudaStream_t st) {
+  const int nl = (int)lv.size();
+  uint32_t T = merge_tile(eb);
+  (void)st;
+  for (auto& L : lv) {
+    L.rank = A.alloc<uint64_t>(L.npairs * L.sbs, ps);
+    L.plans = A.alloc<PairPlan>(L.npairs, ps);
+    L.wins = A.alloc<uint64_t>(L.npairs * L.tpp * kHMax, ps);
+    L.nwin = A.alloc<uint32_t>(L.npairs * L.tpp, ps);
+  }
+  for (auto& L : lv) {
+    launch_rank_tables(L.LJ, L.sbs, L.rank, ps);
+    launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, ps);
+    launch_windows(L.plans, L.npairs, L.tpp, T, L.rank, L.wins, L.nwin, ps);
+  }
+  CK(cudaGetLastError());
+  // tail sizes -> host
+  uint64_t tot_pairs = 0;
+  std::vector<uint64_t> pprefix(nl + 1, 0);
+  for (int i = 0; i < nl; ++i) {
+    pprefix[i] = tot_pairs;
+    tot_pairs += lv[i].npairs;
+  }
+  pprefix[nl] = tot_pairs;
+  std::vector<PairPlan> hplans(tot_pairs);
+  for (int i = 0; i < nl; ++i)
+    CK(cudaMemcpyAsync(hplans.data() + pprefix[i], lv[i].plans, lv[i].npairs * sizeof(PairPlan),
+                       cudaMemcpyDeviceToHost, ps));
+  CK(cudaStreamSynchronize(ps));
+  std::vector<uint64_t> offs(tot_pairs);
+  for (int i = 0; i < nl; ++i) {
+    uint64_t acc = 0;
+    for (uint64_t g = 0; g < lv[i].npairs; ++g) {
+      offs[pprefix[i] + g] = acc;
+      acc += hplans[pprefix[i] + g].tail_len;
+    }
+    lv[i].total = acc;
+  }
+  uint64_t* d_offs = A.alloc<uint64_t>(tot_pairs, ps);
+  CK(cudaMemcpyAsync(d_offs, offs.data(), tot_pairs * 8, cudaMemcpyHostToDevice, ps));
+  std::vector<LevelTail> ht(nl);
+  for (int i = 0; i < nl; ++i) {
+    auto& L = lv[i];
+    set_tail_off_kernel<<<(unsigned)((L.npairs + 255) / 256), 256, 0, ps>>>(L.plans, d_offs + pprefix[i], L.npairs);
+    count_launch();
+    L.rec_key = A.alloc<uint64_t>(L.total, ps);
+    L.rec_pair = A.alloc<uint32_t>(L.total, ps);
+    ht[i] = LevelTail{L.plans, L.npairs, L.rec_key, L.rec_pair};
+  }
+  LevelTail* d_lt = A.alloc<LevelTail>(nl, ps);
+  uint64_t* d_pp = A.alloc<uint64_t>(nl + 1, ps);
+  CK(cudaMemcpyAsync(d_lt, ht.data(), nl * sizeof(LevelTail), cudaMemcpyHostToDevice, ps));
+  CK(cudaMemcpyAsync(d_pp, pprefix.data(), (nl + 1) * 8, cudaMemcpyHostToDevice, ps));
+  launch_tail_decode(d_lt, nl, d_pp, tot_pairs, d_bits, ps);
+  // per round: sort tail targets, build (dst, src)
+  uint64_t nbits_key = 1;
+  {
+    uint64_t mx = 0;
+    for (auto& L : lv) mx = std::max(mx, (uint64_t)L.LJ.J.batch * L.LJ.J.len);
+    if (lv[0].LJ.E.active) mx = lv[0].LJ.E.lo + lv[0].LJ.E.n1 + lv[0].LJ.E.n2;
+    while ((1ULL << nbits_key) <= mx && nbits_key < 64) ++nbits_key;
+  }
+  for (auto& L : lv) {
+    CK(cudaEventCreateWithFlags(&L.ev_tail, cudaEventDisableTiming));
+    if (L.total) {
+      L.skey = A.alloc<uint64_t>(L.total, ps);
+      L.sval = A.alloc<uint32_t>(L.total, ps);
+      L.ival = A.alloc<uint32_t>(L.total, ps);
+      L.predx = A.alloc<uint64_t>(L.total, ps);
+      L.keyed = A.alloc<uint8_t>(L.total, ps);
+      L.dst = A.alloc<uint64_t>(2 * L.total, ps);
+      L.src = A.alloc<uint64_t>(2 * L.total, ps);
+      L.tmp = A.alloc<uint64_t>(2 * L.total, ps);
+      launch_iota32(L.ival, L.total, ps);
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, L.rec_key, L.skey, L.ival, L.sval, (int)L.total, 0,
+                                         (int)nbits_key, ps));
+      void* tstore = A.alloc<unsigned char>(tb, ps);
+      CK(cub::DeviceRadixSort::SortPairs(tstore, tb, L.rec_key, L.skey, L.ival, L.sval, (int)L.total, 0,
+                                         (int)nbits_key, ps));
+      count_launch();
+      CK(cudaMemsetAsync(L.keyed, 0, L.total, ps));
+      CK(cudaMemsetAsync(L.dst, 0xFF, 2 * L.total * 8, ps));
+      launch_tail_plan(L.plans, L.rec_key, L.rec_pair, L.skey, L.sval, L.total, L.predx, L.keyed, L.dst, L.src, ps);
+      launch_tail_chase(L.plans, L.rec_key, L.rec_pair, L.predx, L.keyed, L.total, L.dst, L.src, ps);
+    }
+    CK(cudaEventRecord(L.ev_tail, ps));
+  }
+  CK(cudaGetLastError());
+}
+
+struct SideStream {
+  cudaStream_t s = nullptr;
+  SideStream() { cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); }
+  ~SideStream() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+static cudaStream_t side_stream() {
+  static thread_local SideStream ss;
+  return ss.s;
+}
+
+// Run rounds 1..c over `cur` (data currently there), ping-ponging with `other`.
+// Returns the buffer holding the result.
+static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* other, cudaStream_t st) {
+  for (auto& L : lv) {
+    {
+      StageTimer tm(2, st);
+      launch_merge_level(eb, cur, other, L.plans, L.npairs, L.tpp, L.rank, L.wins, L.nwin, st);
+    }
+    {
+      StageTimer tm(3, st);
+      launch_copy_tail_region(eb, cur, other, L.plans, L.npairs, st);
+      CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
+      launch_tail_apply(eb, other, L.dst, L.src, L.tmp, 2 * L.total, st);
+    }
+    std::swap(cur, other);
+  }
+  CK(cudaGetLastError());
+  return cur;
+}
+
+static std::vector<LevelBufs> make_levels(const ArrayJob& J, int eb) {
+  std::vector<LevelBufs> lv;
+  uint32_t T = merge_tile(eb);
+  for (int r = 1; r <= J.c; ++r) {
+    LevelBufs L;
+    L.LJ.J = J;
+    L.LJ.E = ExplicitTask{};
+    L.LJ.r = r;
+    L.npairs = J.batch << (J.c - r);
+    L.LJ.npairs = L.npairs;
+    uint64_t Nmax = (J.len >> (J.c - r)) + 2;
+    uint64_t n1max = (J.len >> (J.c - r + 1)) + 1;
+    L.sbs = (Nmax + 1 + 511) / 512 + 1;
+    L.tpp = (uint32_t)((n1max + T - 1) / T);
+    lv.push_back(L);
+  }
+  return lv;
+}
+
+// The whole tasked schedule for a batch of arrays (batch = 1: one array).
+static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d_bits, cudaStream_t st) {
+  const uint64_t ntot = J.batch * J.len;
+  if (ntot == 0) return;
+  setup_pool_once();
+  Arena A;
+  cudaStream_t ps = side_stream();
+  std::vector<LevelBufs> lv = make_levels(J, eb);
+  void* scratch = A.alloc<unsigned char>(ntot * eb, st);
+  const uint64_t nleaves = J.batch * J.q;
+  const uint64_t mmax = (J.len >> J.c) + 1;
+  ExplicitTask E0{};
+  try {
+    uint16_t* draws = nullptr;
+    uint16_t* lscr = nullptr;
+    uint32_t grid = 0;
+    bool fast_leaf = mmax <= 65536;
+    if (fast_leaf) {
+      draws = A.alloc<uint16_t>(ntot, st);
+      grid = leaf_apply_grid(nleaves, (uint32_t)mmax, num_sms());
+      lscr = A.alloc<uint16_t>((uint64_t)grid * 2 * mmax, st);
+    }
+    fork_side(st, ps);
+    {
+      StageTimer tm(0, st);
+      if (fast_leaf) launch_leaf_decode16(J, E0, nleaves, draws, d_bits, st);
+    }
+    void* cur;
+    {
+      StageTimer tm(1, st);
+      if (fast_leaf) {
+        launch_leaf_apply(eb, J, E0, nleaves, data, scratch, draws, lscr, (uint32_t)mmax, grid, st);
+      } else {
+        CK(cudaMemcpyAsync(scratch, data, ntot * eb, cudaMemcpyDeviceToDevice, st));
+        launch_leaf_serial(eb, J, E0, nleaves, scratch, d_bits, st);
+      }
+      cur = scratch;
+    }
+    CK(cudaGetLastError());
+    // plans run on the side stream while the leaf stage runs
+    if (!lv.empty()) build_plans(lv, eb, d_bits, A, ps, st);
+    void* res = run_rounds(lv, eb, cur, data, st);
+    if (res != data) {
+      StageTimer tm(4, st);
+      CK(cudaMemcpyAsync(data, res, ntot * eb, cudaMemcpyDeviceToDevice, st));
+    }
+  } catch (...) {
+    cudaStreamSynchronize(ps);
+    cudaStreamSynchronize(st);
+    for (auto& L : lv)
+      if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+    A.release(st);
+    throw;
+  }
+  cudaEvent_t done;
+  CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  CK(cudaEventRecord(done, ps));
+  CK(cudaStreamWaitEvent(st, done, 0));
+  cudaEventDestroy(done);
+  for (auto& L : lv)
+    if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+  A.release(st);
+}
+
+// ---------------------------------------------------- bit-source state maths
+// State after consuming T more bits (SURVEY A2 closed form of bitstream.py:152-176).
+static void advance_state(uint64_t s[4], uint64_t T) {
+  uint64_t state = s[0], buf = s[1], buflen = s[2], consumed = s[3];
+  if (T <= buflen) {
+    buflen -= T;
+    buf = buflen ? (buf & ((1ULL << buflen) - 1)) : 0;
+  } else {
+    uint64_t need = T - buflen;
+    uint64_t w = (need + 63) / 64;
+    state += w * GOLDEN;
+    uint64_t rem = 64 * w - need;
+    buf = rem ? (mix64(state) & ((1ULL << rem) - 1)) : 0;
+    buflen = rem;
+  }
+  s[0] = state; s[1] = buf; s[2] = buflen; s[3] = consumed + T;
+}
+
+static StreamDesc desc_from_state(const uint64_t s[4]) {
+  StreamDesc d;
+  d.state = s[0];
+  d.plen = (uint32_t)s[2];
+  d.buf = d.plen ? (s[1] & ((1ULL << d.plen) - 1)) : 0;
+  d.pad = 0;
+  return d;
+}
+
+static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t l, const StreamDesc& sd,
+                            unsigned long long* d_bits, cudaStream_t st) {
+  setup_pool_once();
+  Arena A;
+  cudaStream_t ps = side_stream();
+  std::vector<LevelBufs> lv(1);
+  LevelBufs& L = lv[0];
+  uint64_t N = l - j;
+  L.LJ.J = ArrayJob{1, N, 1, 0, 0, 0};
+  L.LJ.E = ExplicitTask{1, j, k - j, l - k, sd};
+  L.LJ.r = 1;
+  L.LJ.npairs = 1;
+  L.npairs = 1;
+  L.sbs = (N + 1 + 511) / 512 + 1;
+  uint32_t T = merge_tile(eb);
+  L.tpp = (uint32_t)((k - j + T - 1) / T);
+  if (L.tpp == 0) L.tpp = 1;
+  try {
+    unsigned char* scratch = A.alloc<unsigned char>(N * eb, st);
+    fork_side(st, ps);
+    build_plans(lv, eb, d_bits, A, ps, st);
+    // kernels address elements by absolute index; shift the scratch base so
+    // index j lands on scratch[0].
+    void* out_base = (void*)(scratch - j * eb);
+    launch_merge_level(eb, data, out_base, L.plans, 1, L.tpp, L.rank, L.wins, L.nwin, st);
+    launch_copy_tail_region(eb, data, out_base, L.plans, 1, st);
+    CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
+    launch_tail_apply(eb, out_base, L.dst, L.src, L.tmp, 2 * L.total, st);
+    CK(cudaMemcpyAsync((unsigned char*)data + j * eb, scratch, N * eb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaGetLastError());
+  } catch (...) {
+    cudaStreamSynchronize(ps);
+    cudaStreamSynchronize(st);
+    if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+    A.release(st);
+    throw;
+  }
+  cudaEvent_t done;
+  CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  CK(cudaEventRecord(done, ps));
+  CK(cudaStreamWaitEvent(st, done, 0));
+  cudaEventDestroy(done);
+  if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+  A.release(st);
+}
+
+static void run_single_leaf(int eb, void* data, uint64_t lo, uint64_t hi, const StreamDesc& sd,
+                            unsigned long long* d_bits, cudaStream_t st) {
+  setup_pool_once();
+  Arena A;
+  uint64_t m = hi - lo;
+  ArrayJob J{1, m, 1, 0, 0, 0};
+  ExplicitTask E{1, lo, m, 0, sd};
+  try {
+    if (m <= 65536) {
+      uint16_t* draws = A.alloc<uint16_t>(m, st);
+      unsigned char* scratch = A.alloc<unsigned char>(m * eb, st);
+      uint16_t* lscr = A.alloc<uint16_t>(2 * m, st);
+      // absolute-index kernels: shift bases so index lo lands on element 0
+      launch_leaf_decode16(J, E, 1, draws - lo, d_bits, st);
+      launch_leaf_apply(eb, J, E, 1, data, (void*)(scratch - lo * eb), draws - lo, lscr, (uint32_t)m, 1, st);
+      CK(cudaMemcpyAsync((unsigned char*)data + lo * eb, scratch, m * eb, cudaMemcpyDeviceToDevice, st));
+    } else {
+      launch_leaf_serial(eb, J, E, 1, data, d_bits, st);
+    }
+    CK(cudaGetLastError());
+  } catch (...) {
+    cudaStreamSynchronize(st);
+    A.release(st);
+    throw;
+  }
+  A.release(st);
+}
+
+}  // namespace sk
+
+// ===================================================================== C ABI
+using namespace sk;
+
+#define SK_TRY try {
+#define SK_CATCH                                   \
+  }                                                \
+  catch (const CudaError& e) {                     \
+    return e.code;                                 \
+  }                                                \
+  catch (const std::exception& e) {                \
+    set_err(e.what());                             \
+    return SK_ECUDA;                               \
+  }                                                \
+  return SK_OK;
+
+static int check_eb(int eb) {
+  if (eb != 4 && eb != 8) {
+    set_err("elem_bytes must be 4 or 8");
+    return SK_EINVAL;
+  }
+  return SK_OK;
+}
+
+static int fetch_bits(unsigned long long* d_bits, uint64_t* out, uint64_t count, cudaStream_t st) {
+  if (out) {
+    CK(cudaMemcpyAsync(out, d_bits, count * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return SK_OK;
+}
+
+extern "C" {
+
+int sk_version(void) { return 1; }
+const char* sk_last_error(void) { return g_err.c_str(); }
+uint64_t sk_launch_count(void) { return g_launches.load(); }
+
+void sk_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  memset(g_prof_launch, 0, sizeof(g_prof_launch));
+  g_prof_on = on != 0;
+}
+
+int sk_profile_read(double* ms_out, uint64_t* launches_out, int max_stages) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  int ns = std::min(max_stages, kStages);
+  std::vector<double> acc(kStages, 0.0);
+  for (auto& r : g_prof) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    acc[r.stage] += ms;
+  }
+  for (int i = 0; i < ns; ++i) {
+    if (ms_out) ms_out[i] = acc[i];
+    if (launches_out) launches_out[i] = g_prof_launch[i];
+  }
+  return ns;
+}
+
+int sk_merge_shuffle_parallel(void* data, int elem_bytes, uint64_t n, uint64_t cutoff, uint64_t seed,
+                              uint64_t* bits_out, void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (n && !data) { set_err("null data"); return SK_EINVAL; }
+  if (cutoff == 0) cutoff = 65536;
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  unsigned long long* d_bits;
+  CK(cudaMallocAsync((void**)&d_bits, 8, st));
+  CK(cudaMemsetAsync(d_bits, 0, 8, st));
+  int c = plan_c(n, cutoff);
+  ArrayJob J{1, n, 1ULL << c, c, 0, seed};
+  try {
+    run_job(elem_bytes, data, J, d_bits, st);
+    fetch_bits(d_bits, bits_out, 1, st);
+  } catch (...) {
+    cudaFreeAsync(d_bits, st);
+    throw;
+  }
+  CK(cudaFreeAsync(d_bits, st));
+  SK_CATCH
+}
+
+int sk_merge_shuffle_parallel_host(void* host_data, int elem_bytes, uint64_t n, uint64_t cutoff, uint64_t seed,
+                                   uint64_t* bits_out, void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (n && !host_data) { set_err("null data"); return SK_EINVAL; }
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  void* d = nullptr;
+  CK(cudaMallocAsync(&d, n ? n * elem_bytes : 1, st));
+  CK(cudaMemcpyAsync(d, host_data, n * elem_bytes, cudaMemcpyHostToDevice, st));
+  uint64_t bits = 0;
+  int rc = sk_merge_shuffle_parallel(d, elem_bytes, n, cutoff, seed, &bits, stream);
+  if (rc == SK_OK) {
+    CK(cudaMemcpyAsync(host_data, d, n * elem_bytes, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaFreeAsync(d, st));
+  CK(cudaStreamSynchronize(st));
+  if (rc) return rc;
+  if (bits_out) *bits_out = bits;
+  SK_CATCH
+}
+
+int sk_batched_shuffle(void* data, int elem_bytes, uint64_t batch, uint64_t len, uint64_t cutoff, uint64_t seed,
+                       uint64_t* bits_out, void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (batch && len && !data) { set_err("null data"); return SK_EINVAL; }
+  if (cutoff == 0) cutoff = 65536;
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  unsigned long long* d_bits;
+  CK(cudaMallocAsync((void**)&d_bits, (batch ? batch : 1) * 8, st));
+  CK(cudaMemsetAsync(d_bits, 0, (batch ? batch : 1) * 8, st));
+  int c = plan_c(len, cutoff);
+  ArrayJob J{batch, len, 1ULL << c, c, 1, seed};
+  try {
+    run_job(elem_bytes, data, J, d_bits, st);
+    fetch_bits(d_bits, bits_out, batch, st);
+  } catch (...) {
+    cudaFreeAsync(d_bits, st);
+    throw;
+  }
+  CK(cudaFreeAsync(d_bits, st));
+  SK_CATCH
+}
+
+int sk_fy_range(void* data, int elem_bytes, uint64_t lo, uint64_t hi, uint64_t state_io[4], void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (!state_io || hi < lo) { set_err("bad range or state"); return SK_EINVAL; }
+  if (state_io[2] > 63) { set_err("buffered_bits must be < 64"); return SK_EINVAL; }
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  if (hi - lo >= 2) {
+    unsigned long long* d_bits;
+    CK(cudaMallocAsync((void**)&d_bits, 8, st));
+    CK(cudaMemsetAsync(d_bits, 0, 8, st));
+    uint64_t bits = 0;
+    try {
+      run_single_leaf(elem_bytes, data, lo, hi, desc_from_state(state_io), d_bits, st);
+      fetch_bits(d_bits, &bits, 1, st);
+    } catch (...) {
+      cudaFreeAsync(d_bits, st);
+      throw;
+    }
+    CK(cudaFreeAsync(d_bits, st));
+    advance_state(state_io, bits);
+  }
+  SK_CATCH
+}
+
+int sk_merge_range(void* data, int elem_bytes, uint64_t j, uint64_t k, uint64_t l, uint64_t state_io[4],
+                   void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (!state_io || k < j || l < k) { set_err("bad merge range or state"); return SK_EINVAL; }
+  if (state_io[2] > 63) { set_err("buffered_bits must be < 64"); return SK_EINVAL; }
+  if (k == j || l == k) return SK_OK;  // _kernels.py:99-100
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  unsigned long long* d_bits;
+  CK(cudaMallocAsync((void**)&d_bits, 8, st));
+  CK(cudaMemsetAsync(d_bits, 0, 8, st));
+  uint64_t bits = 0;
+  try {
+    run_single_pair(elem_bytes, data, j, k, l, desc_from_state(state_io), d_bits, st);
+    fetch_bits(d_bits, &bits, 1, st);
+  } catch (...) {
+    cudaFreeAsync(d_bits, st);
+    throw;
+  }
+  CK(cudaFreeAsync(d_bits, st));
+  advance_state(state_io, bits);
+  SK_CATCH
+}
+
+int sk_merge_shuffle_seq(void* data, int elem_bytes, uint64_t n, uint64_t cutoff, uint64_t state_io[4],
+                         void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (!state_io) { set_err("null state"); return SK_EINVAL; }
+  if (state_io[2] > 63) { set_err("buffered_bits must be < 64"); return SK_EINVAL; }
+  if (cutoff == 0) cutoff = 65536;
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  unsigned long long* d_bits;
+  CK(cudaMallocAsync((void**)&d_bits, 8, st));
+  CK(cudaMemsetAsync(d_bits, 0, 8, st));
+  uint64_t bits = 0;
+  if (n) launch_seq(elem_bytes, data, n, cutoff, desc_from_state(state_io), d_bits, st);
+  CK(cudaGetLastError());
+  fetch_bits(d_bits, &bits, 1, st);
+  CK(cudaFreeAsync(d_bits, st));
+  advance_state(state_io, bits);
+  SK_CATCH
+}
+
+int sk_chi_counts(int algo, int n, uint64_t trials, uint64_t seed, uint64_t cutoff, int64_t* counts_out,
+                  void* stream) {
+  if (algo < 0 || algo > 2 || n < 1 || n > 20 || !counts_out) {
+    set_err("chi_counts: algo in {0,1,2}, 1 <= n <= 20");
+    return SK_EINVAL;
+  }
+  if (cutoff == 0) cutoff = 65536;
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  uint64_t nf = 1;
+  for (int i = 2; i <= n; ++i) nf *= (uint64_t)i;
+  unsigned long long* d;
+  CK(cudaMallocAsync((void**)&d, nf * 8, st));
+  CK(cudaMemsetAsync(d, 0, nf * 8, st));
+  if (trials) launch_chi(algo, n, trials, seed, cutoff, d, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(counts_out, d, nf * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(d, st));
+  CK(cudaStreamSynchronize(st));
+  SK_CATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,490 @@
+// merge.cu -- one merge round of the parallel schedule (reference: _kernels.py:96-121
+// _merge, shufflers.py:158-191 merge, rounds shufflers.py:117-130 / 291-297).
+//
+// Phase 1 (the coin-flip swap merge) is rewritten as a gather over "windows":
+// the A queue of the in-place merge is the stream F with F[u] = A[u] (u < n1)
+// and F[n1 + k] = F[select1(k)], so a tile of A elements [u0, u1) travels through
+// contiguous windows V_0 = [u0, u1), V_{h+1} = [n1 + rank'(start V_h),
+// n1 + rank'(end V_h)) (rank' = ones before min(p, t)).  In a window, a zero at p
+// emits the carried A element, a one emits B[rank'(p)] and carries the A element
+// on to the next window.  Windows of all tiles partition [0, X); [X, N) is the
+// identity (A queue empty).  Every element is read once and written once.
+// (Derivation + CPU check: tests/decomp_model.py merge_phase1_model.)
+//
+// Phase 2 (tail insertion, x = t..N-1: swap(x, FDR(x+1))) is precomputed as a
+// (dst, src) list over the touched set (tests/decomp_model.py tail_plan_model)
+// and applied as a gather then a scatter.
+//
+// Everything except the element movement depends only on (schedule, seed), so
+// the rank tables, stop points, window chains, tail draws and tail plans are
+// built on a side stream while the leaf stage runs.
+#include "sk_kernels.h"
+
+namespace sk {
+
+// ------------------------------------------------------------- rank tables
+__global__ void rank_count_kernel(LevelJob LJ, uint64_t sbs, uint64_t* __restrict__ rank) {
+  uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t per = sbs - 1;
+  if (idx >= LJ.npairs * per) return;
+  uint64_t g = idx / per, k = idx - g * per;
+  uint64_t s, n1, n2, arr;
+  StreamDesc sd;
+  pair_geom(LJ, g, s, n1, n2, sd, arr);
+  uint64_t N = n1 + n2;
+  uint64_t* R = rank + g * sbs;
+  if (k == 0) R[0] = 0;
+  uint64_t cnt = 0;
+  if (n1 && n2 && (k << 9) < N + 1) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) cnt += __popcll(chunk(sd, (k << 3) + w));
+  }
+  R[k + 1] = cnt;
+}
+
+// In-place inclusive scan of each pair's table (one CTA per pair).
+__global__ void __launch_bounds__(1024) seg_scan_kernel(uint64_t* __restrict__ rank, uint64_t sbs) {
+  uint64_t* R = rank + (uint64_t)blockIdx.x * sbs;
+  __shared__ uint64_t wsum[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint64_t carry = 0;
+  for (uint64_t base = 0; base < sbs; base += 1024) {
+    uint64_t i = base + tid;
+    uint64_t x = (i < sbs) ? R[i] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint64_t w = wsum[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= (uint32_t)o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    uint64_t add = carry + (wid ? wsum[wid - 1] : 0);
+    if (i < sbs) R[i] = x + add;
+    carry += wsum[31];
+    __syncthreads();
+  }
+}
+
+void launch_rank_tables(const LevelJob& LJ, uint64_t sbs, uint64_t* rank, cudaStream_t st) {
+  uint64_t total = LJ.npairs * (sbs - 1);
+  if (!total) return;
+  rank_count_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(LJ, sbs, rank);
+  count_launch();
+  seg_scan_kernel<<<(unsigned)LJ.npairs, 1024, 0, st>>>(rank, sbs);
+  count_launch();
+}
+
+// ------------------------------------------------------------ pair plans
+// position (from the MSB) of the r-th (0-based) set bit of x; it must exist
+__device__ __forceinline__ uint32_t select_msb(uint64_t x, uint32_t r) {
+  uint32_t pos = 0, c;
+  c = __popcll(x >> 32);            if (r >= c) { r -= c; pos += 32; x <<= 32; }
+  c = __popc((uint32_t)(x >> 48));  if (r >= c) { r -= c; pos += 16; x <<= 16; }
+  c = __popc((uint32_t)(x >> 56));  if (r >= c) { r -= c; pos += 8;  x <<= 8; }
+  c = __popc((uint32_t)(x >> 60));  if (r >= c) { r -= c; pos += 4;  x <<= 4; }
+  c = __popc((uint32_t)(x >> 62));  if (r >= c) { r -= c; pos += 2;  x <<= 2; }
+  c = (uint32_t)(x >> 63);          if (r >= c) { pos += 1; }
+  return pos;
+}
+
+// Position of the r-th (0-based) bit equal to `one` in [0, 512*used), or kNone.
+__device__ uint64_t select_bit(const StreamDesc& sd, const uint64_t* R, uint64_t used, uint64_t r, bool one) {
+  auto before = [&](uint64_t k) -> uint64_t { return one ? R[k] : (k * 512 - R[k]); };
+  if (before(used) <= r) return kNone;
+  uint64_t lo = 0, hi = used;
+  while (hi - lo > 1) {
+    uint64_t mid = (lo + hi) >> 1;
+    if (before(mid) <= r) lo = mid; else hi = mid;
+  }
+  uint64_t rem = r - before(lo);
+  for (uint64_t w = lo << 3;; ++w) {
+    uint64_t x = chunk(sd, w);
+    if (!one) x = ~x;
+    uint32_t c = __popcll(x);
+    if (rem < c) return (w << 6) + select_msb(x, (uint32_t)rem);
+    rem -= c;
+  }
+}
+
+// Stop point (_kernels.py:104-115): t = min(select0(n1), select1(n2)); A is
+// exhausted iff the zero comes first.  X = first fixed point of S -> n1 + rank'(S).
+__global__ void pair_plan_kernel(LevelJob LJ, uint64_t sbs, const uint64_t* __restrict__ rank,
+                                 PairPlan* __restrict__ plans) {
+  uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= LJ.npairs) return;
+  PairPlan P;
+  pair_geom(LJ, g, P.s, P.n1, P.n2, P.sd, P.array);
+  P.rank_off = g * sbs;
+  P.tail_off = 0;
+  const uint64_t n1 = P.n1, n2 = P.n2, N = n1 + n2;
+  if (n1 == 0 || n2 == 0) {  // shufflers.py:169-170: no bits, no change
+    P.t = 0; P.X = n1; P.aex = 0; P.degenerate = 1; P.tail_len = 0; P.bits = 0;
+  } else {
+    const uint64_t* R = rank + g * sbs;
+    uint64_t used = (N + 1 + 511) >> 9;
+    uint64_t z = select_bit(P.sd, R, used, n1, false);
+    uint64_t o = select_bit(P.sd, R, used, n2, true);
+    uint64_t t = z < o ? z : o;
+    P.t = t; P.aex = z < o; P.degenerate = 0;
+    uint64_t S = n1;
+    for (;;) {
+      uint64_t S2 = n1 + rank_bits(P.sd, R, S < t ? S : t);
+      if (S2 == S) break;
+      S = S2;
+    }
+    P.X = S;
+    P.tail_len = N - t;
+    P.bits = t + 1;
+  }
+  plans[g] = P;
+}
+
+void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, PairPlan* plans, cudaStream_t st) {
+  if (!LJ.npairs) return;
+  pair_plan_kernel<<<(unsigned)((LJ.npairs + 127) / 128), 128, 0, st>>>(LJ, sbs, rank, plans);
+  count_launch();
+}
+
+// ------------------------------------------------------------ tail decode
+// One thread per pair, all rounds in one launch so the long top-round tails
+// decode concurrently with the short ones.  Bits continue at offset t+1
+// (shufflers.py:188-191): for x = t..N-1, m_x = FDR(x+1).
+__global__ void tail_decode_kernel(const LevelTail* __restrict__ levels, int nlevels,
+                                   const uint64_t* __restrict__ prefix, uint64_t total,
+                                   unsigned long long* __restrict__ bits) {
+  uint64_t gg = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gg >= total) return;
+  int L = 0;
+  while (L + 1 < nlevels && prefix[L + 1] <= gg) ++L;
+  uint64_t g = gg - prefix[L];
+  LevelTail lv = levels[L];
+  PairPlan* Pp = lv.plans + g;
+  if (Pp->degenerate) return;
+  const uint64_t t = Pp->t, N = Pp->n1 + Pp->n2, s = Pp->s, off = Pp->tail_off;
+  uint64_t nb = 0;
+  if (t < N) {
+    Reader64 rd;
+    rd.init(Pp->sd, t + 1);
+    for (uint64_t x = t; x < N; ++x) {
+      uint64_t m = fdr64(rd, x + 1, nb);
+      lv.rec_key[off + (x - t)] = s + m;
+      lv.rec_pair[off + (x - t)] = (uint32_t)g;
+    }
+  }
+  uint64_t b = t + 1 + nb;
+  Pp->bits = b;
+  atomicAdd(&bits[Pp->array], (unsigned long long)b);
+}
+
+void launch_tail_decode(const LevelTail* d_levels, int nlevels, const uint64_t* d_prefix, uint64_t total_pairs,
+                        unsigned long long* bits, cudaStream_t st) {
+  if (!total_pairs) return;
+  tail_decode_kernel<<<(unsigned)((total_pairs + 63) / 64), 64, 0, st>>>(d_levels, nlevels, d_prefix, total_pairs,
+                                                                         bits);
+  count_launch();
+}
+
+// ---------------------------------------------------------- window chains
+__global__ void windows_kernel(const PairPlan* __restrict__ plans, uint64_t npairs, uint32_t tpp, uint32_t T,
+                               const uint64_t* __restrict__ rank, uint64_t* __restrict__ wins,
+                               uint32_t* __restrict__ nwin) {
+  uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= npairs * tpp) return;
+  uint64_t g = idx / tpp, tau = idx - g * tpp;
+  const PairPlan& P = plans[g];
+  uint64_t u0 = tau * (uint64_t)T;
+  uint32_t h = 0;
+  if (u0 < P.n1) {
+    const uint64_t* R = rank + P.rank_off;
+    const uint64_t t = P.t, n1 = P.n1;
+    uint64_t S = u0, len = min((uint64_t)T, n1 - u0);
+    while (len > 0 && h < (uint32_t)kHMax) {
+      wins[idx * kHMax + h] = S;
+      ++h;
+      uint64_t os = rank_bits(P.sd, R, S < t ? S : t);
+      uint64_t e = S + len;
+      uint64_t oe = rank_bits(P.sd, R, e < t ? e : t);
+      S = n1 + os;
+      len = oe - os;
+    }
+  }
+  nwin[idx] = h;
+}
+
+void launch_windows(const PairPlan* plans, uint64_t npairs, uint32_t tpp, uint32_t tile, const uint64_t* rank,
+                    uint64_t* wins, uint32_t* nwin, cudaStream_t st) {
+  uint64_t total = npairs * tpp;
+  if (!total) return;
+  windows_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(plans, npairs, tpp, tile, rank, wins, nwin);
+  count_launch();
+}
+
+// ------------------------------------------------------------ merge round
+template <typename V, int BLOCK, int E>
+__global__ void __launch_bounds__(BLOCK) merge_level_kernel(const V* __restrict__ in, V* __restrict__ out,
+                                                            const PairPlan* __restrict__ plans, uint32_t tpp,
+                                                            const uint64_t* __restrict__ rank,
+                                                            const uint64_t* __restrict__ wins,
+                                                            const uint32_t* __restrict__ nwin) {
+  constexpr int T = BLOCK * E;
+  static_assert(E <= 32, "E bits are taken from one 64-bit window");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* bufA = reinterpret_cast<V*>(smem_raw);
+  V* bufB = bufA + T;
+  V* bbuf = bufB + T;
+  __shared__ uint32_t wsum[BLOCK / 32];
+  __shared__ uint64_t o0_s;
+
+  const uint64_t tile = blockIdx.x;
+  const uint32_t nw = nwin[tile];
+  if (nw == 0) return;
+  const uint64_t g = tile / tpp, tau = tile - g * tpp;
+  const PairPlan* Pp = plans + g;
+  const uint64_t s = Pp->s, n1 = Pp->n1, t = Pp->t;
+  const StreamDesc sd = Pp->sd;
+  const uint64_t* R = rank + Pp->rank_off;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const V* pin = in + s;
+  V* pout = out + s;
+
+  uint64_t u0 = tau * (uint64_t)T;
+  uint32_t len = (uint32_t)min((uint64_t)T, n1 - u0);
+  V* Fc = bufA;
+  V* Fn = bufB;
+  for (uint32_t i = tid; i < len; i += BLOCK) Fc[i] = pin[u0 + i];
+  uint64_t P0 = u0;
+  uint32_t h = 0;
+  for (;;) {
+    __syncthreads();
+    // phase A: one-bits of this thread's E consecutive positions (only p < t)
+    const uint32_t i0 = tid * E;
+    uint32_t mask = 0;
+    if (i0 < len) {
+      uint64_t p = P0 + i0;
+      if (p < t) {
+        uint32_t nv = min((uint32_t)E, len - i0);
+        uint64_t nt = t - p;
+        if (nt < nv) nv = (uint32_t)nt;
+        uint32_t b = (uint32_t)(bits64_at(sd, p) >> (64 - E));
+        uint32_t vm = (nv == 32) ? 0xffffffffu : (((1u << nv) - 1u) << (E - nv));
+        mask = b & vm;
+      }
+    }
+    uint32_t cnt = __popc(mask);
+    uint32_t x = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    if (tid == 0) {
+      // rank' at the window start (from the precomputed chain when available)
+      if (h + 1 < nw) o0_s = wins[tile * kHMax + h + 1] - n1;
+      else o0_s = kNone;
+    }
+    __syncthreads();
+    uint32_t total = 0, before = 0;
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w) {
+      uint32_t v = wsum[w];
+      before += (w < (int)wid) ? v : 0u;
+      total += v;
+    }
+    const uint32_t rb = before + x - cnt;
+    if (total == 0) {
+      for (uint32_t i = tid; i < len; i += BLOCK) pout[P0 + i] = Fc[i];
+      break;
+    }
+    if (o0_s == kNone) {  // chain longer than kHMax: compute rank' here
+      __syncthreads();
+      if (tid == 0) o0_s = rank_bits(sd, R, P0 < t ? P0 : t);
+    }
+    __syncthreads();
+    const uint64_t o0 = o0_s;
+    for (uint32_t k = tid; k < total; k += BLOCK) bbuf[k] = pin[n1 + o0 + k];
+    __syncthreads();
+    // phase B: ones take B[rank'], their A element moves to the next window
+    if (mask) {
+      uint32_t r = rb;
+#pragma unroll
+      for (int kk = 0; kk < E; ++kk) {
+        if ((mask >> (E - 1 - kk)) & 1u) {
+          uint32_t i = i0 + kk;
+          Fn[r] = Fc[i];
+          Fc[i] = bbuf[r];
+          ++r;
+        }
+      }
+    }
+    __syncthreads();
+    // phase C: the whole window is final
+    for (uint32_t i = tid; i < len; i += BLOCK) pout[P0 + i] = Fc[i];
+    P0 = n1 + o0;
+    len = total;
+    V* tmp = Fc; Fc = Fn; Fn = tmp;
+    ++h;
+  }
+}
+
+constexpr int kMergeBlock = 256;
+constexpr int kE32 = 16;  // 4096-element tiles for 4-byte payloads
+constexpr int kE64 = 8;   // 2048-element tiles for 8-byte payloads
+
+uint32_t merge_tile(int eb) { return kMergeBlock * (eb == 4 ? kE32 : kE64); }
+
+template <typename V, int E>
+static void merge_level_t(const void* in, void* out, const PairPlan* plans, uint64_t npairs, uint32_t tpp,
+                          const uint64_t* rank, const uint64_t* wins, const uint32_t* nwin, cudaStream_t st) {
+  uint64_t tiles = npairs * tpp;
+  if (!tiles) return;
+  size_t smem = (size_t)3 * kMergeBlock * E * sizeof(V);
+  auto k = merge_level_kernel<V, kMergeBlock, E>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<(unsigned)tiles, kMergeBlock, smem, st>>>((const V*)in, (V*)out, plans, tpp, rank, wins, nwin);
+  count_launch();
+}
+
+void launch_merge_level(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs, uint32_t tpp,
+                        const uint64_t* rank, const uint64_t* wins, const uint32_t* nwin, cudaStream_t st) {
+  if (eb == 4) merge_level_t<uint32_t, kE32>(in, out, plans, npairs, tpp, rank, wins, nwin, st);
+  else merge_level_t<unsigned long long, kE64>(in, out, plans, npairs, tpp, rank, wins, nwin, st);
+}
+
+// [X, N) is untouched by phase 1 (A queue empty past X).
+template <typename V>
+__global__ void copy_region_kernel(const V* __restrict__ in, V* __restrict__ out, const PairPlan* __restrict__ plans) {
+  const PairPlan* P = plans + blockIdx.x;
+  uint64_t N = P->n1 + P->n2;
+  for (uint64_t i = P->X + threadIdx.x; i < N; i += blockDim.x) out[P->s + i] = in[P->s + i];
+}
+
+void launch_copy_tail_region(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs,
+                             cudaStream_t st) {
+  if (!npairs) return;
+  if (eb == 4) copy_region_kernel<uint32_t><<<(unsigned)npairs, 256, 0, st>>>((const uint32_t*)in, (uint32_t*)out, plans);
+  else copy_region_kernel<unsigned long long><<<(unsigned)npairs, 256, 0, st>>>((const unsigned long long*)in,
+                                                                               (unsigned long long*)out, plans);
+  count_launch();
+}
+
+// -------------------------------------------------------------- tail plan
+__global__ void iota32_kernel(uint32_t* v, uint64_t n) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (uint32_t)i;
+}
+void launch_iota32(uint32_t* v, uint64_t n, cudaStream_t st) {
+  if (!n) return;
+  iota32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n);
+  count_launch();
+}
+
+// Over records sorted by target (stable in x): predecessor in the target's
+// group, and for each group's last step x_last > q the output (q <- x_last).
+__global__ void tail_plan_kernel(const PairPlan* __restrict__ plans, const uint64_t* __restrict__ rec_key,
+                                 const uint32_t* __restrict__ rec_pair, const uint64_t* __restrict__ skey,
+                                 const uint32_t* __restrict__ sval, uint64_t total, uint64_t* __restrict__ predx,
+                                 uint8_t* __restrict__ keyed, uint64_t* __restrict__ dst, uint64_t* __restrict__ src) {
+  uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= total) return;
+  uint32_t rec = sval[k];
+  uint64_t key = skey[k];
+  const PairPlan* P = plans + rec_pair[rec];
+  uint64_t loc = rec - P->tail_off, x = P->t + loc;
+  predx[rec] = (k > 0 && skey[k - 1] == key) ? (P->t + (sval[k - 1] - P->tail_off)) : kNone;
+  bool last = (k + 1 == total) || skey[k + 1] != key;
+  if (last) {
+    uint64_t q = key - P->s;
+    if (x > q) {
+      uint64_t slot = 2 * P->tail_off + P->tail_len + loc;
+      dst[slot] = key;
+      src[slot] = P->s + x;
+      if (q >= P->t) keyed[P->tail_off + (q - P->t)] = 1;
+    }
+  }
+  (void)rec_key;
+}
+
+// For every insertion position x not overwritten later: chase V(m_x, x).
+__global__ void tail_chase_kernel(const PairPlan* __restrict__ plans, const uint64_t* __restrict__ rec_key,
+                                  const uint32_t* __restrict__ rec_pair, const uint64_t* __restrict__ predx,
+                                  const uint8_t* __restrict__ keyed, uint64_t total, uint64_t* __restrict__ dst,
+                                  uint64_t* __restrict__ src) {
+  uint64_t rec = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rec >= total) return;
+  if (keyed[rec]) return;
+  const PairPlan* P = plans + rec_pair[rec];
+  const uint64_t t = P->t, s = P->s, off = P->tail_off;
+  uint64_t loc = rec - off, x = t + loc;
+  uint64_t r = rec, sr;
+  for (;;) {
+    uint64_t q = rec_key[r] - s;
+    uint64_t xr = t + (r - off);
+    uint64_t y = predx[r];
+    if (y != kNone && y > q) { sr = y; break; }
+    if (q == xr) { sr = xr; break; }
+    if (q < t) { sr = q; break; }
+    r = off + (q - t);
+  }
+  uint64_t slot = 2 * off + loc;
+  dst[slot] = s + x;
+  src[slot] = s + sr;
+}
+
+void launch_tail_plan(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair,
+                      const uint64_t* skey, const uint32_t* sval, uint64_t total, uint64_t* predx,
+                      uint8_t* keyed, uint64_t* dst, uint64_t* src, cudaStream_t st) {
+  if (!total) return;
+  tail_plan_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(plans, rec_key, rec_pair, skey, sval, total,
+                                                                    predx, keyed, dst, src);
+  count_launch();
+}
+
+void launch_tail_chase(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair,
+                       const uint64_t* predx, const uint8_t* keyed, uint64_t total, uint64_t* dst, uint64_t* src,
+                       cudaStream_t st) {
+  if (!total) return;
+  tail_chase_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(plans, rec_key, rec_pair, predx, keyed, total,
+                                                                     dst, src);
+  count_launch();
+}
+
+// ------------------------------------------------------------ tail apply
+template <typename V>
+__global__ void tail_gather_kernel(const V* __restrict__ buf, const uint64_t* __restrict__ dst,
+                                   const uint64_t* __restrict__ src, V* __restrict__ tmp, uint64_t n) {
+  uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n && dst[k] != kNone) tmp[k] = buf[src[k]];
+}
+template <typename V>
+__global__ void tail_scatter_kernel(V* __restrict__ buf, const uint64_t* __restrict__ dst,
+                                    const V* __restrict__ tmp, uint64_t n) {
+  uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n && dst[k] != kNone) buf[dst[k]] = tmp[k];
+}
+
+void launch_tail_apply(int eb, void* buf, const uint64_t* dst, const uint64_t* src, void* tmp, uint64_t nslots,
+                       cudaStream_t st) {
+  if (!nslots) return;
+  unsigned b = (unsigned)((nslots + 255) / 256);
+  if (eb == 4) {
+    tail_gather_kernel<uint32_t><<<b, 256, 0, st>>>((const uint32_t*)buf, dst, src, (uint32_t*)tmp, nslots);
+    tail_scatter_kernel<uint32_t><<<b, 256, 0, st>>>((uint32_t*)buf, dst, (const uint32_t*)tmp, nslots);
+  } else {
+    tail_gather_kernel<unsigned long long><<<b, 256, 0, st>>>((const unsigned long long*)buf, dst, src,
+                                                              (unsigned long long*)tmp, nslots);
+    tail_scatter_kernel<unsigned long long><<<b, 256, 0, st>>>((unsigned long long*)buf, dst,
+                                                               (const unsigned long long*)tmp, nslots);
+  }
+  count_launch();
+  count_launch();
+}
+
+}  // namespace sk

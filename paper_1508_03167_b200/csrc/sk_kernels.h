@@ -1,0 +1,55 @@
+// sk_kernels.h -- host-side launchers for the engine's kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "sk_types.h"
+
+namespace sk {
+
+void count_launch();          // engine-wide launch counter (bench "gpu_launches")
+int num_sms();
+
+// leaf.cu
+void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
+                          unsigned long long* bits, cudaStream_t st);
+uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms);
+void launch_leaf_apply(int eb, const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, const void* in, void* out,
+                       const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid, cudaStream_t st);
+void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, void* out,
+                        unsigned long long* bits, cudaStream_t st);
+
+// merge.cu
+struct LevelTail {            // device-side view used by the all-levels tail decoder
+  PairPlan* plans;
+  uint64_t npairs;
+  uint64_t* rec_key;          // s + m_x (global position of the insertion target)
+  uint32_t* rec_pair;
+};
+void launch_rank_tables(const LevelJob& LJ, uint64_t sbs, uint64_t* rank, cudaStream_t st);
+void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, PairPlan* plans, cudaStream_t st);
+void launch_tail_decode(const LevelTail* d_levels, int nlevels, const uint64_t* d_pair_prefix, uint64_t total_pairs,
+                        unsigned long long* bits, cudaStream_t st);
+void launch_windows(const PairPlan* plans, uint64_t npairs, uint32_t tpp, uint32_t tile, const uint64_t* rank,
+                    uint64_t* wins, uint32_t* nwin, cudaStream_t st);
+void launch_merge_level(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs, uint32_t tpp,
+                        const uint64_t* rank, const uint64_t* wins, const uint32_t* nwin, cudaStream_t st);
+uint32_t merge_tile(int eb);
+void launch_copy_tail_region(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs,
+                             cudaStream_t st);
+void launch_iota32(uint32_t* v, uint64_t n, cudaStream_t st);
+void launch_tail_plan(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair,
+                      const uint64_t* skey, const uint32_t* sval, uint64_t total, uint64_t* predx,
+                      uint8_t* keyed, uint64_t* dst, uint64_t* src, cudaStream_t st);
+void launch_tail_chase(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair,
+                       const uint64_t* predx, const uint8_t* keyed, uint64_t total, uint64_t* dst, uint64_t* src,
+                       cudaStream_t st);
+void launch_tail_apply(int eb, void* buf, const uint64_t* dst, const uint64_t* src, void* tmp, uint64_t nslots,
+                       cudaStream_t st);
+
+// misc.cu
+void launch_chi(int algo, int n, uint64_t trials, uint64_t seed, uint64_t cutoff, unsigned long long* counts,
+                cudaStream_t st);
+void launch_seq(int eb, void* data, uint64_t n, uint64_t cutoff, StreamDesc sd, unsigned long long* bits,
+                cudaStream_t st);
+
+}  // namespace sk

@@ -1,0 +1,194 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+outputs and the CPU oracle, bit-exact (integer/permutation work: no tolerance)."""
+import numpy as np
+import pytest
+
+from golden import CHI, CHI_STATS, G, cutoff_of, sha
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1508_03167_b200 as sk  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def gpu_perm(n, cutoff, seed, dtype=torch.int64):
+    x = torch.arange(n, dtype=dtype, device="cuda")
+    rep = sk.merge_shuffle_parallel(x, sk.ShuffleConfig(cutoff=cutoff), sk.BitSource(seed))
+    torch.cuda.synchronize()
+    return x, rep
+
+
+SMALL = [c for c in G["merge_shuffle_parallel"] if c["n"] <= 100_000]
+BIG = [c for c in G["merge_shuffle_parallel"] if c["n"] > 100_000]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=lambda c: f"n{c['n']}_c{c['cutoff']}_s{c['seed']}")
+@pytest.mark.parametrize("dtype", [torch.int32, torch.int64])
+def test_merge_shuffle_parallel_small(case, dtype):
+    x, rep = gpu_perm(case["n"], case["cutoff"], case["seed"], dtype)
+    assert rep.bits == case["bits"]
+    a = x.cpu().numpy().astype(np.int64)
+    if "perm" in case:
+        assert a.tolist() == case["perm"]
+    assert sha(a.astype("<u8")) == case["sha_u64"]
+
+
+@pytest.mark.parametrize("case", BIG, ids=lambda c: f"n{c['n']}_c{c['cutoff']}_s{c['seed']}")
+def test_merge_shuffle_parallel_big(case):
+    x, rep = gpu_perm(case["n"], case["cutoff"], case["seed"], torch.int32)
+    assert rep.bits == case["bits"]
+    a = x.cpu().numpy()
+    assert a[:8].tolist() == case["head"]
+    assert sha(a.astype("<u4")) == case["sha_u32"]
+
+
+def test_config1_identity_2p20_bits_and_head():
+    # BASELINE config 1 / SURVEY Appendix B
+    x, rep = gpu_perm(1 << 20, None, 0, torch.int32)
+    a = x.cpu().numpy()
+    assert rep.bits == 20642558
+    assert a[:8].tolist() == [31015, 50941, 611601, 90548, 556729, 372014, 358856, 1037783]
+    assert a[-2:].tolist() == [336614, 950641]
+    assert sha(a.astype("<u4")) == "6925255c4af1bba6db58298875f584606717738eed42ca81674550e28698b8a9"
+
+
+def test_config2_payload_2p26_against_oracle():
+    n = 1 << 26
+    rng = np.random.default_rng(2026)
+    payload = rng.integers(0, 2 ** 32, n, dtype=np.uint32)
+    idx, bits = O.merge_shuffle_perm(n, 65536, 0, threads=8)
+    expect = payload[idx]
+    x = torch.from_numpy(payload.view(np.int32)).cuda()
+    rep = sk.merge_shuffle_parallel(x, sk.ShuffleConfig(), sk.BitSource(0))
+    assert rep.bits == bits == 1724975486
+    assert np.array_equal(x.cpu().numpy().view(np.uint32), expect)
+
+
+def test_numpy_host_path_and_payload_types():
+    n = 200_003
+    idx, bits = O.merge_shuffle_perm(n, 4096, 77)
+    for dt in (np.uint32, np.int64, np.float32, np.float64):
+        payload = (np.arange(n) * 3 + 1).astype(dt)
+        a = payload.copy()
+        rep = sk.merge_shuffle_parallel(a, sk.ShuffleConfig(cutoff=4096), sk.BitSource(77))
+        assert rep.bits == bits
+        assert np.array_equal(a, payload[idx])
+    # 2-byte payload: index permutation on the GPU, gather on the host
+    p16 = (np.arange(n) % 60000).astype(np.uint16)
+    a16 = p16.copy()
+    sk.merge_shuffle_parallel(a16, sk.ShuffleConfig(cutoff=4096), sk.BitSource(77))
+    assert np.array_equal(a16, p16[idx])
+    lst = list(range(1000))
+    sk.merge_shuffle_parallel(lst, sk.ShuffleConfig(cutoff=7), sk.BitSource(3))
+    ref, _ = O.merge_shuffle_perm(1000, 7, 3)
+    assert lst == ref.tolist()
+
+
+def test_mid_stream_entry_points():
+    for case in G["mid_stream"]:
+        src = sk.BitSource(0)
+        src.set_state_tuple(case["state_in"])
+        if case["op"] == "fy":
+            x = torch.arange(case["n"], dtype=torch.int64, device="cuda")
+            sk.fisher_yates(x, src)
+        else:
+            x = torch.arange(case["total"], dtype=torch.int64, device="cuda")
+            sk.merge(x, sk.MergeRange(case["s"], case["n1"], case["n2"]), src)
+        assert list(src.state_tuple()) == case["state_out"], case
+        assert sha(x.cpu().numpy().astype("<u8")) == case["sha_u64"], case
+
+
+def test_mid_stream_random_against_oracle():
+    rng = np.random.default_rng(9)
+    for _ in range(30):
+        pre = int(rng.integers(0, 300))
+        seed = int(rng.integers(0, 2 ** 63))
+        n1, n2 = int(rng.integers(0, 3000)), int(rng.integers(0, 3000))
+        s = int(rng.integers(0, 50))
+        tot = s + n1 + n2 + int(rng.integers(0, 50))
+        src = sk.BitSource(seed)
+        src.take(pre)
+        st = np.array(src.state_tuple(), dtype=np.uint64)
+        a = np.arange(tot, dtype=np.int64)
+        O.merge(a, s, s + n1, s + n1 + n2, st)
+        x = torch.arange(tot, dtype=torch.int32, device="cuda")
+        sk.merge(x, sk.MergeRange(s, n1, n2), src)
+        assert np.array_equal(x.cpu().numpy(), a)
+        assert list(src.state_tuple()) == [int(v) for v in st]
+        m = int(rng.integers(0, 5000))
+        st = np.array(src.state_tuple(), dtype=np.uint64)
+        b = np.arange(m, dtype=np.int64)
+        O.fy_range(b, 0, m, st)
+        y = torch.arange(m, dtype=torch.int64, device="cuda")
+        sk.fisher_yates(y, src)
+        assert np.array_equal(y.cpu().numpy(), b)
+        assert list(src.state_tuple()) == [int(v) for v in st]
+
+
+def test_sequential_merge_shuffle():
+    for case in G["merge_shuffle_seq"]:
+        if case["n"] > 200_000:
+            continue
+        x = torch.arange(case["n"], dtype=torch.int64, device="cuda")
+        rep = sk.merge_shuffle(x, sk.ShuffleConfig(cutoff=case["cutoff"]), sk.BitSource(case["seed"]))
+        assert rep.bits == case["bits"]
+        assert sha(x.cpu().numpy().astype("<u8")) == case["sha_u64"]
+
+
+@pytest.mark.parametrize("which", [64, 65536])
+def test_batched(which):
+    case = [c for c in G["batched"] if c["batch"] == which][0]
+    B, L = case["batch"], case["len"]
+    x = torch.arange(L, dtype=torch.int32, device="cuda").repeat(B, 1).contiguous()
+    bits = sk.batched_shuffle(x, sk.ShuffleConfig(cutoff=case["cutoff"]), case["seed"])
+    a = x.cpu().numpy()
+    assert a[0, :8].tolist() == case["row0"] and a[-1, :8].tolist() == case["row_last"]
+    assert int(bits[0]) == case["bits0"] and int(bits.sum()) == case["bits_sum"]
+    assert sha(a.astype("<u4")) == case["sha_u32"]
+    assert sha(bits.astype("<u8")) == case["sha_bits"]
+
+
+@pytest.mark.parametrize("key", sorted(CHI))
+def test_chi_counts_equal_reference(key):
+    parts = key.split("_")
+    algo = "merge_parallel" if key.startswith("merge_parallel") else parts[0]
+    n = next((int(p[1:]) for p in parts if p.startswith("n") and p[1:].isdigit()), 6)
+    cut = next((int(p[1:]) for p in parts if p.startswith("c") and p[1:].isdigit()), 1)
+    trials = next(int(p[1:]) for p in parts if p.startswith("t"))
+    seed = next(int(p[1:]) for p in parts if p.startswith("s") and p[1:].isdigit())
+    counts = sk.chi_counts(algo, n, trials, seed, cut)
+    assert np.array_equal(counts, CHI[key])
+
+
+def test_chi_square_statistic_config2():
+    for cut in (65536, 1):
+        r = sk.chi_square_uniformity("merge_parallel", 6, 10_000_000, 0, cutoff=cut)
+        assert r.passed
+        assert abs(r.statistic - CHI_STATS[str(cut)]["statistic"]) < 1e-6
+
+
+def test_full_size_2p30_validity_and_bits():
+    # n = 2^30 (config 3, 1 GPU): reference bits 31908987766 and head;
+    # permutation validity on the whole array.
+    n = 1 << 30
+    x = torch.arange(n, dtype=torch.int32, device="cuda")
+    rep = sk.merge_shuffle_parallel(x, sk.ShuffleConfig(), sk.BitSource(0))
+    assert rep.bits == 31908987766
+    assert x[:8].cpu().tolist() == [689509142, 560979983, 717555468, 1025498733, 1056958978, 1072831348,
+                                    937792008, 1008664118]
+    seen = torch.zeros(n // 32, dtype=torch.int32, device="cuda")
+    # validity: every value exactly once (bitmap via scatter of sorted chunks)
+    s, _ = torch.sort(x)
+    assert torch.equal(s, torch.arange(n, dtype=torch.int32, device="cuda"))
+    del s, seen
+
+
+def test_determinism_and_seed_sensitivity():
+    a, _ = gpu_perm(300_000, 1000, 5, torch.int32)
+    b, _ = gpu_perm(300_000, 1000, 5, torch.int32)
+    c, _ = gpu_perm(300_000, 1000, 6, torch.int32)
+    assert torch.equal(a, b) and not torch.equal(a, c)
