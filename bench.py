@@ -1,0 +1,310 @@
+"""Benchmark: MergeShuffle of n = 2^30 uint32 uniform-random payload (BASELINE
+config 3 at 1 GPU), metric Gelem/s permuted.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full merge_shuffle_parallel (leaf Fisher-Yates + 14 merge rounds,
+bit-exact with the reference) of the resident 4 GiB array.  Timing: CUDA
+events on the launching stream, barrier + synchronize on both sides, max over
+ranks.  The array (4 GiB) is 32x the L2, so no flush is needed between steps.
+
+Extra keys: roofline (dominant kernel = the merge-round window kernel),
+cpu_baseline (the C oracle port on the host cores, bounded sample), e2e
+(through the C ABI host entry with pinned host buffers, H2D+D2H inside the
+timed region), gpu_launches, clocks.
+
+--impl reference: the reference's CPU path.  The reference is a Python/numba
+package that cannot travel to the GPU box, so its C restatement (oracle/,
+parity-pinned to the reference's goldens) runs with all host threads on a
+bounded sample of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gelem/s permuted (uint32, n=2^30) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "Gelem/s"
+LOG2N = 30
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--log2n", type=int, default=LOG2N)
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_init(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(seconds_target=12.0, log2n=26):
+    """The oracle port on all host threads, a bounded sample of the workload:
+    merge_shuffle_tasked on 2^log2n int64 indices (same leaf size and schedule)
+    plus the uint32 payload gather, repeated until ~seconds_target."""
+    import numpy as np
+    from oracle import oracle as O
+    O.build()
+    cores = cpu_cores()
+    n = 1 << log2n
+    payload = np.random.default_rng(0).integers(0, 2 ** 32, n, dtype=np.uint32)
+    idx = np.arange(n, dtype=np.int64)
+    O.merge_shuffle_tasked(idx, 65536, 0, cores)  # warm (page-in)
+    times = []
+    t_all = time.perf_counter()
+    while True:
+        idx = np.arange(n, dtype=np.int64)
+        t0 = time.perf_counter()
+        O.merge_shuffle_tasked(idx, 65536, 0, cores)
+        _ = payload[idx]
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > seconds_target or len(times) >= 20:
+            break
+    med = statistics.median(times)
+    return {"value": round(n / med / 1e9, 6), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle merge_shuffle_tasked on 2^{log2n} int64 indices + uint32 payload gather, "
+                      f"{len(times)} runs, median {med:.3f}s, {cores} threads ({cpu_model()})"}
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_from_profile():
+    p = os.path.join(ROOT, "profiles", "merge_kernel_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        b = oracle_sample(seconds_target=4.0 if i < args.warmup else 8.0)
+        if i >= args.warmup:
+            steps.append(b)
+        base = b
+    vals = [s["value"] for s in steps]
+    v = statistics.median(vals)
+    n = 1 << args.log2n
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(n / (v * 1e9) * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"merge_shuffle_parallel n=2^{args.log2n} uint32 uniform payload, cutoff 65536",
+                       "n": n, "elem_bytes": 4, "cutoff": 65536, "seed": 0, "parallelism": "host threads"},
+            "cpu_baseline": {**base, "value": v},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1508_03167_b200 as sk
+    from paper_1508_03167_b200 import _lib
+    lib = _lib.load()
+    n = 1 << args.log2n
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    x = torch.randint(-2 ** 31, 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    bits = ctypes.c_uint64(0)
+
+    def step():
+        _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), 4, n, 65536, 0, None, sp))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # one checked step: bits equal the reference's for this n (seed 0)
+    _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), 4, n, 65536, 0, ctypes.byref(bits), sp))
+
+    lib.sk_profile_enable(1)
+    l0 = lib.sk_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = lib.sk_launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    stage_ms = (ctypes.c_double * 5)()
+    stage_l = (ctypes.c_uint64 * 5)()
+    lib.sk_profile_read(stage_ms, stage_l, 5)
+    lib.sk_profile_enable(0)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * n / (ms_per_step * 1e-3) / 1e9
+
+    # roofline: merge-round window kernel; algorithmic bytes per launch = one
+    # read + one write of the array (2 * 4 B * n)
+    merge_ms = stage_ms[2]
+    merge_launches = max(1, stage_l[2])
+    per_launch_ms = merge_ms / merge_launches
+    alg_bytes = 2 * 4 * n
+    achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+    tr = traffic_from_profile()
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": tr.get("bytes_per_launch") if tr else None,
+            "peak_source": peak_kind, "kernel": "merge_level_kernel (one merge round)",
+            "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": round(per_launch_ms, 4),
+            "stage_ms_per_step": {k: round(stage_ms[i] / args.steps, 4) for i, k in
+                                  enumerate(["leaf_decode", "leaf_apply", "merge_window", "identity+tail",
+                                             "final_copy"])},
+            "passes_per_step": round(ms_per_step / (alg_bytes / (peak * 1e9) * 1e3), 2)}
+
+    # e2e through the C ABI host entry (pinned host buffers, H2D + D2H inside)
+    e2e = None
+    if args.e2e_steps > 0:
+        host = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        host.copy_(x.cpu())
+        hp = ctypes.c_void_p(host.data_ptr())
+        _lib.check(lib.sk_merge_shuffle_parallel_host(hp, 4, n, 65536, 0, None, sp))  # warm
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            _lib.check(lib.sk_merge_shuffle_parallel_host(hp, 4, n, 65536, 0, ctypes.byref(bits), sp))
+        el = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([el], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": round(world * n * args.e2e_steps / el / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n + 8,
+               "path": "sk_merge_shuffle_parallel_host (C ABI), pinned host buffer"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample()
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                "data": "synthetic: uniform-random 32-bit payload (torch.Generator seed 1234+rank)",
+                "config": {"workload": f"merge_shuffle_parallel n=2^{args.log2n} uint32 uniform payload, "
+                                       "cutoff 65536 (16384 leaves, 14 merge rounds), seed 0",
+                           "n_per_gpu": n, "elem_bytes": 4, "cutoff": 65536, "seed": 0,
+                           "parallelism": "replicas" if world > 1 else "1 GPU",
+                           "l2": "input 4 GiB >> 126 MB L2; no flush needed",
+                           "bits_per_shuffle": int(bits.value)},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

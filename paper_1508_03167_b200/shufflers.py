@@ -170,7 +170,11 @@ class _Device:
     def finish(self):
         res = self.dev
         if self.perm_mode:
-            res = self.payload[self.dev]
+            torch = self.torch
+            pl = self.payload
+            sview = {1: torch.int8, 2: torch.int16}.get(pl.element_size())
+            src = pl.view(sview) if sview is not None else pl
+            res = src[self.dev].view(pl.dtype)
             if self.kind == "cuda":
                 self.payload.copy_(res)
                 return
