@@ -126,8 +126,10 @@ struct LevelBufs {
   uint32_t tpp = 0;
   uint64_t* rank = nullptr;
   PairPlan* plans = nullptr;
-  uint64_t* wins = nullptr;
+  WinRec* wins = nullptr;
   uint32_t* nwin = nullptr;
+  uint32_t* flag_list = nullptr;   // tiles for the sequential-window kernel
+  uint32_t* flag_count = nullptr;
   // tails
   uint64_t total = 0;
   uint64_t* rec_key = nullptr;
@@ -169,15 +171,20 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
   for (auto& L : lv) {
     L.rank = A.alloc<uint64_t>(L.npairs * L.sbs, ps);
     L.plans = A.alloc<PairPlan>(L.npairs, ps);
-    L.wins = A.alloc<uint64_t>(L.npairs * L.tpp * kHMax, ps);
+    L.wins = A.alloc<WinRec>(L.npairs * L.tpp * kHMax, ps);
     L.nwin = A.alloc<uint32_t>(L.npairs * L.tpp, ps);
+    L.flag_list = A.alloc<uint32_t>(L.npairs * L.tpp, ps);
+    L.flag_count = A.alloc<uint32_t>(1, ps);
+    CK(cudaMemsetAsync(L.flag_count, 0, 4, ps));
   }
   for (auto& L : lv) {
     launch_rank_tables(L.LJ, L.sbs, L.rank, ps);
     launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, ps);
-    launch_windows(L.plans, L.npairs, L.tpp, T, L.rank, L.wins, L.nwin, ps);
+    launch_windows(L.plans, L.npairs, L.tpp, T, L.rank, L.wins, L.nwin, L.flag_list, L.flag_count, ps);
   }
   CK(cudaGetLastError());
+  // (the host synchronization below also orders the data stream's merge
+  // kernels after these window chains)
   // tail sizes -> host
   uint64_t tot_pairs = 0;
   std::vector<uint64_t> pprefix(nl + 1, 0);
@@ -272,7 +279,8 @@ static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* oth
   for (auto& L : lv) {
     {
       StageTimer tm(2, st);
-      launch_merge_level(eb, cur, other, L.plans, L.npairs, L.tpp, L.rank, L.wins, L.nwin, st);
+      launch_merge_level(eb, cur, other, L.plans, L.npairs, L.tpp, L.rank, L.wins, L.nwin, L.flag_list, L.flag_count,
+                         st);
     }
     {
       StageTimer tm(3, st);
@@ -315,7 +323,7 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
   std::vector<LevelBufs> lv = make_levels(J, eb);
   void* scratch = A.alloc<unsigned char>(ntot * eb, st);
   const uint64_t nleaves = J.batch * J.q;
-  const uint64_t mmax = (J.len >> J.c) + 1;
+  const uint64_t mmax = (J.len + J.q - 1) >> J.c;  // largest leaf: ceil(len / q)
   ExplicitTask E0{};
   try {
     uint16_t* draws = nullptr;
@@ -325,7 +333,7 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
     if (fast_leaf) {
       draws = A.alloc<uint16_t>(ntot, st);
       grid = leaf_apply_grid(nleaves, (uint32_t)mmax, num_sms());
-      lscr = A.alloc<uint16_t>((uint64_t)grid * 2 * mmax, st);
+      lscr = A.alloc<uint16_t>((uint64_t)grid * 3 * mmax, st);
     }
     fork_side(st, ps);
     {
@@ -420,7 +428,8 @@ static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t
     // kernels address elements by absolute index; shift the scratch base so
     // index j lands on scratch[0].
     void* out_base = (void*)(scratch - j * eb);
-    launch_merge_level(eb, data, out_base, L.plans, 1, L.tpp, L.rank, L.wins, L.nwin, st);
+    launch_merge_level(eb, data, out_base, L.plans, 1, L.tpp, L.rank, L.wins, L.nwin, L.flag_list, L.flag_count,
+                       st);
     launch_copy_tail_region(eb, data, out_base, L.plans, 1, st);
     CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
     launch_tail_apply(eb, out_base, L.dst, L.src, L.tmp, 2 * L.total, st);
@@ -453,7 +462,7 @@ static void run_single_leaf(int eb, void* data, uint64_t lo, uint64_t hi, const 
     if (m <= 65536) {
       uint16_t* draws = A.alloc<uint16_t>(m, st);
       unsigned char* scratch = A.alloc<unsigned char>(m * eb, st);
-      uint16_t* lscr = A.alloc<uint16_t>(2 * m, st);
+      uint16_t* lscr = A.alloc<uint16_t>(3 * m, st);
       // absolute-index kernels: shift bases so index lo lands on element 0
       launch_leaf_decode16(J, E, 1, draws - lo, d_bits, st);
       launch_leaf_apply(eb, J, E, 1, data, (void*)(scratch - lo * eb), draws - lo, lscr, (uint32_t)m, 1, st);

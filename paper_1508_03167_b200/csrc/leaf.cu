@@ -2,7 +2,7 @@
 // shufflers.py:137-155, leaf tasks shufflers.py:268-278).
 //
 // Two kernels:
-//  * leaf_decode_kernel: one thread per leaf decodes the m-1 fast-dice-roller
+//  * leaf_decode16_kernel: one lane per leaf decodes the m-1 fast-dice-roller
 //    draws j_i (i = m-1 .. 1) of its substream.  This is the only serial part:
 //    draws are variable-length so draw k's bit offset depends on draws < k.
 //  * leaf_apply_kernel: one CTA per leaf applies the m-1 swaps in parallel via
@@ -11,28 +11,94 @@
 //      final[i] = orig[W(N(i))] (or orig[j_i] if none), final[0] = orig[W(0)],
 //      W(x) = W(H(x)) if H(x) exists else x.
 //    Steps are bucketed by target with a shared-memory counting sort (16-bit
-//    counters, two per 32-bit word, atomics in smem), buckets are tiny so each is
-//    insertion-sorted by its owner, then every output gathers through the chain.
+//    counters, two per 32-bit word, atomics in smem); each step's bucket
+//    successor is found by a min-scan of its (tiny) bucket, then every output
+//    gathers through the chain.
 #include <algorithm>
 #include "sk_kernels.h"
 
 namespace sk {
 
-template <typename DT>
-__global__ void __launch_bounds__(128) leaf_decode_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
-                                                          DT* __restrict__ draws,
-                                                          unsigned long long* __restrict__ bits) {
-  uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= nleaves) return;
-  LeafDesc L = leaf_desc(J, E, g);
-  uint64_t m = L.hi - L.lo;
-  if (m < 2) return;
-  Reader32 rd;
-  rd.init(L.sd, 0);
-  uint64_t nb = 0;
-  DT* dr = draws + L.lo;
-  for (uint32_t i = (uint32_t)m - 1; i >= 1; --i) dr[i] = (DT)fdr32(rd, i + 1, nb);
-  atomicAdd(&bits[L.array], (unsigned long long)nb);
+// One lane per leaf, one fast-dice-roller *iteration* per loop trip (so lanes
+// whose draws reject do not stall the others), bits served from a per-lane ring
+// of 32-bit half-words in shared memory that the warp tops up in bulk (uniform
+// mix64 work, no per-lane divergent word generation).  Bounds <= 65536, so one
+// iteration takes k <= 16 bits and TRIPS=16 iterations take at most 9 halves.
+constexpr int kDecodeTrips = 16;
+__global__ void __launch_bounds__(32) leaf_decode16_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
+                                                           uint16_t* __restrict__ draws,
+                                                           unsigned long long* __restrict__ bits) {
+  __shared__ uint32_t ring[16][32];
+  const uint32_t lane = threadIdx.x;
+  const uint64_t g = (uint64_t)blockIdx.x * 32 + lane;
+  LeafDesc L;
+  uint32_t m = 0;
+  if (g < nleaves) {
+    L = leaf_desc(J, E, g);
+    m = (uint32_t)(L.hi - L.lo);
+  } else {
+    L.lo = 0; L.hi = 0; L.array = 0; L.sd = fresh_stream(0);
+  }
+  uint32_t i = m >= 2 ? m - 1 : 0;
+  uint16_t* dr = draws + L.lo;
+  uint64_t gw = 0;
+  uint32_t wr = 0, rd = 0;
+  if (i) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      uint64_t x = chunk(L.sd, gw++);
+      ring[wr & 15][lane] = (uint32_t)(x >> 32);
+      ring[(wr + 1) & 15][lane] = (uint32_t)x;
+      wr += 2;
+    }
+  }
+  uint32_t A = ring[0][lane], B = ring[1][lane], C = ring[2][lane];
+  rd = 3;
+  uint32_t pos = 0;
+  uint32_t b = i + 1, bm1 = i, lb = 31 - __clz(i | 1), v = 1, c = 0;
+  uint32_t nb = 0;
+  while (__any_sync(0xffffffffu, i != 0)) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (i != 0 && wr - rd <= 14) {
+        uint64_t x = chunk(L.sd, gw++);
+        ring[wr & 15][lane] = (uint32_t)(x >> 32);
+        ring[(wr + 1) & 15][lane] = (uint32_t)x;
+        wr += 2;
+      }
+    }
+#pragma unroll 4
+    for (int tr = 0; tr < kDecodeTrips; ++tr) {
+      // branch-free trip: lanes that finished (i == 0) keep their state
+      const bool act = i != 0;
+      uint32_t lv = 31 - __clz(v);
+      uint32_t k = lb - lv;
+      k += ((v << k) <= bm1) ? 1u : 0u;
+      k = act ? k : 0u;
+      uint32_t x = __funnelshift_l(B, A, pos);
+      uint32_t r = k ? (x >> (32 - k)) : 0u;
+      uint32_t cc = (c << k) | r;
+      pos += k;
+      nb += k;
+      const bool acc = act && cc < b;
+      if (acc) dr[i] = (uint16_t)cc;
+      const uint32_t i_old = i;
+      c = acc ? 0u : cc - b;
+      v = acc ? 1u : (v << k) - b;
+      i = acc ? i_old - 1 : i_old;          // next step, bound b = i + 1
+      b = acc ? i_old : b;
+      bm1 = acc ? i_old - 1 : bm1;
+      lb = acc ? 31 - __clz((i_old - 1) | 1) : lb;
+      const uint32_t nxt = ring[rd & 15][lane];
+      const bool cross = pos >= 32;
+      pos = cross ? pos - 32 : pos;
+      A = cross ? B : A;
+      B = cross ? C : B;
+      C = cross ? nxt : C;
+      rd += cross ? 1u : 0u;
+    }
+  }
+  if (m >= 2) atomicAdd(&bits[L.array], (unsigned long long)nb);
 }
 
 // Warp-segmented exclusive scan over `m` 16-bit counters packed in smem.
@@ -73,10 +139,10 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
   extern __shared__ uint32_t sh[];
   __shared__ uint32_t warp_tot[BLOCK / 32];
   uint16_t* c16 = reinterpret_cast<uint16_t*>(sh);
-  uint16_t* bucket = scratch + (uint64_t)blockIdx.x * 2 * mmax;
+  uint16_t* bucket = scratch + (uint64_t)blockIdx.x * 3 * mmax;
   uint16_t* Nn = bucket + mmax;
+  uint16_t* Hg = Nn + mmax;
   const uint32_t tid = threadIdx.x;
-  const uint32_t lane = tid & 31, wid = tid >> 5, nw = BLOCK / 32;
 
   for (uint64_t g = blockIdx.x; g < nleaves; g += gridDim.x) {
     LeafDesc L = leaf_desc(J, E, g);
@@ -108,44 +174,29 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
       bucket[(old >> sh16) & 0xFFFFu] = (uint16_t)s;
     }
     __syncthreads();
-    // 4. per target: sort bucket, successor links N, first-step-above H (in place of c16)
-    {
-      const uint32_t S = (((m + nw - 1) / nw) + 31) & ~31u;
-      const uint32_t b0 = wid * S, b1 = min(m, b0 + S);
-      uint32_t carry = (b0 > 0 && b0 < m) ? c16[b0 - 1] : 0;  // end of bucket b0-1
-      __syncthreads();
-      for (uint32_t base = b0; base < b1; base += 32) {
-        uint32_t p = base + lane;
-        uint32_t en = (p < b1) ? c16[p] : 0;
-        uint32_t st = __shfl_up_sync(0xffffffffu, en, 1);
-        if (lane == 0) st = carry;
-        carry = __shfl_sync(0xffffffffu, en, 31);
-        if (p < b1) {
-          uint32_t len = en - st;
-          uint32_t H = 0;
-          if (len) {
-            if (len >= 2) {  // insertion sort (buckets hold ~1 entry on average)
-              for (uint32_t a = st + 1; a < en; ++a) {
-                uint16_t v = bucket[a];
-                uint32_t b = a;
-                while (b > st && bucket[b - 1] > v) { bucket[b] = bucket[b - 1]; --b; }
-                bucket[b] = v;
-              }
-            }
-            uint32_t prev = bucket[st];
-            for (uint32_t a = st + 1; a < en; ++a) {
-              uint32_t cur = bucket[a];
-              Nn[prev] = (uint16_t)cur;
-              prev = cur;
-            }
-            Nn[prev] = 0;
-            uint32_t f0 = bucket[st];
-            H = (f0 > p) ? f0 : (len >= 2 ? (uint32_t)bucket[st + 1] : 0u);
-          }
-          c16[p] = (uint16_t)H;
-        }
+    // 4. successor links without sorting: N(s) = min{s' > s in bucket(j_s)},
+    //    H(x) = min{s' > x in bucket(x)}; buckets hold ~1 step on average.
+    for (uint32_t s = 1 + tid; s < m; s += BLOCK) {
+      uint32_t p = dr[s];
+      uint32_t en = c16[p], st = p ? c16[p - 1] : 0u;
+      uint32_t best = 0xFFFFFFFFu;
+      for (uint32_t a = st; a < en; ++a) {
+        uint32_t v = bucket[a];
+        if (v > s && v < best) best = v;
       }
+      Nn[s] = (uint16_t)(best == 0xFFFFFFFFu ? 0u : best);
     }
+    for (uint32_t x = tid; x < m; x += BLOCK) {
+      uint32_t en = c16[x], st = x ? c16[x - 1] : 0u;
+      uint32_t best = 0xFFFFFFFFu;
+      for (uint32_t a = st; a < en; ++a) {
+        uint32_t v = bucket[a];
+        if (v > x && v < best) best = v;
+      }
+      Hg[x] = (uint16_t)(best == 0xFFFFFFFFu ? 0u : best);
+    }
+    __syncthreads();
+    for (uint32_t x = tid; x < m; x += BLOCK) c16[x] = Hg[x];
     __syncthreads();
     // 5. chase and gather
     for (uint32_t i = tid; i < m; i += BLOCK) {
@@ -195,8 +246,8 @@ __global__ void leaf_serial_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
                           unsigned long long* bits, cudaStream_t st) {
   if (!nleaves) return;
-  unsigned blocks = (unsigned)((nleaves + 127) / 128);
-  leaf_decode_kernel<uint16_t><<<blocks, 128, 0, st>>>(J, E, nleaves, draws, bits);
+  unsigned blocks = (unsigned)((nleaves + 31) / 32);
+  leaf_decode16_kernel<<<blocks, 32, 0, st>>>(J, E, nleaves, draws, bits);
   count_launch();
 }
 

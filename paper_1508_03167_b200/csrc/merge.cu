@@ -18,6 +18,7 @@
 // Everything except the element movement depends only on (schedule, seed), so
 // the rank tables, stop points, window chains, tail draws and tail plans are
 // built on a side stream while the leaf stage runs.
+#include <algorithm>
 #include "sk_kernels.h"
 
 namespace sk {
@@ -193,9 +194,14 @@ void launch_tail_decode(const LevelTail* d_levels, int nlevels, const uint64_t* 
 }
 
 // ---------------------------------------------------------- window chains
+// Window chain of every tile.  nwin = number of windows (the chain ends with an
+// empty window), or kHMax+1+stored when the chain is longer than kHMax or the
+// tile's carried elements exceed the parallel kernel's buffer (cap): such tiles
+// take the sequential-window kernel.
 __global__ void windows_kernel(const PairPlan* __restrict__ plans, uint64_t npairs, uint32_t tpp, uint32_t T,
-                               const uint64_t* __restrict__ rank, uint64_t* __restrict__ wins,
-                               uint32_t* __restrict__ nwin) {
+                               const uint64_t* __restrict__ rank, WinRec* __restrict__ wins,
+                               uint32_t* __restrict__ nwin, uint64_t cap, uint32_t* __restrict__ flag_list,
+                               uint32_t* __restrict__ flag_count) {
   uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= npairs * tpp) return;
   uint64_t g = idx / tpp, tau = idx - g * tpp;
@@ -205,9 +211,10 @@ __global__ void windows_kernel(const PairPlan* __restrict__ plans, uint64_t npai
   if (u0 < P.n1) {
     const uint64_t* R = rank + P.rank_off;
     const uint64_t t = P.t, n1 = P.n1;
-    uint64_t S = u0, len = min((uint64_t)T, n1 - u0);
+    uint64_t S = u0, len = min((uint64_t)T, n1 - u0), carried = 0;
     while (len > 0 && h < (uint32_t)kHMax) {
-      wins[idx * kHMax + h] = S;
+      wins[idx * kHMax + h] = WinRec{S, len};
+      if (h) carried += len;
       ++h;
       uint64_t os = rank_bits(P.sd, R, S < t ? S : t);
       uint64_t e = S + len;
@@ -215,38 +222,109 @@ __global__ void windows_kernel(const PairPlan* __restrict__ plans, uint64_t npai
       S = n1 + os;
       len = oe - os;
     }
+    if (len > 0 || carried > cap) {  // flagged; stored count kept
+      h += kHMax + 1;
+      flag_list[atomicAdd(flag_count, 1u)] = (uint32_t)idx;
+    }
   }
   nwin[idx] = h;
 }
 
 void launch_windows(const PairPlan* plans, uint64_t npairs, uint32_t tpp, uint32_t tile, const uint64_t* rank,
-                    uint64_t* wins, uint32_t* nwin, cudaStream_t st) {
+                    WinRec* wins, uint32_t* nwin, uint32_t* flag_list, uint32_t* flag_count, cudaStream_t st) {
   uint64_t total = npairs * tpp;
   if (!total) return;
-  windows_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(plans, npairs, tpp, tile, rank, wins, nwin);
+  windows_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(plans, npairs, tpp, tile, rank, wins, nwin,
+                                                                  merge_carry_cap(tile), flag_list, flag_count);
   count_launch();
 }
 
 // ------------------------------------------------------------ merge round
-template <typename V, int BLOCK, int E>
-__global__ void __launch_bounds__(BLOCK) merge_level_kernel(const V* __restrict__ in, V* __restrict__ out,
-                                                            const PairPlan* __restrict__ plans, uint32_t tpp,
-                                                            const uint64_t* __restrict__ rank,
-                                                            const uint64_t* __restrict__ wins,
-                                                            const uint32_t* __restrict__ nwin) {
+// One-bit masks of a warp's rounds: lane l < E covers window positions
+// [seg0 + 32l, seg0 + 32l + 32); only positions < len and < t count.
+template <int E>
+__device__ __forceinline__ uint32_t round_mask(const StreamDesc& sd, uint64_t P0, uint32_t seg0, uint32_t len,
+                                               uint64_t t, uint32_t lane) {
+  uint32_t mword = 0;
+  if (lane < (uint32_t)E) {
+    uint32_t i = seg0 + lane * 32;
+    if (i < len) {
+      uint64_t p = P0 + i;
+      if (p < t) {
+        uint32_t nv = min(32u, len - i);
+        uint64_t nt = t - p;
+        if (nt < nv) nv = (uint32_t)nt;
+        uint32_t b = (uint32_t)(bits64_at(sd, p) >> 32);
+        mword = (nv == 32) ? b : (b & ~(0xffffffffu >> nv));
+      }
+    }
+  }
+  return mword;
+}
+
+// Phase B for one warp: ones take B[rank'] (from bbuf), their A element moves
+// to the next window's buffer.  Lane-consecutive positions: conflict-free smem.
+template <typename V, int E>
+__device__ __forceinline__ void move_ones(V* Fc, V* Fn, const V* bbuf, uint32_t mword, uint32_t round_base,
+                                          uint32_t before, uint32_t seg0, uint32_t len, uint32_t lane) {
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    if (seg0 + 32 * k >= len) break;
+    uint32_t m = __shfl_sync(0xffffffffu, mword, k);
+    uint32_t rb = __shfl_sync(0xffffffffu, round_base, k);
+    if ((m >> (31 - lane)) & 1u) {
+      uint32_t i = seg0 + 32 * k + lane;
+      uint32_t r = before + rb + __popc(m & ~(0xffffffffu >> lane));
+      Fn[r] = Fc[i];
+      Fc[i] = bbuf[r];
+    }
+  }
+}
+
+// Split a run of `cnt` elements at global address `src` into an unaligned
+// head, a 16-byte aligned body (TMA bulk copy) and a tail; `off` is chosen so
+// the body lands 16-byte aligned in shared memory.
+template <typename V>
+struct RunSplit {
+  uint32_t head, body, tail;  // elements
+};
+template <typename V>
+__device__ __forceinline__ RunSplit<V> split_run(const V* src, uint32_t cnt) {
+  constexpr uint32_t VPA = 16 / sizeof(V);
+  uint32_t mis = (uint32_t)((uintptr_t)src & 15);
+  uint32_t head = ((16 - mis) & 15) / sizeof(V);
+  RunSplit<V> r;
+  if (head >= cnt) { r.head = cnt; r.body = 0; r.tail = 0; return r; }
+  r.head = head;
+  r.body = ((cnt - head) / VPA) * VPA;
+  r.tail = cnt - head - r.body;
+  return r;
+}
+
+// Sequential-window fallback (tiles flagged by windows_kernel): windows are
+// walked one after the other, B runs of the stored windows prefetched by TMA.
+template <typename V, int BLOCK, int E, int BCAP>
+__device__ __noinline__ void merge_seq_tile(const uint64_t tile, const V* __restrict__ in, V* __restrict__ out,
+                                            const PairPlan* __restrict__ plans, uint32_t tpp,
+                                            const uint64_t* __restrict__ rank, const WinRec* __restrict__ wins,
+                                            const uint32_t* __restrict__ nwin, unsigned char* smem_raw) {
   constexpr int T = BLOCK * E;
+  constexpr uint32_t VPA = 16 / sizeof(V);
+  constexpr uint32_t WSPAN = 32 * E;  // positions per warp
+  constexpr uint32_t NOPF = 0xFFFFFFFFu;
   static_assert(E <= 32, "E bits are taken from one 64-bit window");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* bufA = reinterpret_cast<V*>(smem_raw);
-  V* bufB = bufA + T;
-  V* bbuf = bufB + T;
+  V* bufA = reinterpret_cast<V*>(smem_raw);   // T + VPA (tile, misaligned start)
+  V* bufB = bufA + T + VPA;                   // T
+  V* bbuf = bufB + T;                         // BCAP: every window's B run
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ WinRec sw[kHMax];
+  __shared__ uint32_t boff[kHMax];
   __shared__ uint32_t wsum[BLOCK / 32];
+  __shared__ uint32_t a_off_s;
   __shared__ uint64_t o0_s;
 
-  const uint64_t tile = blockIdx.x;
-  const uint32_t nw = nwin[tile];
-  if (nw == 0) return;
-  const uint64_t g = tile / tpp, tau = tile - g * tpp;
+  const uint32_t nw = nwin[tile] - (kHMax + 1);  // stored windows; later ones computed here
+  const uint64_t g = tile / tpp;
   const PairPlan* Pp = plans + g;
   const uint64_t s = Pp->s, n1 = Pp->n1, t = Pp->t;
   const StreamDesc sd = Pp->sd;
@@ -255,41 +333,77 @@ __global__ void __launch_bounds__(BLOCK) merge_level_kernel(const V* __restrict_
   const V* pin = in + s;
   V* pout = out + s;
 
-  uint64_t u0 = tau * (uint64_t)T;
-  uint32_t len = (uint32_t)min((uint64_t)T, n1 - u0);
-  V* Fc = bufA;
-  V* Fn = bufB;
-  for (uint32_t i = tid; i < len; i += BLOCK) Fc[i] = pin[u0 + i];
-  uint64_t P0 = u0;
-  uint32_t h = 0;
-  for (;;) {
-    __syncthreads();
-    // phase A: one-bits of this thread's E consecutive positions (only p < t)
-    const uint32_t i0 = tid * E;
-    uint32_t mask = 0;
-    if (i0 < len) {
-      uint64_t p = P0 + i0;
-      if (p < t) {
-        uint32_t nv = min((uint32_t)E, len - i0);
-        uint64_t nt = t - p;
-        if (nt < nv) nv = (uint32_t)nt;
-        uint32_t b = (uint32_t)(bits64_at(sd, p) >> (64 - E));
-        uint32_t vm = (nv == 32) ? 0xffffffffu : (((1u << nv) - 1u) << (E - nv));
-        mask = b & vm;
+  // ---- prefetch: A tile + the B run of every stored window, one TMA batch
+  if (tid < nw) sw[tid] = wins[tile * kHMax + tid];
+  if (tid == 0) mbar_init(&mbar, 1);
+  __syncthreads();
+  const uint64_t u0 = sw[0].start;
+  uint32_t len = (uint32_t)sw[0].len;
+  if (tid == 0) {
+    RunSplit<V> ra = split_run<V>(pin + u0, len);
+    uint32_t aoff = (VPA - (ra.head % VPA)) % VPA;
+    a_off_s = aoff;
+    uint32_t tx = ra.body * sizeof(V);
+    uint32_t cur = 0;
+    for (uint32_t h = 0; h + 1 < nw; ++h) {
+      uint32_t cnt = (uint32_t)sw[h + 1].len;
+      RunSplit<V> rb = split_run<V>(pin + sw[h + 1].start, cnt);
+      uint32_t off = ((cur + rb.head + VPA - 1) / VPA) * VPA - rb.head;
+      if (off + cnt <= (uint32_t)BCAP) {
+        boff[h] = off;
+        cur = off + cnt;
+        tx += rb.body * sizeof(V);
+      } else {
+        boff[h] = NOPF;
       }
     }
-    uint32_t cnt = __popc(mask);
+    mbar_arrive_expect_tx(&mbar, tx);
+    if (ra.body) bulk_g2s(bufA + aoff + ra.head, pin + u0 + ra.head, ra.body * sizeof(V), &mbar);
+    for (uint32_t h = 0; h + 1 < nw; ++h) {
+      if (boff[h] == NOPF) continue;
+      uint32_t cnt = (uint32_t)sw[h + 1].len;
+      RunSplit<V> rb = split_run<V>(pin + sw[h + 1].start, cnt);
+      if (rb.body)
+        bulk_g2s(bbuf + boff[h] + rb.head, pin + sw[h + 1].start + rb.head, rb.body * sizeof(V), &mbar);
+    }
+  }
+  __syncthreads();
+  if (wid == 1) {  // unaligned heads/tails with plain loads
+    for (uint32_t h = lane; h < nw; h += 32) {
+      const V* src;
+      V* dst;
+      uint32_t cnt;
+      if (h == 0) {
+        src = pin + u0; dst = bufA + a_off_s; cnt = len;
+      } else {
+        if (boff[h - 1] == NOPF) continue;
+        src = pin + sw[h].start; dst = bbuf + boff[h - 1]; cnt = (uint32_t)sw[h].len;
+      }
+      RunSplit<V> r = split_run<V>(src, cnt);
+      for (uint32_t k = 0; k < r.head; ++k) dst[k] = src[k];
+      for (uint32_t k = r.head + r.body; k < cnt; ++k) dst[k] = src[k];
+    }
+  }
+  __syncthreads();
+  mbar_wait(&mbar, 0);
+
+  V* Fc = bufA + a_off_s;
+  V* Fn = bufB;
+  uint64_t P0 = u0;
+  uint32_t h = 0;
+  bool done = false;
+  // ---- block mode: windows wider than one warp's span
+  while (len > WSPAN) {
+    const uint32_t seg0 = wid * WSPAN;
+    uint32_t mword = round_mask<E>(sd, P0, seg0, len, t, lane);
+    const uint32_t cnt = __popc(mword);
     uint32_t x = cnt;
     for (int o = 1; o < 32; o <<= 1) {
       uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= (uint32_t)o) x += y;
     }
+    const uint32_t round_base = x - cnt;
     if (lane == 31) wsum[wid] = x;
-    if (tid == 0) {
-      // rank' at the window start (from the precomputed chain when available)
-      if (h + 1 < nw) o0_s = wins[tile * kHMax + h + 1] - n1;
-      else o0_s = kNone;
-    }
     __syncthreads();
     uint32_t total = 0, before = 0;
 #pragma unroll
@@ -298,39 +412,273 @@ __global__ void __launch_bounds__(BLOCK) merge_level_kernel(const V* __restrict_
       before += (w < (int)wid) ? v : 0u;
       total += v;
     }
-    const uint32_t rb = before + x - cnt;
     if (total == 0) {
       for (uint32_t i = tid; i < len; i += BLOCK) pout[P0 + i] = Fc[i];
+      done = true;
       break;
     }
-    if (o0_s == kNone) {  // chain longer than kHMax: compute rank' here
-      __syncthreads();
+    uint64_t o0;
+    const V* bsrc;
+    if (h + 1 < nw) {
+      o0 = sw[h + 1].start - n1;
+      bsrc = (boff[h] != NOPF) ? (const V*)(bbuf + boff[h]) : pin + n1 + o0;
+    } else {  // chain longer than kHMax: rank' computed here, B read from global
       if (tid == 0) o0_s = rank_bits(sd, R, P0 < t ? P0 : t);
+      __syncthreads();
+      o0 = o0_s;
+      bsrc = pin + n1 + o0;
     }
+    if (seg0 < len) move_ones<V, E>(Fc, Fn, bsrc, mword, round_base, before, seg0, len, lane);
     __syncthreads();
-    const uint64_t o0 = o0_s;
-    for (uint32_t k = tid; k < total; k += BLOCK) bbuf[k] = pin[n1 + o0 + k];
-    __syncthreads();
-    // phase B: ones take B[rank'], their A element moves to the next window
-    if (mask) {
-      uint32_t r = rb;
-#pragma unroll
-      for (int kk = 0; kk < E; ++kk) {
-        if ((mask >> (E - 1 - kk)) & 1u) {
-          uint32_t i = i0 + kk;
-          Fn[r] = Fc[i];
-          Fc[i] = bbuf[r];
-          ++r;
-        }
-      }
-    }
-    __syncthreads();
-    // phase C: the whole window is final
     for (uint32_t i = tid; i < len; i += BLOCK) pout[P0 + i] = Fc[i];
+    P0 = n1 + o0;
+    len = total;
+    // the next window's first barrier orders these reads of Fc before the
+    // next phase B rewrites it as Fn
+    V* tmp = Fc; Fc = Fn; Fn = tmp;
+    ++h;
+  }
+  if (done) return;
+  __syncthreads();
+  if (wid != 0) return;
+  // ---- warp mode: the remaining (geometrically shrinking) windows, warp 0 only
+  for (;;) {
+    uint32_t mword = round_mask<E>(sd, P0, 0, len, t, lane);
+    const uint32_t cnt = __popc(mword);
+    uint32_t x = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    const uint32_t round_base = x - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
+    if (total == 0) {
+      for (uint32_t i = lane; i < len; i += 32) pout[P0 + i] = Fc[i];
+      return;
+    }
+    uint64_t o0;
+    const V* bsrc;
+    if (h + 1 < nw) {
+      o0 = sw[h + 1].start - n1;
+      bsrc = (boff[h] != NOPF) ? (const V*)(bbuf + boff[h]) : pin + n1 + o0;
+    } else {
+      o0 = rank_bits(sd, R, P0 < t ? P0 : t);
+      bsrc = pin + n1 + o0;
+    }
+    move_ones<V, E>(Fc, Fn, bsrc, mword, round_base, 0, 0, len, lane);
+    __syncwarp();
+    for (uint32_t i = lane; i < len; i += 32) pout[P0 + i] = Fc[i];
     P0 = n1 + o0;
     len = total;
     V* tmp = Fc; Fc = Fn; Fn = tmp;
     ++h;
+    __syncwarp();
+  }
+}
+
+template <typename V, int BLOCK, int E, int BCAP>
+__global__ void __launch_bounds__(BLOCK) merge_level_seq_kernel(const V* __restrict__ in, V* __restrict__ out,
+                                                                const PairPlan* __restrict__ plans, uint32_t tpp,
+                                                                const uint64_t* __restrict__ rank,
+                                                                const WinRec* __restrict__ wins,
+                                                                const uint32_t* __restrict__ nwin,
+                                                                const uint32_t* __restrict__ flag_list,
+                                                                const uint32_t* __restrict__ flag_count) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t nf = *flag_count;
+  for (uint32_t k = blockIdx.x; k < nf; k += gridDim.x) {
+    merge_seq_tile<V, BLOCK, E, BCAP>(flag_list[k], in, out, plans, tpp, rank, wins, nwin, smem_raw);
+    __syncthreads();
+  }
+}
+
+// All windows of a tile at once.  The plan fixes every window's position range,
+// so every window's bits are known up front: window h's k-th one-bit carries
+// the element at sel_h[k] (its position in window h) into window h+1, position
+// k.  A zero at position i of window h therefore outputs
+// A[sel_0[sel_1[... sel_{h-1}[i]]]] (mean chain length 0.5), a one outputs
+// window h's k-th B element.  Phases (each over all windows, block-parallel):
+// TMA prefetch -> bit masks + segmented rank scan -> sel scatter -> outputs.
+template <typename V, int BLOCK, int T, int BCAP>
+__global__ void __launch_bounds__(BLOCK) merge_level_kernel(const V* __restrict__ in, V* __restrict__ out,
+                                                            const PairPlan* __restrict__ plans, uint32_t tpp,
+                                                            const WinRec* __restrict__ wins,
+                                                            const uint32_t* __restrict__ nwin) {
+  constexpr uint32_t VPA = 16 / sizeof(V);
+  constexpr uint32_t NOPF = 0xFFFFFFFFu;
+  constexpr int MAXCH = (T + BCAP) / 32 + kHMax;  // 32-position chunks over all windows
+  constexpr int CPT = (MAXCH + BLOCK - 1) / BLOCK;
+  constexpr int BBUF = BCAP + 2 * VPA * kHMax;      // B runs incl. alignment padding
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  V* bufA = reinterpret_cast<V*>(smem_raw);    // T + VPA: the A tile
+  V* bbuf = bufA + T + VPA;                    // BBUF: B run of every window
+  uint16_t* sel = reinterpret_cast<uint16_t*>(bbuf + BBUF);  // BCAP
+  uint32_t* cmask = reinterpret_cast<uint32_t*>(sel + BCAP);  // MAXCH
+  uint32_t* cpre = cmask + MAXCH;                             // MAXCH
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ WinRec sw[kHMax];
+  __shared__ uint32_t boff[kHMax];
+  __shared__ uint32_t cbase[kHMax + 1];   // first chunk of window h
+  __shared__ uint32_t sbase[kHMax + 1];   // first sel slot of window h
+  __shared__ uint8_t cwin[MAXCH];         // window of each chunk
+  __shared__ uint32_t wsum[BLOCK / 32];
+  __shared__ uint32_t a_off_s;
+
+  const uint64_t tile = blockIdx.x;
+  const uint32_t nw = nwin[tile];
+  if (nw == 0 || nw > (uint32_t)kHMax) return;
+  const PairPlan* Pp = plans + tile / tpp;
+  const uint64_t s = Pp->s, t = Pp->t;
+  const StreamDesc sd = Pp->sd;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const V* pin = in + s;
+  V* pout = out + s;
+
+  if (tid < nw) sw[tid] = wins[tile * kHMax + tid];
+  if (tid == 0) mbar_init(&mbar, 1);
+  __syncthreads();
+  if (wid == 0) {
+    // warp 0 lays out the runs (lane owns windows lane and lane+32): chunk
+    // bases, sel bases and padded B-run slots by warp scans, then every lane
+    // issues its own TMA bulk copies and plain head/tail loads.
+    uint32_t carry_c = 0, carry_s = 0, carry_b = 0, tx = 0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t h = lane + 32 * q;
+      const bool valid = h < nw;
+      const uint32_t lh = valid ? (uint32_t)sw[h].len : 0u;
+      const uint32_t nchh = (lh + 31) / 32;
+      const uint32_t cnt = (valid && h + 1 < nw) ? (uint32_t)sw[h + 1].len : 0u;
+      RunSplit<V> rb = split_run<V>(pin + (cnt ? sw[h + 1].start : 0), cnt);
+      const uint32_t slot = cnt ? ((cnt + 2 * VPA - 1) / VPA) * VPA : 0u;
+      uint32_t xc = nchh, xs = cnt, xb = slot;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t yc = __shfl_up_sync(0xffffffffu, xc, o);
+        uint32_t ys = __shfl_up_sync(0xffffffffu, xs, o);
+        uint32_t yb = __shfl_up_sync(0xffffffffu, xb, o);
+        if (lane >= (uint32_t)o) { xc += yc; xs += ys; xb += yb; }
+      }
+      const uint32_t cb = carry_c + xc - nchh, sb = carry_s + xs - cnt, bs = carry_b + xb - slot;
+      if (valid) {
+        cbase[h] = cb;
+        sbase[h] = sb;
+        uint32_t off = NOPF;
+        if (cnt && bs + slot <= (uint32_t)BBUF) {
+          off = bs + (VPA - (rb.head % VPA)) % VPA;
+          tx += rb.body * sizeof(V);
+        }
+        boff[h] = off;
+        if (h == nw - 1) { cbase[nw] = cb + nchh; sbase[nw] = sb + cnt; }
+      }
+      carry_c += __shfl_sync(0xffffffffu, xc, 31);
+      carry_s += __shfl_sync(0xffffffffu, xs, 31);
+      carry_b += __shfl_sync(0xffffffffu, xb, 31);
+    }
+    const uint32_t len0 = (uint32_t)sw[0].len;
+    RunSplit<V> ra = split_run<V>(pin + sw[0].start, len0);
+    const uint32_t aoff = (VPA - (ra.head % VPA)) % VPA;
+    if (lane == 0) tx += ra.body * sizeof(V);
+    for (int o = 16; o; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
+    if (lane == 0) {
+      a_off_s = aoff;
+      mbar_arrive_expect_tx(&mbar, tx);
+      if (ra.body) bulk_g2s(bufA + aoff + ra.head, pin + sw[0].start + ra.head, ra.body * sizeof(V), &mbar);
+    }
+    __syncwarp();
+    if (lane < ra.head) bufA[aoff + lane] = pin[sw[0].start + lane];
+    for (uint32_t k = ra.head + ra.body + lane; k < len0; k += 32) bufA[aoff + k] = pin[sw[0].start + k];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t h = lane + 32 * q;
+      if (h + 1 < nw && boff[h] != NOPF) {
+        const uint32_t cnt = (uint32_t)sw[h + 1].len;
+        const V* src = pin + sw[h + 1].start;
+        V* dst = bbuf + boff[h];
+        RunSplit<V> rb = split_run<V>(src, cnt);
+        if (rb.body) bulk_g2s(dst + rb.head, src + rb.head, rb.body * sizeof(V), &mbar);
+        for (uint32_t k = 0; k < rb.head; ++k) dst[k] = src[k];
+        for (uint32_t k = rb.head + rb.body; k < cnt; ++k) dst[k] = src[k];
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t nch = cbase[nw];
+  // ---- bit masks of every chunk (positions >= t count as zeros) + rank scan
+  uint32_t csum[CPT];
+  uint32_t tsum = 0;
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    uint32_t c = tid * CPT + q;
+    uint32_t m = 0;
+    if (c < nch) {
+      uint32_t lo = 0, hi = nw;  // window of chunk c: cbase[lo] <= c < cbase[lo+1]
+      while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (cbase[mid] <= c) lo = mid; else hi = mid;
+      }
+      const uint32_t h = lo;
+      cwin[c] = (uint8_t)h;
+      uint32_t i0 = (c - cbase[h]) * 32;
+      uint64_t p = sw[h].start + i0;
+      if (p < t) {
+        uint32_t nv = min(32u, (uint32_t)sw[h].len - i0);
+        uint64_t nt = t - p;
+        if (nt < nv) nv = (uint32_t)nt;
+        uint32_t b = (uint32_t)(bits64_at(sd, p) >> 32);
+        m = (nv == 32) ? b : (b & ~(0xffffffffu >> nv));
+      }
+      cmask[c] = m;
+    }
+    csum[q] = __popc(m);
+    tsum += csum[q];
+  }
+  uint32_t x = tsum;
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  uint32_t before = 0;
+#pragma unroll
+  for (int w = 0; w < BLOCK / 32; ++w) before += (w < (int)wid) ? wsum[w] : 0u;
+  uint32_t run = before + x - tsum;
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    uint32_t c = tid * CPT + q;
+    if (c < nch) cpre[c] = run;   // ones before chunk c over all windows
+    run += csum[q];
+  }
+  __syncthreads();
+  // ---- sel scatter: window h's r-th one sits at position i of window h
+  for (uint32_t c = wid; c < nch; c += BLOCK / 32) {
+    uint32_t m = cmask[c];
+    if ((m >> (31 - lane)) & 1u) {
+      uint32_t h = cwin[c];
+      uint32_t r = cpre[c] - cpre[cbase[h]] + __popc(m & ~(0xffffffffu >> lane));
+      sel[sbase[h] + r] = (uint16_t)((c - cbase[h]) * 32 + lane);
+    }
+  }
+  __syncthreads();
+  mbar_wait(&mbar, 0);
+  // ---- outputs
+  const V* Fa = bufA + a_off_s;
+  for (uint32_t c = wid; c < nch; c += BLOCK / 32) {
+    uint32_t h = cwin[c];
+    uint32_t i = (c - cbase[h]) * 32 + lane;
+    uint32_t lh = (uint32_t)sw[h].len;
+    if (i >= lh) continue;
+    uint32_t m = cmask[c];
+    V val;
+    if ((m >> (31 - lane)) & 1u) {
+      uint32_t r = cpre[c] - cpre[cbase[h]] + __popc(m & ~(0xffffffffu >> lane));
+      val = (boff[h] != NOPF) ? bbuf[boff[h] + r] : pin[sw[h + 1].start + r];
+    } else {
+      uint32_t r = i;
+      for (int k = (int)h - 1; k >= 0; --k) r = sel[sbase[k] + r];
+      val = Fa[r];
+    }
+    pout[sw[h].start + i] = val;
   }
 }
 
@@ -340,22 +688,41 @@ constexpr int kE64 = 8;   // 2048-element tiles for 8-byte payloads
 
 uint32_t merge_tile(int eb) { return kMergeBlock * (eb == 4 ? kE32 : kE64); }
 
+uint64_t merge_carry_cap(uint32_t tile) { return tile + tile / 4; }
+
 template <typename V, int E>
 static void merge_level_t(const void* in, void* out, const PairPlan* plans, uint64_t npairs, uint32_t tpp,
-                          const uint64_t* rank, const uint64_t* wins, const uint32_t* nwin, cudaStream_t st) {
+                          const uint64_t* rank, const WinRec* wins, const uint32_t* nwin, const uint32_t* flag_list,
+                          const uint32_t* flag_count, cudaStream_t st) {
   uint64_t tiles = npairs * tpp;
   if (!tiles) return;
-  size_t smem = (size_t)3 * kMergeBlock * E * sizeof(V);
-  auto k = merge_level_kernel<V, kMergeBlock, E>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<(unsigned)tiles, kMergeBlock, smem, st>>>((const V*)in, (V*)out, plans, tpp, rank, wins, nwin);
-  count_launch();
+  constexpr int T = kMergeBlock * E;
+  constexpr int BCAP = T + T / 4;  // == merge_carry_cap(T)
+  constexpr int MAXCH = (T + BCAP) / 32 + kHMax;
+  {
+    constexpr int BBUF = BCAP + 2 * (16 / sizeof(V)) * kHMax;
+    size_t smem = (size_t)(T + 16 / sizeof(V) + BBUF) * sizeof(V) + (size_t)BCAP * 2 + (size_t)MAXCH * 8;
+    auto k = merge_level_kernel<V, kMergeBlock, T, BCAP>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<(unsigned)tiles, kMergeBlock, smem, st>>>((const V*)in, (V*)out, plans, tpp, wins, nwin);
+    count_launch();
+  }
+  {
+    size_t smem = (size_t)(T + 16 / sizeof(V) + T + BCAP) * sizeof(V);
+    auto k = merge_level_seq_kernel<V, kMergeBlock, E, BCAP>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    unsigned g = (unsigned)std::min<uint64_t>(tiles, (uint64_t)num_sms() * 2);
+    k<<<g, kMergeBlock, smem, st>>>((const V*)in, (V*)out, plans, tpp, rank, wins, nwin, flag_list, flag_count);
+    count_launch();
+  }
 }
 
 void launch_merge_level(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs, uint32_t tpp,
-                        const uint64_t* rank, const uint64_t* wins, const uint32_t* nwin, cudaStream_t st) {
-  if (eb == 4) merge_level_t<uint32_t, kE32>(in, out, plans, npairs, tpp, rank, wins, nwin, st);
-  else merge_level_t<unsigned long long, kE64>(in, out, plans, npairs, tpp, rank, wins, nwin, st);
+                        const uint64_t* rank, const WinRec* wins, const uint32_t* nwin, const uint32_t* flag_list,
+                        const uint32_t* flag_count, cudaStream_t st) {
+  if (eb == 4) merge_level_t<uint32_t, kE32>(in, out, plans, npairs, tpp, rank, wins, nwin, flag_list, flag_count, st);
+  else merge_level_t<unsigned long long, kE64>(in, out, plans, npairs, tpp, rank, wins, nwin, flag_list, flag_count,
+                                               st);
 }
 
 // [X, N) is untouched by phase 1 (A queue empty past X).

@@ -30,10 +30,12 @@ void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, Pa
 void launch_tail_decode(const LevelTail* d_levels, int nlevels, const uint64_t* d_pair_prefix, uint64_t total_pairs,
                         unsigned long long* bits, cudaStream_t st);
 void launch_windows(const PairPlan* plans, uint64_t npairs, uint32_t tpp, uint32_t tile, const uint64_t* rank,
-                    uint64_t* wins, uint32_t* nwin, cudaStream_t st);
+                    WinRec* wins, uint32_t* nwin, uint32_t* flag_list, uint32_t* flag_count, cudaStream_t st);
 void launch_merge_level(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs, uint32_t tpp,
-                        const uint64_t* rank, const uint64_t* wins, const uint32_t* nwin, cudaStream_t st);
+                        const uint64_t* rank, const WinRec* wins, const uint32_t* nwin, const uint32_t* flag_list,
+                        const uint32_t* flag_count, cudaStream_t st);
 uint32_t merge_tile(int eb);
+uint64_t merge_carry_cap(uint32_t tile);
 void launch_copy_tail_region(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs,
                              cudaStream_t st);
 void launch_iota32(uint32_t* v, uint64_t n, cudaStream_t st);

@@ -47,7 +47,13 @@ struct PairPlan {
   uint32_t degenerate;  // n1 == 0 || n2 == 0: no bits, identity
 };
 
-constexpr int kHMax = 40;            // stored window starts per merge tile
+constexpr int kHMax = 40;            // stored windows per merge tile
+
+// Window h of a merge tile: positions [start, start+len) of its pair.
+struct WinRec {
+  uint64_t start;
+  uint64_t len;
+};
 constexpr uint64_t kNone = ~0ULL;
 
 // Leaf descriptor computed on device from an ArrayJob (or the explicit task).
