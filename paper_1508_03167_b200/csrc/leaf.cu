@@ -11,8 +11,8 @@
 //      final[i] = orig[W(N(i))] (or orig[j_i] if none), final[0] = orig[W(0)],
 //      W(x) = W(H(x)) if H(x) exists else x.
 //    Steps are bucketed by target with a shared-memory counting sort (16-bit
-//    counters, two per 32-bit word, atomics in smem); each step's bucket
-//    successor is found by a min-scan of its (tiny) bucket, then every output
+//    counters, two per 32-bit word, atomics in smem); each bucket (~1 step on
+//    average) is sorted in registers by the lane owning the target, then every output
 //    gathers through the chain.
 #include <algorithm>
 #include "sk_kernels.h"
@@ -25,6 +25,14 @@ namespace sk {
 // mix64 work, no per-lane divergent word generation).  Bounds <= 65536, so one
 // iteration takes k <= 16 bits and TRIPS=16 iterations take at most 9 halves.
 constexpr int kDecodeTrips = 16;
+
+template <bool FRESH>
+__device__ __forceinline__ uint64_t leaf_word(const StreamDesc& sd, uint64_t w) {
+  if (FRESH) return mix64(sd.state + (w + 1) * GOLDEN);  // fresh substream: no prefix
+  return chunk(sd, w);
+}
+
+template <bool FRESH>
 __global__ void __launch_bounds__(32) leaf_decode16_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
                                                            uint16_t* __restrict__ draws,
                                                            unsigned long long* __restrict__ bits) {
@@ -39,29 +47,31 @@ __global__ void __launch_bounds__(32) leaf_decode16_kernel(ArrayJob J, ExplicitT
   } else {
     L.lo = 0; L.hi = 0; L.array = 0; L.sd = fresh_stream(0);
   }
-  uint32_t i = m >= 2 ? m - 1 : 0;
+  uint32_t i = m >= 2 ? m - 1 : 0;   // current step; its bound is i + 1
   uint16_t* dr = draws + L.lo;
   uint64_t gw = 0;
-  uint32_t wr = 0, rd = 0;
+  uint32_t wr = 0;
   if (i) {
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-      uint64_t x = chunk(L.sd, gw++);
+      uint64_t x = leaf_word<FRESH>(L.sd, gw++);
       ring[wr & 15][lane] = (uint32_t)(x >> 32);
       ring[(wr + 1) & 15][lane] = (uint32_t)x;
       wr += 2;
     }
   }
-  uint32_t A = ring[0][lane], B = ring[1][lane], C = ring[2][lane];
-  rd = 3;
+  // four-half window A|B|C|D: the extraction uses A|B; C and D are already
+  // loaded so a ring read has two word crossings of slack before its use
+  uint32_t A = ring[0][lane], B = ring[1][lane], C = ring[2][lane], D = ring[3][lane];
+  uint32_t rd = 4;
   uint32_t pos = 0;
-  uint32_t b = i + 1, bm1 = i, lb = 31 - __clz(i | 1), v = 1, c = 0;
+  uint32_t lb = 31 - __clz(i | 1), v = 1, c = 0;
   uint32_t nb = 0;
   while (__any_sync(0xffffffffu, i != 0)) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (i != 0 && wr - rd <= 14) {
-        uint64_t x = chunk(L.sd, gw++);
+        uint64_t x = leaf_word<FRESH>(L.sd, gw++);
         ring[wr & 15][lane] = (uint32_t)(x >> 32);
         ring[(wr + 1) & 15][lane] = (uint32_t)x;
         wr += 2;
@@ -69,32 +79,31 @@ __global__ void __launch_bounds__(32) leaf_decode16_kernel(ArrayJob J, ExplicitT
     }
 #pragma unroll 4
     for (int tr = 0; tr < kDecodeTrips; ++tr) {
-      // branch-free trip: lanes that finished (i == 0) keep their state
+      // one fast-dice-roller iteration (_kernels.py:71-82); finished lanes
+      // (i == 0) compute harmlessly but never store or advance
       const bool act = i != 0;
-      uint32_t lv = 31 - __clz(v);
-      uint32_t k = lb - lv;
-      k += ((v << k) <= bm1) ? 1u : 0u;
-      k = act ? k : 0u;
-      uint32_t x = __funnelshift_l(B, A, pos);
-      uint32_t r = k ? (x >> (32 - k)) : 0u;
-      uint32_t cc = (c << k) | r;
-      pos += k;
-      nb += k;
+      const uint32_t b = i + 1;
+      uint32_t k = lb - (31 - __clz(v));
+      k += ((v << k) < b) ? 1u : 0u;
+      const uint32_t x = __funnelshift_l(B, A, pos);
+      const uint32_t cc = (c << k) | (x >> (32 - k));
       const bool acc = act && cc < b;
-      if (acc) dr[i] = (uint16_t)cc;
-      const uint32_t i_old = i;
       c = acc ? 0u : cc - b;
       v = acc ? 1u : (v << k) - b;
-      i = acc ? i_old - 1 : i_old;          // next step, bound b = i + 1
-      b = acc ? i_old : b;
-      bm1 = acc ? i_old - 1 : bm1;
-      lb = acc ? 31 - __clz((i_old - 1) | 1) : lb;
-      const uint32_t nxt = ring[rd & 15][lane];
+      if (acc) dr[i] = (uint16_t)cc;
+      // floor(log2(i-1)) drops by one exactly when i is a power of two
+      lb = (acc && i == (1u << lb)) ? lb - 1 : lb;
+      i = acc ? i - 1 : i;
+      const uint32_t kk = act ? k : 0u;
+      nb += kk;
+      pos += kk;
       const bool cross = pos >= 32;
+      const uint32_t nxt = ring[rd & 15][lane];
       pos = cross ? pos - 32 : pos;
       A = cross ? B : A;
       B = cross ? C : B;
-      C = cross ? nxt : C;
+      C = cross ? D : C;
+      D = cross ? nxt : D;
       rd += cross ? 1u : 0u;
     }
   }
@@ -131,6 +140,43 @@ __device__ __forceinline__ void scan_counts16(uint16_t* c16, uint32_t m, uint32_
   }
 }
 
+// compare-exchange (ascending)
+__device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
+  uint32_t lo = min(a, b), hi = max(a, b);
+  a = lo; b = hi;
+}
+
+// Load a bucket of len <= N entries into registers (missing ones = 0xFFFF)
+// and sort ascending with a bitonic network (compile-time indices only).
+template <int N>
+__device__ __forceinline__ void sort_bucket(uint32_t (&e)[N], const uint16_t* b, uint32_t len) {
+#pragma unroll
+  for (int a = 0; a < N; ++a) e[a] = ((uint32_t)a < len) ? (uint32_t)b[a] : 0xFFFFu;
+#pragma unroll
+  for (int k2 = 2; k2 <= N; k2 <<= 1) {
+#pragma unroll
+    for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        const int b2 = a ^ j2;
+        if (b2 > a) {
+          if ((a & k2) == 0) cswap(e[a], e[b2]);
+          else cswap(e[b2], e[a]);
+        }
+      }
+    }
+  }
+}
+
+// successor links of a sorted bucket: N(e[a]) = e[a+1], N(last) = none
+template <int N>
+__device__ __forceinline__ void link_bucket(const uint32_t (&e)[N], uint32_t len, uint16_t* Nn) {
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    if ((uint32_t)a < len) Nn[e[a]] = ((uint32_t)a + 1 < len) ? (uint16_t)e[(a + 1) % N] : (uint16_t)0;
+  }
+}
+
 template <typename V, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
                                                            const V* __restrict__ in, V* __restrict__ out,
@@ -139,77 +185,108 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
   extern __shared__ uint32_t sh[];
   __shared__ uint32_t warp_tot[BLOCK / 32];
   uint16_t* c16 = reinterpret_cast<uint16_t*>(sh);
-  uint16_t* bucket = scratch + (uint64_t)blockIdx.x * 3 * mmax;
-  uint16_t* Nn = bucket + mmax;
-  uint16_t* Hg = Nn + mmax;
+  const uint32_t ms = (mmax + 1) & ~1u;  // even stride: Hg is copied as 32-bit words
+  uint16_t* bucket = scratch + (uint64_t)blockIdx.x * 3 * ms;
+  uint16_t* Nn = bucket + ms;
+  uint16_t* Hg = Nn + ms;
   const uint32_t tid = threadIdx.x;
 
   for (uint64_t g = blockIdx.x; g < nleaves; g += gridDim.x) {
-    LeafDesc L = leaf_desc(J, E, g);
+    const LeafDesc L = leaf_desc(J, E, g);
     const uint32_t m = (uint32_t)(L.hi - L.lo);
-    const V* src_in = in + L.lo;
-    V* dst = out + L.lo;
+    const V* __restrict__ src_in = in + L.lo;
+    V* __restrict__ dst = out + L.lo;
     if (m < 2) {
       if (m == 1 && tid == 0) dst[0] = src_in[0];
       continue;
     }
-    const uint16_t* dr = draws + L.lo;
+    const uint16_t* __restrict__ dr = draws + L.lo;
     const uint32_t nwords = (m + 1) >> 1;
     for (uint32_t w = tid; w < nwords; w += BLOCK) sh[w] = 0;
     __syncthreads();
-    // 1. histogram of targets
+    // 1. histogram of targets (steps s = 1 .. m-1; dr[0] is unused)
+#pragma unroll 4
     for (uint32_t s = 1 + tid; s < m; s += BLOCK) {
-      uint32_t j = dr[s];
-      atomicAdd(&sh[j >> 1], 1u << ((j & 1) * 16));
+      const uint32_t j = dr[s];
+      atomicAdd(&sh[j >> 1], 1u << ((j & 1) << 4));
     }
     __syncthreads();
     // 2. bucket starts
     scan_counts16(c16, m, warp_tot);
     __syncthreads();
-    // 3. scatter step ids into their target's bucket
+    // 3. scatter step ids into their target's bucket (order inside a bucket is arbitrary)
+#pragma unroll 4
     for (uint32_t s = 1 + tid; s < m; s += BLOCK) {
-      uint32_t j = dr[s];
-      uint32_t sh16 = (j & 1) * 16;
-      uint32_t old = atomicAdd(&sh[j >> 1], 1u << sh16);
+      const uint32_t j = dr[s];
+      const uint32_t sh16 = (j & 1) << 4;
+      const uint32_t old = atomicAdd(&sh[j >> 1], 1u << sh16);
       bucket[(old >> sh16) & 0xFFFFu] = (uint16_t)s;
     }
     __syncthreads();
-    // 4. successor links without sorting: N(s) = min{s' > s in bucket(j_s)},
-    //    H(x) = min{s' > x in bucket(x)}; buckets hold ~1 step on average.
-    for (uint32_t s = 1 + tid; s < m; s += BLOCK) {
-      uint32_t p = dr[s];
-      uint32_t en = c16[p], st = p ? c16[p - 1] : 0u;
-      uint32_t best = 0xFFFFFFFFu;
-      for (uint32_t a = st; a < en; ++a) {
-        uint32_t v = bucket[a];
-        if (v > s && v < best) best = v;
+    // 4. per target p (lane-consecutive targets, warps interleaved so the long
+    //    buckets of targets near 0 -- mean length ln(m/p) -- spread over all
+    //    warps): sort the bucket in registers (networks for <= 4, 8, 16, 32
+    //    entries), link successors N, and write H(p) = first step > p
+    //    targeting p to Hg (copied over c16 after the barrier).
+    for (uint32_t p = tid; p < m; p += BLOCK) {
+      const uint32_t en = c16[p];
+      const uint32_t st = p ? (uint32_t)c16[p - 1] : 0u;
+      const uint32_t len = en - st;
+      uint32_t H = 0;
+      if (len == 1) {
+        const uint32_t e0 = bucket[st];
+        Nn[e0] = 0;
+        H = (e0 > p) ? e0 : 0u;
+      } else if (len >= 2 && len <= 4) {
+        uint32_t e[4];
+        sort_bucket<4>(e, bucket + st, len);
+        link_bucket<4>(e, len, Nn);
+        H = (e[0] > p) ? e[0] : e[1];
+      } else if (len > 4 && len <= 8) {
+        uint32_t e[8];
+        sort_bucket<8>(e, bucket + st, len);
+        link_bucket<8>(e, len, Nn);
+        H = (e[0] > p) ? e[0] : e[1];
+      } else if (len > 8 && len <= 16) {
+        uint32_t e[16];
+        sort_bucket<16>(e, bucket + st, len);
+        link_bucket<16>(e, len, Nn);
+        H = (e[0] > p) ? e[0] : e[1];
+      } else if (len > 16 && len <= 32) {
+        uint32_t e[32];
+        sort_bucket<32>(e, bucket + st, len);
+        link_bucket<32>(e, len, Nn);
+        H = (e[0] > p) ? e[0] : e[1];
+      } else if (len > 32) {
+        for (uint32_t a = st + 1; a < en; ++a) {  // (practically never) insertion sort in place
+          const uint16_t v = bucket[a];
+          uint32_t b = a;
+          while (b > st && bucket[b - 1] > v) { bucket[b] = bucket[b - 1]; --b; }
+          bucket[b] = v;
+        }
+        uint32_t prev = bucket[st];
+        for (uint32_t a = st + 1; a < en; ++a) {
+          const uint32_t cur = bucket[a];
+          Nn[prev] = (uint16_t)cur;
+          prev = cur;
+        }
+        Nn[prev] = 0;
+        const uint32_t f0 = bucket[st];
+        H = (f0 > p) ? f0 : (uint32_t)bucket[st + 1];
       }
-      Nn[s] = (uint16_t)(best == 0xFFFFFFFFu ? 0u : best);
-    }
-    for (uint32_t x = tid; x < m; x += BLOCK) {
-      uint32_t en = c16[x], st = x ? c16[x - 1] : 0u;
-      uint32_t best = 0xFFFFFFFFu;
-      for (uint32_t a = st; a < en; ++a) {
-        uint32_t v = bucket[a];
-        if (v > x && v < best) best = v;
-      }
-      Hg[x] = (uint16_t)(best == 0xFFFFFFFFu ? 0u : best);
+      Hg[p] = (uint16_t)H;
     }
     __syncthreads();
-    for (uint32_t x = tid; x < m; x += BLOCK) c16[x] = Hg[x];
+    for (uint32_t w = tid; w < nwords; w += BLOCK) sh[w] = reinterpret_cast<const uint32_t*>(Hg)[w];
     __syncthreads();
-    // 5. chase and gather
+    // 5. chase and gather: final[i] = orig[W(N(i))] or orig[j_i]; final[0] = orig[W(0)]
+#pragma unroll 4
     for (uint32_t i = tid; i < m; i += BLOCK) {
-      uint32_t x;
+      uint32_t x = (i == 0) ? 0u : (uint32_t)Nn[i];
       uint32_t src;
-      bool done = false;
-      if (i == 0) {
-        x = 0;
+      if (i != 0 && x == 0) {
+        src = dr[i];
       } else {
-        x = Nn[i];
-        if (x == 0) { src = dr[i]; done = true; }
-      }
-      if (!done) {
         uint32_t h;
         while ((h = c16[x]) != 0) x = h;
         src = x;
@@ -247,7 +324,10 @@ void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nle
                           unsigned long long* bits, cudaStream_t st) {
   if (!nleaves) return;
   unsigned blocks = (unsigned)((nleaves + 31) / 32);
-  leaf_decode16_kernel<<<blocks, 32, 0, st>>>(J, E, nleaves, draws, bits);
+  if (E.active && E.sd.plen != 0)
+    leaf_decode16_kernel<false><<<blocks, 32, 0, st>>>(J, E, nleaves, draws, bits);
+  else
+    leaf_decode16_kernel<true><<<blocks, 32, 0, st>>>(J, E, nleaves, draws, bits);
   count_launch();
 }
 

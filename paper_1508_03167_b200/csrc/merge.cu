@@ -513,14 +513,14 @@ __global__ void __launch_bounds__(BLOCK) merge_level_kernel(const V* __restrict_
   V* bufA = reinterpret_cast<V*>(smem_raw);    // T + VPA: the A tile
   V* bbuf = bufA + T + VPA;                    // BBUF: B run of every window
   uint16_t* sel = reinterpret_cast<uint16_t*>(bbuf + BBUF);  // BCAP
-  uint32_t* cmask = reinterpret_cast<uint32_t*>(sel + BCAP);  // MAXCH
-  uint32_t* cpre = cmask + MAXCH;                             // MAXCH
+  uint32_t* cmask = reinterpret_cast<uint32_t*>(sel + BCAP);  // MAXCH one-bit masks
+  uint32_t* cinfo = cmask + MAXCH;                            // MAXCH (window << 16 | chunk in window)
+  uint32_t* crank = cinfo + MAXCH;                            // MAXCH window rank of first one
   __shared__ __align__(8) uint64_t mbar;
   __shared__ WinRec sw[kHMax];
   __shared__ uint32_t boff[kHMax];
   __shared__ uint32_t cbase[kHMax + 1];   // first chunk of window h
   __shared__ uint32_t sbase[kHMax + 1];   // first sel slot of window h
-  __shared__ uint8_t cwin[MAXCH];         // window of each chunk
   __shared__ uint32_t wsum[BLOCK / 32];
   __shared__ uint32_t a_off_s;
 
@@ -603,23 +603,29 @@ __global__ void __launch_bounds__(BLOCK) merge_level_kernel(const V* __restrict_
   }
   __syncthreads();
   const uint32_t nch = cbase[nw];
-  // ---- bit masks of every chunk (positions >= t count as zeros) + rank scan
+  // ---- bit masks of every chunk (positions >= t count as zeros) + rank scan.
+  // Thread tid owns chunks [tid*CPT, tid*CPT+CPT) (contiguous, so the window
+  // index only moves forward).
   uint32_t csum[CPT];
   uint32_t tsum = 0;
+  uint32_t h = 0;
+  {
+    const uint32_t c0 = tid * CPT;
+    uint32_t lo = 0, hi = nw;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (cbase[mid] <= c0) lo = mid; else hi = mid;
+    }
+    h = lo;
+  }
 #pragma unroll
   for (int q = 0; q < CPT; ++q) {
-    uint32_t c = tid * CPT + q;
+    const uint32_t c = tid * CPT + q;
     uint32_t m = 0;
     if (c < nch) {
-      uint32_t lo = 0, hi = nw;  // window of chunk c: cbase[lo] <= c < cbase[lo+1]
-      while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (cbase[mid] <= c) lo = mid; else hi = mid;
-      }
-      const uint32_t h = lo;
-      cwin[c] = (uint8_t)h;
-      uint32_t i0 = (c - cbase[h]) * 32;
-      uint64_t p = sw[h].start + i0;
+      while (cbase[h + 1] <= c) ++h;
+      const uint32_t i0 = (c - cbase[h]) * 32;
+      const uint64_t p = sw[h].start + i0;
       if (p < t) {
         uint32_t nv = min(32u, (uint32_t)sw[h].len - i0);
         uint64_t nt = t - p;
@@ -639,46 +645,65 @@ __global__ void __launch_bounds__(BLOCK) merge_level_kernel(const V* __restrict_
   }
   if (lane == 31) wsum[wid] = x;
   __syncthreads();
-  uint32_t before = 0;
+  {
+    uint32_t run = x - tsum;
 #pragma unroll
-  for (int w = 0; w < BLOCK / 32; ++w) before += (w < (int)wid) ? wsum[w] : 0u;
-  uint32_t run = before + x - tsum;
+    for (int w = 0; w < BLOCK / 32; ++w) run += (w < (int)wid) ? wsum[w] : 0u;
+    // per chunk: (window, chunk-in-window) and the window rank of its first one
+    // (ones before window h == sbase[h], fixed by the plan)
+    uint32_t hh;
+    const uint32_t c0 = tid * CPT;
+    uint32_t lo = 0, hi = nw;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (cbase[mid] <= c0) lo = mid; else hi = mid;
+    }
+    hh = lo;
 #pragma unroll
-  for (int q = 0; q < CPT; ++q) {
-    uint32_t c = tid * CPT + q;
-    if (c < nch) cpre[c] = run;   // ones before chunk c over all windows
-    run += csum[q];
+    for (int q = 0; q < CPT; ++q) {
+      const uint32_t c = c0 + q;
+      if (c < nch) {
+        while (cbase[hh + 1] <= c) ++hh;
+        cinfo[c] = (hh << 16) | (c - cbase[hh]);
+        crank[c] = run - sbase[hh];
+      }
+      run += csum[q];
+    }
   }
   __syncthreads();
   // ---- sel scatter: window h's r-th one sits at position i of window h
+  const uint32_t ltmask = ~(0xffffffffu >> lane);  // lanes before this one (MSB-first)
   for (uint32_t c = wid; c < nch; c += BLOCK / 32) {
-    uint32_t m = cmask[c];
+    const uint32_t m = cmask[c];
     if ((m >> (31 - lane)) & 1u) {
-      uint32_t h = cwin[c];
-      uint32_t r = cpre[c] - cpre[cbase[h]] + __popc(m & ~(0xffffffffu >> lane));
-      sel[sbase[h] + r] = (uint16_t)((c - cbase[h]) * 32 + lane);
+      const uint32_t info = cinfo[c];
+      const uint32_t r = crank[c] + __popc(m & ltmask);
+      sel[sbase[info >> 16] + r] = (uint16_t)(((info & 0xFFFFu) << 5) + lane);
     }
   }
   __syncthreads();
   mbar_wait(&mbar, 0);
-  // ---- outputs
+  // ---- outputs: one warp per chunk (window uniform across the warp), both the
+  // one-path (B element) and the zero-path (A element through the sel chain)
+  // evaluated branch-free, one coalesced store per lane.
   const V* Fa = bufA + a_off_s;
   for (uint32_t c = wid; c < nch; c += BLOCK / 32) {
-    uint32_t h = cwin[c];
-    uint32_t i = (c - cbase[h]) * 32 + lane;
-    uint32_t lh = (uint32_t)sw[h].len;
-    if (i >= lh) continue;
-    uint32_t m = cmask[c];
-    V val;
-    if ((m >> (31 - lane)) & 1u) {
-      uint32_t r = cpre[c] - cpre[cbase[h]] + __popc(m & ~(0xffffffffu >> lane));
-      val = (boff[h] != NOPF) ? bbuf[boff[h] + r] : pin[sw[h + 1].start + r];
-    } else {
-      uint32_t r = i;
-      for (int k = (int)h - 1; k >= 0; --k) r = sel[sbase[k] + r];
-      val = Fa[r];
-    }
-    pout[sw[h].start + i] = val;
+    const uint32_t info = cinfo[c];
+    const uint32_t hw = info >> 16;
+    const uint32_t i = ((info & 0xFFFFu) << 5) + lane;
+    const uint32_t lh = (uint32_t)sw[hw].len;
+    const uint32_t m = cmask[c];
+    const bool inb = i < lh;
+    const bool one = (m >> (31 - lane)) & 1u;
+    uint32_t r = inb ? i : lh - 1;
+    for (int k = (int)hw - 1; k >= 0; --k) r = sel[sbase[k] + r];
+    const V vz = Fa[r];
+    const uint32_t ro = crank[c] + __popc(m & ltmask);
+    const uint32_t bo = boff[hw];
+    V vo = vz;
+    if (bo != NOPF) vo = bbuf[bo + ro];
+    else if (one && inb) vo = pin[sw[hw + 1].start + ro];
+    if (inb) pout[sw[hw].start + i] = one ? vo : vz;
   }
 }
 
@@ -701,7 +726,7 @@ static void merge_level_t(const void* in, void* out, const PairPlan* plans, uint
   constexpr int MAXCH = (T + BCAP) / 32 + kHMax;
   {
     constexpr int BBUF = BCAP + 2 * (16 / sizeof(V)) * kHMax;
-    size_t smem = (size_t)(T + 16 / sizeof(V) + BBUF) * sizeof(V) + (size_t)BCAP * 2 + (size_t)MAXCH * 8;
+    size_t smem = (size_t)(T + 16 / sizeof(V) + BBUF) * sizeof(V) + (size_t)BCAP * 2 + (size_t)MAXCH * 12;
     auto k = merge_level_kernel<V, kMergeBlock, T, BCAP>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)tiles, kMergeBlock, smem, st>>>((const V*)in, (V*)out, plans, tpp, wins, nwin);
