@@ -123,13 +123,11 @@ static int plan_c(uint64_t n, uint64_t cutoff) {
 struct LevelBufs {
   LevelJob LJ;
   uint64_t sbs = 0, npairs = 0;
-  uint32_t tpp = 0;
   uint64_t* rank = nullptr;
   PairPlan* plans = nullptr;
-  WinRec* wins = nullptr;
-  uint32_t* nwin = nullptr;
-  uint32_t* flag_list = nullptr;   // tiles for the sequential-window kernel
-  uint32_t* flag_count = nullptr;
+  uint64_t* segs = nullptr;                 // npairs x kSMax segment boundaries
+  unsigned long long* seglen_max = nullptr;  // kSMax: longest segment h over pairs
+  uint64_t seglen_host[kSMax] = {};
   // tails
   uint64_t total = 0;
   uint64_t* rec_key = nullptr;
@@ -166,21 +164,18 @@ static void fork_side(cudaStream_t st, cudaStream_t ps) {
 static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* d_bits, Arena& A, cudaStream_t ps,
                         cudaStream_t st) {
   const int nl = (int)lv.size();
-  uint32_t T = merge_tile(eb);
   (void)st;
+  (void)eb;
   for (auto& L : lv) {
     L.rank = A.alloc<uint64_t>(L.npairs * L.sbs, ps);
     L.plans = A.alloc<PairPlan>(L.npairs, ps);
-    L.wins = A.alloc<WinRec>(L.npairs * L.tpp * kHMax, ps);
-    L.nwin = A.alloc<uint32_t>(L.npairs * L.tpp, ps);
-    L.flag_list = A.alloc<uint32_t>(L.npairs * L.tpp, ps);
-    L.flag_count = A.alloc<uint32_t>(1, ps);
-    CK(cudaMemsetAsync(L.flag_count, 0, 4, ps));
+    L.segs = A.alloc<uint64_t>(L.npairs * kSMax, ps);
+    L.seglen_max = A.alloc<unsigned long long>(kSMax, ps);
+    CK(cudaMemsetAsync(L.seglen_max, 0, kSMax * 8, ps));
   }
   for (auto& L : lv) {
     launch_rank_tables(L.LJ, L.sbs, L.rank, ps);
-    launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, ps);
-    launch_windows(L.plans, L.npairs, L.tpp, T, L.rank, L.wins, L.nwin, L.flag_list, L.flag_count, ps);
+    launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, L.segs, L.seglen_max, ps);
   }
   CK(cudaGetLastError());
   // (the host synchronization below also orders the data stream's merge
@@ -194,9 +189,11 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
   }
   pprefix[nl] = tot_pairs;
   std::vector<PairPlan> hplans(tot_pairs);
-  for (int i = 0; i < nl; ++i)
+  for (int i = 0; i < nl; ++i) {
     CK(cudaMemcpyAsync(hplans.data() + pprefix[i], lv[i].plans, lv[i].npairs * sizeof(PairPlan),
                        cudaMemcpyDeviceToHost, ps));
+    CK(cudaMemcpyAsync(lv[i].seglen_host, lv[i].seglen_max, kSMax * 8, cudaMemcpyDeviceToHost, ps));
+  }
   CK(cudaStreamSynchronize(ps));
   std::vector<uint64_t> offs(tot_pairs);
   for (int i = 0; i < nl; ++i) {
@@ -279,8 +276,7 @@ static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* oth
   for (auto& L : lv) {
     {
       StageTimer tm(2, st);
-      launch_merge_level(eb, cur, other, L.plans, L.npairs, L.tpp, L.rank, L.wins, L.nwin, L.flag_list, L.flag_count,
-                         st);
+      launch_merge_round(eb, cur, other, L.plans, L.npairs, L.rank, L.segs, L.seglen_host, st);
     }
     {
       StageTimer tm(3, st);
@@ -296,7 +292,7 @@ static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* oth
 
 static std::vector<LevelBufs> make_levels(const ArrayJob& J, int eb) {
   std::vector<LevelBufs> lv;
-  uint32_t T = merge_tile(eb);
+  (void)eb;
   for (int r = 1; r <= J.c; ++r) {
     LevelBufs L;
     L.LJ.J = J;
@@ -305,9 +301,7 @@ static std::vector<LevelBufs> make_levels(const ArrayJob& J, int eb) {
     L.npairs = J.batch << (J.c - r);
     L.LJ.npairs = L.npairs;
     uint64_t Nmax = (J.len >> (J.c - r)) + 2;
-    uint64_t n1max = (J.len >> (J.c - r + 1)) + 1;
     L.sbs = (Nmax + 1 + 511) / 512 + 1;
-    L.tpp = (uint32_t)((n1max + T - 1) / T);
     lv.push_back(L);
   }
   return lv;
@@ -418,9 +412,6 @@ static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t
   L.LJ.npairs = 1;
   L.npairs = 1;
   L.sbs = (N + 1 + 511) / 512 + 1;
-  uint32_t T = merge_tile(eb);
-  L.tpp = (uint32_t)((k - j + T - 1) / T);
-  if (L.tpp == 0) L.tpp = 1;
   try {
     unsigned char* scratch = A.alloc<unsigned char>(N * eb, st);
     fork_side(st, ps);
@@ -428,8 +419,7 @@ static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t
     // kernels address elements by absolute index; shift the scratch base so
     // index j lands on scratch[0].
     void* out_base = (void*)(scratch - j * eb);
-    launch_merge_level(eb, data, out_base, L.plans, 1, L.tpp, L.rank, L.wins, L.nwin, L.flag_list, L.flag_count,
-                       st);
+    launch_merge_round(eb, data, out_base, L.plans, 1, L.rank, L.segs, L.seglen_host, st);
     launch_copy_tail_region(eb, data, out_base, L.plans, 1, st);
     CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
     launch_tail_apply(eb, out_base, L.dst, L.src, L.tmp, 2 * L.total, st);

@@ -11,8 +11,8 @@
 //      final[i] = orig[W(N(i))] (or orig[j_i] if none), final[0] = orig[W(0)],
 //      W(x) = W(H(x)) if H(x) exists else x.
 //    Steps are bucketed by target with a shared-memory counting sort (16-bit
-//    counters, two per 32-bit word, atomics in smem); each bucket (~1 step on
-//    average) is sorted in registers by the lane owning the target, then every output
+//    counters, two per 32-bit word, atomics in smem); one lane per bucket
+//    entry scans its (tiny) bucket for its successor, then every output
 //    gathers through the chain.
 #include <algorithm>
 #include "sk_kernels.h"
@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(32) leaf_decode16_kernel(ArrayJob J, ExplicitT
   }
   uint32_t i = m >= 2 ? m - 1 : 0;   // current step; its bound is i + 1
   uint16_t* dr = draws + L.lo;
+  uint16_t* wp = dr + i;             // where draw i goes
   uint64_t gw = 0;
   uint32_t wr = 0;
   if (i) {
@@ -83,17 +84,20 @@ __global__ void __launch_bounds__(32) leaf_decode16_kernel(ArrayJob J, ExplicitT
       // (i == 0) compute harmlessly but never store or advance
       const bool act = i != 0;
       const uint32_t b = i + 1;
-      uint32_t k = lb - (31 - __clz(v));
+      uint32_t k = lb + __clz(v) - 31;
       k += ((v << k) < b) ? 1u : 0u;
       const uint32_t x = __funnelshift_l(B, A, pos);
       const uint32_t cc = (c << k) | (x >> (32 - k));
-      const bool acc = act && cc < b;
+      const uint32_t acc = (act && cc < b) ? 1u : 0u;
+      // predicated 16-bit store through a running pointer (wp == &dr[i])
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.global.u16 [%1], %2;\n}" ::"r"(acc), "l"(wp),
+                   "h"((unsigned short)cc)
+                   : "memory");
+      wp -= acc;
       c = acc ? 0u : cc - b;
       v = acc ? 1u : (v << k) - b;
-      if (acc) dr[i] = (uint16_t)cc;
-      // floor(log2(i-1)) drops by one exactly when i is a power of two
-      lb = (acc && i == (1u << lb)) ? lb - 1 : lb;
-      i = acc ? i - 1 : i;
+      lb -= (acc && i == (1u << lb)) ? 1u : 0u;  // floor(log2(i-1)) drops at powers of two
+      i -= acc;
       const uint32_t kk = act ? k : 0u;
       nb += kk;
       pos += kk;
@@ -146,35 +150,12 @@ __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
   a = lo; b = hi;
 }
 
-// Load a bucket of len <= N entries into registers (missing ones = 0xFFFF)
-// and sort ascending with a bitonic network (compile-time indices only).
-template <int N>
-__device__ __forceinline__ void sort_bucket(uint32_t (&e)[N], const uint16_t* b, uint32_t len) {
-#pragma unroll
-  for (int a = 0; a < N; ++a) e[a] = ((uint32_t)a < len) ? (uint32_t)b[a] : 0xFFFFu;
-#pragma unroll
-  for (int k2 = 2; k2 <= N; k2 <<= 1) {
-#pragma unroll
-    for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-#pragma unroll
-      for (int a = 0; a < N; ++a) {
-        const int b2 = a ^ j2;
-        if (b2 > a) {
-          if ((a & k2) == 0) cswap(e[a], e[b2]);
-          else cswap(e[b2], e[a]);
-        }
-      }
-    }
-  }
-}
-
-// successor links of a sorted bucket: N(e[a]) = e[a+1], N(last) = none
-template <int N>
-__device__ __forceinline__ void link_bucket(const uint32_t (&e)[N], uint32_t len, uint16_t* Nn) {
-#pragma unroll
-  for (int a = 0; a < N; ++a) {
-    if ((uint32_t)a < len) Nn[e[a]] = ((uint32_t)a + 1 < len) ? (uint16_t)e[(a + 1) % N] : (uint16_t)0;
-  }
+// TMA bulk prefetch of [p, p+bytes) (16-byte aligned interior) into L2.
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
+  const uintptr_t a0 = ((uintptr_t)p + 15) & ~(uintptr_t)15;
+  const uintptr_t a1 = ((uintptr_t)p + bytes) & ~(uintptr_t)15;
+  if (a1 > a0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
 }
 
 template <typename V, int BLOCK>
@@ -201,97 +182,167 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
       continue;
     }
     const uint16_t* __restrict__ dr = draws + L.lo;
+    if (tid == 0) {  // pull this leaf's data and the next leaf's draws into L2
+      l2_prefetch(src_in, (size_t)m * sizeof(V));
+      if (g == blockIdx.x) l2_prefetch(dr, (size_t)m * 2);
+      if (g + gridDim.x < nleaves) {
+        const LeafDesc Ln = leaf_desc(J, E, g + gridDim.x);
+        l2_prefetch(draws + Ln.lo, (size_t)(Ln.hi - Ln.lo) * 2);
+      }
+    }
     const uint32_t nwords = (m + 1) >> 1;
-    for (uint32_t w = tid; w < nwords; w += BLOCK) sh[w] = 0;
+    for (uint32_t w = tid; w < nwords; w += BLOCK) {
+      sh[w] = 0;
+      reinterpret_cast<uint32_t*>(Hg)[w] = 0;  // H(p) = none unless set in step 4
+    }
     __syncthreads();
-    // 1. histogram of targets (steps s = 1 .. m-1; dr[0] is unused)
+    // 1. histogram of targets (steps s = 1 .. m-1; dr[0] is unused); draws
+    //    are read 8 at a time when the leaf is 16-byte aligned
+    const bool vec = ((((uintptr_t)dr) & 15) == 0);
+    if (vec) {
+      const uint4* dv = reinterpret_cast<const uint4*>(dr);
+      const uint32_t nv = m >> 3;
+#pragma unroll 2
+      for (uint32_t q = tid; q < nv; q += BLOCK) {
+        const uint4 w = dv[q];
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const uint32_t j = (ws[h >> 1] >> ((h & 1) << 4)) & 0xFFFFu;
+          if (q != 0 || h != 0) atomicAdd(&sh[j >> 1], 1u << ((j & 1) << 4));
+        }
+      }
+      for (uint32_t s = (nv << 3) + tid; s < m; s += BLOCK) {
+        if (s == 0) continue;
+        const uint32_t j = dr[s];
+        atomicAdd(&sh[j >> 1], 1u << ((j & 1) << 4));
+      }
+    } else {
 #pragma unroll 4
-    for (uint32_t s = 1 + tid; s < m; s += BLOCK) {
-      const uint32_t j = dr[s];
-      atomicAdd(&sh[j >> 1], 1u << ((j & 1) << 4));
+      for (uint32_t s = 1 + tid; s < m; s += BLOCK) {
+        const uint32_t j = dr[s];
+        atomicAdd(&sh[j >> 1], 1u << ((j & 1) << 4));
+      }
     }
     __syncthreads();
     // 2. bucket starts
     scan_counts16(c16, m, warp_tot);
     __syncthreads();
     // 3. scatter step ids into their target's bucket (order inside a bucket is arbitrary)
+    if (vec) {
+      const uint4* dv = reinterpret_cast<const uint4*>(dr);
+      const uint32_t nv = m >> 3;
+#pragma unroll 2
+      for (uint32_t q = tid; q < nv; q += BLOCK) {
+        const uint4 w = dv[q];
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const uint32_t j = (ws[h >> 1] >> ((h & 1) << 4)) & 0xFFFFu;
+          if (q != 0 || h != 0) {
+            const uint32_t sh16 = (j & 1) << 4;
+            const uint32_t old = atomicAdd(&sh[j >> 1], 1u << sh16);
+            bucket[(old >> sh16) & 0xFFFFu] = (uint16_t)((q << 3) + h);
+          }
+        }
+      }
+      for (uint32_t s = (nv << 3) + tid; s < m; s += BLOCK) {
+        if (s == 0) continue;
+        const uint32_t j = dr[s];
+        const uint32_t sh16 = (j & 1) << 4;
+        const uint32_t old = atomicAdd(&sh[j >> 1], 1u << sh16);
+        bucket[(old >> sh16) & 0xFFFFu] = (uint16_t)s;
+      }
+    } else {
 #pragma unroll 4
-    for (uint32_t s = 1 + tid; s < m; s += BLOCK) {
-      const uint32_t j = dr[s];
-      const uint32_t sh16 = (j & 1) << 4;
-      const uint32_t old = atomicAdd(&sh[j >> 1], 1u << sh16);
-      bucket[(old >> sh16) & 0xFFFFu] = (uint16_t)s;
+      for (uint32_t s = 1 + tid; s < m; s += BLOCK) {
+        const uint32_t j = dr[s];
+        const uint32_t sh16 = (j & 1) << 4;
+        const uint32_t old = atomicAdd(&sh[j >> 1], 1u << sh16);
+        bucket[(old >> sh16) & 0xFFFFu] = (uint16_t)s;
+      }
     }
     __syncthreads();
-    // 4. per target p (lane-consecutive targets, warps interleaved so the long
-    //    buckets of targets near 0 -- mean length ln(m/p) -- spread over all
-    //    warps): sort the bucket in registers (networks for <= 4, 8, 16, 32
-    //    entries), link successors N, and write H(p) = first step > p
-    //    targeting p to Hg (copied over c16 after the barrier).
-    for (uint32_t p = tid; p < m; p += BLOCK) {
-      const uint32_t en = c16[p];
-      const uint32_t st = p ? (uint32_t)c16[p - 1] : 0u;
-      const uint32_t len = en - st;
-      uint32_t H = 0;
-      if (len == 1) {
-        const uint32_t e0 = bucket[st];
-        Nn[e0] = 0;
-        H = (e0 > p) ? e0 : 0u;
-      } else if (len >= 2 && len <= 4) {
-        uint32_t e[4];
-        sort_bucket<4>(e, bucket + st, len);
-        link_bucket<4>(e, len, Nn);
-        H = (e[0] > p) ? e[0] : e[1];
-      } else if (len > 4 && len <= 8) {
-        uint32_t e[8];
-        sort_bucket<8>(e, bucket + st, len);
-        link_bucket<8>(e, len, Nn);
-        H = (e[0] > p) ? e[0] : e[1];
-      } else if (len > 8 && len <= 16) {
-        uint32_t e[16];
-        sort_bucket<16>(e, bucket + st, len);
-        link_bucket<16>(e, len, Nn);
-        H = (e[0] > p) ? e[0] : e[1];
-      } else if (len > 16 && len <= 32) {
-        uint32_t e[32];
-        sort_bucket<32>(e, bucket + st, len);
-        link_bucket<32>(e, len, Nn);
-        H = (e[0] > p) ? e[0] : e[1];
-      } else if (len > 32) {
-        for (uint32_t a = st + 1; a < en; ++a) {  // (practically never) insertion sort in place
-          const uint16_t v = bucket[a];
-          uint32_t b = a;
-          while (b > st && bucket[b - 1] > v) { bucket[b] = bucket[b - 1]; --b; }
-          bucket[b] = v;
-        }
-        uint32_t prev = bucket[st];
-        for (uint32_t a = st + 1; a < en; ++a) {
-          const uint32_t cur = bucket[a];
-          Nn[prev] = (uint16_t)cur;
-          prev = cur;
-        }
-        Nn[prev] = 0;
-        const uint32_t f0 = bucket[st];
-        H = (f0 > p) ? f0 : (uint32_t)bucket[st + 1];
+    // 4. one lane per bucket entry e (a step, target p = j_e): scan p's bucket
+    //    (mean size-biased length 3) for N(e) = min{e' > e} and for whether e
+    //    is H(p) = min{e' > p}.  No sorting, no per-target divergence.
+    //    Batches of 8 entries per thread keep 8 (then 32) L2 loads in flight
+    //    instead of a chain of dependent loads per entry.
+    for (uint32_t a0 = tid; a0 + 1 < m; a0 += 8 * BLOCK) {
+      uint32_t e[8], p[8], st[8], en[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t a = a0 + k * BLOCK;
+        e[k] = (a + 1 < m) ? (uint32_t)bucket[a] : 0u;
       }
-      Hg[p] = (uint16_t)H;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) p[k] = (a0 + k * BLOCK + 1 < m) ? (uint32_t)dr[e[k]] : 0u;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        en[k] = c16[p[k]];
+        st[k] = p[k] ? (uint32_t)c16[p[k] - 1] : 0u;
+      }
+      uint32_t best[8], between[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // first 4 entries of every bucket, all loads in flight
+        best[k] = 0xFFFFFFFFu; between[k] = 0;
+        uint32_t x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = (st[k] + u < en[k]) ? (uint32_t)bucket[st[k] + u] : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (st[k] + u < en[k]) {
+            best[k] = (x[u] > e[k] && x[u] < best[k]) ? x[u] : best[k];
+            between[k] += (x[u] > p[k] && x[u] < e[k]) ? 1u : 0u;
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        for (uint32_t b = st[k] + 4; b < en[k]; ++b) {  // long buckets (targets near 0)
+          const uint32_t x = bucket[b];
+          best[k] = (x > e[k] && x < best[k]) ? x : best[k];
+          between[k] += (x > p[k] && x < e[k]) ? 1u : 0u;
+        }
+        if (a0 + k * BLOCK + 1 < m) {
+          Nn[e[k]] = (uint16_t)(best[k] == 0xFFFFFFFFu ? 0u : best[k]);
+          if (e[k] > p[k] && between[k] == 0) Hg[p[k]] = (uint16_t)e[k];
+        }
+      }
     }
     __syncthreads();
     for (uint32_t w = tid; w < nwords; w += BLOCK) sh[w] = reinterpret_cast<const uint32_t*>(Hg)[w];
     __syncthreads();
     // 5. chase and gather: final[i] = orig[W(N(i))] or orig[j_i]; final[0] = orig[W(0)]
-#pragma unroll 4
-    for (uint32_t i = tid; i < m; i += BLOCK) {
-      uint32_t x = (i == 0) ? 0u : (uint32_t)Nn[i];
-      uint32_t src;
-      if (i != 0 && x == 0) {
-        src = dr[i];
-      } else {
-        uint32_t h;
-        while ((h = c16[x]) != 0) x = h;
-        src = x;
+    //    (batches of 8 outputs per thread: the N/draw loads, then the data
+    //    gathers, are in flight together)
+    for (uint32_t i0 = tid; i0 < m; i0 += 8 * BLOCK) {
+      uint32_t x[8], d[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t i = i0 + k * BLOCK;
+        x[k] = (i < m && i != 0) ? (uint32_t)Nn[i] : 0u;
+        d[k] = (i < m && i != 0) ? (uint32_t)dr[i] : 0u;
       }
-      dst[i] = src_in[src];
+      V v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t i = i0 + k * BLOCK;
+        uint32_t src;
+        if (i != 0 && x[k] == 0) {
+          src = d[k];
+        } else {
+          uint32_t y = x[k], h;
+          while ((h = c16[y]) != 0) y = h;
+          src = y;
+        }
+        if (i < m) v[k] = src_in[src];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t i = i0 + k * BLOCK;
+        if (i < m) dst[i] = v[k];
+      }
     }
     __syncthreads();
   }
@@ -337,9 +388,9 @@ static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nlea
                          cudaStream_t st) {
   size_t smem = (size_t)((mmax + 1) / 2) * 4;
   if (mmax > 8192) {
-    auto k = leaf_apply_kernel<V, 1024>;
+    auto k = leaf_apply_kernel<V, 512>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, 1024, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax);
+    k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax);
   } else {
     auto k = leaf_apply_kernel<V, 256>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -26,16 +26,14 @@ struct LevelTail {            // device-side view used by the all-levels tail de
   uint32_t* rec_pair;
 };
 void launch_rank_tables(const LevelJob& LJ, uint64_t sbs, uint64_t* rank, cudaStream_t st);
-void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, PairPlan* plans, cudaStream_t st);
+void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, PairPlan* plans, uint64_t* segs,
+                      unsigned long long* seglen_max, cudaStream_t st);
 void launch_tail_decode(const LevelTail* d_levels, int nlevels, const uint64_t* d_pair_prefix, uint64_t total_pairs,
                         unsigned long long* bits, cudaStream_t st);
-void launch_windows(const PairPlan* plans, uint64_t npairs, uint32_t tpp, uint32_t tile, const uint64_t* rank,
-                    WinRec* wins, uint32_t* nwin, uint32_t* flag_list, uint32_t* flag_count, cudaStream_t st);
-void launch_merge_level(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs, uint32_t tpp,
-                        const uint64_t* rank, const WinRec* wins, const uint32_t* nwin, const uint32_t* flag_list,
-                        const uint32_t* flag_count, cudaStream_t st);
+
+void launch_merge_round(int eb, void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
+                        const uint64_t* segs, const uint64_t* seglen_max_host, cudaStream_t st);
 uint32_t merge_tile(int eb);
-uint64_t merge_carry_cap(uint32_t tile);
 void launch_copy_tail_region(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs,
                              cudaStream_t st);
 void launch_iota32(uint32_t* v, uint64_t n, cudaStream_t st);

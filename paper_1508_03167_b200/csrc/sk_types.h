@@ -45,15 +45,13 @@ struct PairPlan {
   uint64_t array;       // owning array (bit accounting)
   uint32_t aex;         // 1: A exhausted (zero stop), 0: B exhausted
   uint32_t degenerate;  // n1 == 0 || n2 == 0: no bits, identity
+  uint32_t nseg;        // segments [S_h, S_{h+1}) of the A queue, h < nseg; X = S_nseg
+  uint32_t pad;
 };
 
-constexpr int kHMax = 40;            // stored windows per merge tile
+constexpr int kSMax = 64;            // stored segment boundaries per pair
 
-// Window h of a merge tile: positions [start, start+len) of its pair.
-struct WinRec {
-  uint64_t start;
-  uint64_t len;
-};
+
 constexpr uint64_t kNone = ~0ULL;
 
 // Leaf descriptor computed on device from an ArrayJob (or the explicit task).
