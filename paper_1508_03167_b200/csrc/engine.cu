@@ -174,7 +174,8 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
     CK(cudaMemsetAsync(L.seglen_max, 0, kSMax * 8, ps));
   }
   for (auto& L : lv) {
-    launch_rank_tables(L.LJ, L.sbs, L.rank, ps);
+    uint64_t* csum = A.alloc<uint64_t>(rank_scan_scratch(L.npairs, L.sbs), ps);
+    launch_rank_tables(L.LJ, L.sbs, L.rank, csum, ps);
     launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, L.segs, L.seglen_max, ps);
   }
   CK(cudaGetLastError());

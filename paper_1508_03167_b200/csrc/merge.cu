@@ -45,44 +45,92 @@ __global__ void rank_count_kernel(LevelJob LJ, uint64_t sbs, uint64_t* __restric
   R[k + 1] = cnt;
 }
 
-// In-place inclusive scan of each pair's table (one CTA per pair).
-__global__ void __launch_bounds__(1024) seg_scan_kernel(uint64_t* __restrict__ rank, uint64_t sbs) {
-  uint64_t* R = rank + (uint64_t)blockIdx.x * sbs;
-  __shared__ uint64_t wsum[32];
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  uint64_t carry = 0;
-  for (uint64_t base = 0; base < sbs; base += 1024) {
-    uint64_t i = base + tid;
-    uint64_t x = (i < sbs) ? R[i] : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= (uint32_t)o) x += y;
-    }
-    if (lane == 31) wsum[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-      uint64_t w = wsum[lane];
-      for (int o = 1; o < 32; o <<= 1) {
-        uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= (uint32_t)o) w += y;
-      }
-      wsum[lane] = w;
-    }
-    __syncthreads();
-    uint64_t add = carry + (wid ? wsum[wid - 1] : 0);
-    if (i < sbs) R[i] = x + add;
-    carry += wsum[31];
-    __syncthreads();
+// In-place inclusive scan of every pair's table, chunked so that the few
+// huge tables of the top rounds are scanned by many CTAs: (A) chunk sums,
+// (B) per-pair exclusive scan of the chunk sums, (C) chunk-local scan + offset.
+constexpr uint32_t kScanChunk = 4096;  // entries per CTA (256 threads x 16)
+
+__global__ void __launch_bounds__(256) scan_chunk_sums(const uint64_t* __restrict__ rank, uint64_t sbs, uint32_t cpp,
+                                                       uint64_t* __restrict__ csum) {
+  __shared__ uint64_t red[8];
+  const uint64_t g = blockIdx.x / cpp, ci = blockIdx.x - g * cpp;
+  const uint64_t* R = rank + g * sbs;
+  const uint64_t b0 = ci * kScanChunk, b1 = min(sbs, b0 + kScanChunk);
+  uint64_t v = 0;
+  for (uint64_t i = b0 + threadIdx.x; i < b1; i += 256) v += R[i];
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    csum[blockIdx.x] = t;
   }
 }
 
-void launch_rank_tables(const LevelJob& LJ, uint64_t sbs, uint64_t* rank, cudaStream_t st) {
+__global__ void scan_chunk_offsets(uint64_t* __restrict__ csum, uint32_t cpp) {
+  uint64_t* c = csum + (uint64_t)blockIdx.x * cpp;
+  const uint32_t lane = threadIdx.x;
+  uint64_t carry = 0;
+  for (uint32_t base = 0; base < cpp; base += 32) {
+    const uint32_t i = base + lane;
+    const uint64_t v = (i < cpp) ? c[i] : 0;
+    uint64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (i < cpp) c[i] = carry + x - v;  // exclusive
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+}
+
+__global__ void __launch_bounds__(256) scan_chunk_apply(uint64_t* __restrict__ rank, uint64_t sbs, uint32_t cpp,
+                                                        const uint64_t* __restrict__ coff) {
+  __shared__ uint64_t wsum[8];
+  const uint64_t g = blockIdx.x / cpp, ci = blockIdx.x - g * cpp;
+  uint64_t* R = rank + g * sbs;
+  const uint64_t b0 = ci * kScanChunk, b1 = min(sbs, b0 + kScanChunk);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t i0 = b0 + (uint64_t)tid * 16;  // 16 consecutive entries per thread
+  uint64_t v[16], sum = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    v[k] = (i0 + k < b1) ? R[i0 + k] : 0;
+    sum += v[k];
+  }
+  uint64_t x = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  uint64_t run = coff[blockIdx.x] + x - sum;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) run += (w < (int)wid) ? wsum[w] : 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    run += v[k];
+    if (i0 + k < b1) R[i0 + k] = run;  // inclusive
+  }
+}
+
+uint64_t rank_scan_scratch(uint64_t npairs, uint64_t sbs) {
+  return npairs * ((sbs + kScanChunk - 1) / kScanChunk);
+}
+
+void launch_rank_tables(const LevelJob& LJ, uint64_t sbs, uint64_t* rank, uint64_t* csum, cudaStream_t st) {
   uint64_t total = LJ.npairs * (sbs - 1);
   if (!total) return;
   rank_count_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(LJ, sbs, rank);
-  count_launch();
-  seg_scan_kernel<<<(unsigned)LJ.npairs, 1024, 0, st>>>(rank, sbs);
-  count_launch();
+  const uint32_t cpp = (uint32_t)((sbs + kScanChunk - 1) / kScanChunk);
+  const unsigned nblk = (unsigned)(LJ.npairs * cpp);
+  scan_chunk_sums<<<nblk, 256, 0, st>>>(rank, sbs, cpp, csum);
+  scan_chunk_offsets<<<(unsigned)LJ.npairs, 32, 0, st>>>(csum, cpp);
+  scan_chunk_apply<<<nblk, 256, 0, st>>>(rank, sbs, cpp, csum);
+  for (int i = 0; i < 4; ++i) count_launch();
 }
 
 // ------------------------------------------------------------ pair plans
@@ -171,41 +219,84 @@ void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, Pa
 }
 
 // ------------------------------------------------------------ tail decode
-// One thread per pair, all rounds in one launch so the long top-round tails
-// decode concurrently with the short ones.  Bits continue at offset t+1
-// (shufflers.py:188-191): for x = t..N-1, m_x = FDR(x+1).
-__global__ void tail_decode_kernel(const LevelTail* __restrict__ levels, int nlevels,
-                                   const uint64_t* __restrict__ prefix, uint64_t total,
-                                   unsigned long long* __restrict__ bits) {
-  uint64_t gg = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// One WARP per pair, all rounds in one launch.  Bits continue at offset t+1
+// (shufflers.py:188-191): for x = t..N-1, m_x = FDR(x+1).  The draws are
+// decoded speculatively 32 at a time: lane l assumes every earlier draw of the
+// batch accepted its first FDR iteration (k0 = ceil(log2 bound) bits), so its
+// offset is a warp prefix sum of k0; the first lane whose own first iteration
+// rejects finishes its draw with the full (serial) FDR and the next batch
+// starts after it.  Tail bounds are ~ the pair size, so for power-of-two pairs
+// a rejection is rare and 32 draws are decoded per step; the result is
+// bit-identical to the serial loop either way.
+__global__ void __launch_bounds__(128) tail_decode_kernel(const LevelTail* __restrict__ levels, int nlevels,
+                                                          const uint64_t* __restrict__ prefix, uint64_t total,
+                                                          unsigned long long* __restrict__ bits) {
+  const uint64_t gg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
   if (gg >= total) return;
   int L = 0;
   while (L + 1 < nlevels && prefix[L + 1] <= gg) ++L;
-  uint64_t g = gg - prefix[L];
-  LevelTail lv = levels[L];
+  const uint64_t g = gg - prefix[L];
+  const LevelTail lv = levels[L];
   PairPlan* Pp = lv.plans + g;
   if (Pp->degenerate) return;
   const uint64_t t = Pp->t, N = Pp->n1 + Pp->n2, s = Pp->s, off = Pp->tail_off;
-  uint64_t nb = 0;
-  if (t < N) {
-    Reader64 rd;
-    rd.init(Pp->sd, t + 1);
-    for (uint64_t x = t; x < N; ++x) {
-      uint64_t m = fdr64(rd, x + 1, nb);
-      lv.rec_key[off + (x - t)] = s + m;
-      lv.rec_pair[off + (x - t)] = (uint32_t)g;
+  const StreamDesc sd = Pp->sd;
+  uint64_t o = t + 1;  // bit offset of the next draw
+  uint64_t x = t;      // next insertion step
+  while (x < N) {
+    const uint64_t xl = x + lane;
+    const bool valid = xl < N;
+    const uint64_t b = xl + 1;
+    const uint32_t k0 = valid ? 64u - __clzll(b - 1) : 0u;
+    uint32_t ps = k0;  // inclusive warp prefix of k0
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ps, d);
+      if (lane >= (uint32_t)d) ps += y;
+    }
+    const uint64_t ol = o + (ps - k0);
+    uint64_t c = 0;
+    bool acc = false;
+    if (valid) {
+      c = bits64_at(sd, ol) >> (64 - k0);
+      acc = c < b;
+    }
+    const uint32_t fail = __ballot_sync(0xffffffffu, valid && !acc);
+    const uint32_t f = fail ? (uint32_t)(__ffs(fail) - 1) : 32u;  // first rejecting lane
+    if (valid && lane < f) {
+      lv.rec_key[off + (xl - t)] = s + c;
+      lv.rec_pair[off + (xl - t)] = (uint32_t)g;
+    }
+    if (f < 32) {
+      uint64_t used = 0, m = 0;
+      if (lane == f) {  // full fast-dice-roller for this draw (_kernels.py:64-82)
+        Reader64 rd;
+        rd.init(sd, ol);
+        m = fdr64(rd, b, used);
+        lv.rec_key[off + (xl - t)] = s + m;
+        lv.rec_pair[off + (xl - t)] = (uint32_t)g;
+      }
+      used = __shfl_sync(0xffffffffu, used, f);
+      const uint64_t of = __shfl_sync(0xffffffffu, ol, f);
+      o = of + used;
+      x += f + 1;
+    } else {
+      o += __shfl_sync(0xffffffffu, ps, 31);
+      x += 32;
     }
   }
-  uint64_t b = t + 1 + nb;
-  Pp->bits = b;
-  atomicAdd(&bits[Pp->array], (unsigned long long)b);
+  if (lane == 0) {
+    const uint64_t bt = o;  // t+1 phase-1 bits + tail bits
+    Pp->bits = bt;
+    atomicAdd(&bits[Pp->array], (unsigned long long)bt);
+  }
 }
 
 void launch_tail_decode(const LevelTail* d_levels, int nlevels, const uint64_t* d_prefix, uint64_t total_pairs,
                         unsigned long long* bits, cudaStream_t st) {
   if (!total_pairs) return;
-  tail_decode_kernel<<<(unsigned)((total_pairs + 63) / 64), 64, 0, st>>>(d_levels, nlevels, d_prefix, total_pairs,
-                                                                         bits);
+  tail_decode_kernel<<<(unsigned)((total_pairs * 32 + 127) / 128), 128, 0, st>>>(d_levels, nlevels, d_prefix,
+                                                                                  total_pairs, bits);
   count_launch();
 }
 

@@ -25,7 +25,8 @@ struct LevelTail {            // device-side view used by the all-levels tail de
   uint64_t* rec_key;          // s + m_x (global position of the insertion target)
   uint32_t* rec_pair;
 };
-void launch_rank_tables(const LevelJob& LJ, uint64_t sbs, uint64_t* rank, cudaStream_t st);
+void launch_rank_tables(const LevelJob& LJ, uint64_t sbs, uint64_t* rank, uint64_t* csum, cudaStream_t st);
+uint64_t rank_scan_scratch(uint64_t npairs, uint64_t sbs);
 void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, PairPlan* plans, uint64_t* segs,
                       unsigned long long* seglen_max, cudaStream_t st);
 void launch_tail_decode(const LevelTail* d_levels, int nlevels, const uint64_t* d_pair_prefix, uint64_t total_pairs,
