@@ -328,7 +328,7 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
     if (fast_leaf) {
       draws = A.alloc<uint16_t>(ntot, st);
       grid = leaf_apply_grid(nleaves, (uint32_t)mmax, num_sms());
-      lscr = A.alloc<uint16_t>((uint64_t)grid * 3 * ((mmax + 1) & ~1ULL) + 8, st);
+      lscr = A.alloc<uint16_t>((uint64_t)grid * 2 * ((mmax + 1) & ~1ULL) + 8, st);
     }
     fork_side(st, ps);
     {
@@ -453,7 +453,7 @@ static void run_single_leaf(int eb, void* data, uint64_t lo, uint64_t hi, const 
     if (m <= 65536) {
       uint16_t* draws = A.alloc<uint16_t>(m, st);
       unsigned char* scratch = A.alloc<unsigned char>(m * eb, st);
-      uint16_t* lscr = A.alloc<uint16_t>(3 * ((m + 1) & ~1ULL) + 8, st);
+      uint16_t* lscr = A.alloc<uint16_t>(2 * ((m + 1) & ~1ULL) + 8, st);
       // absolute-index kernels: shift bases so index lo lands on element 0
       launch_leaf_decode16(J, E, 1, draws - lo, d_bits, st);
       launch_leaf_apply(eb, J, E, 1, data, (void*)(scratch - lo * eb), draws - lo, lscr, (uint32_t)m, 1, st);
@@ -506,6 +506,12 @@ static int fetch_bits(unsigned long long* d_bits, uint64_t* out, uint64_t count,
 extern "C" {
 
 int sk_version(void) { return 1; }
+
+// Internal knobs for performance experiments (not part of the public header).
+int sk_debug_set(int key, int value) {
+  if (key == 1) { debug_set_leaf_stop(value); return 0; }
+  return -1;
+}
 const char* sk_last_error(void) { return g_err.c_str(); }
 uint64_t sk_launch_count(void) { return g_launches.load(); }
 

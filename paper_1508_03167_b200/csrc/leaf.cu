@@ -19,6 +19,9 @@
 
 namespace sk {
 
+// debug: stop the leaf-apply pipeline after phase k (phase timing experiments)
+__device__ int g_leaf_stop = 99;
+
 // One lane per leaf, one fast-dice-roller *iteration* per loop trip (so lanes
 // whose draws reject do not stall the others), bits served from a per-lane ring
 // of 32-bit half-words in shared memory that the warp tops up in bulk (uniform
@@ -158,6 +161,13 @@ __device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
 }
 
+// Leaf apply.  Targets are handled in halves of <= 32768 so that both the
+// 16-bit bucket cursors (64 KB) and the bucket array itself (<= 128 KB) live in
+// shared memory: histogram, scan, scatter and the per-target bucket sort are
+// all shared-memory work.  Successor links N go to global scratch, the H
+// table is staged in global and reloaded into shared memory for the chase.
+constexpr uint32_t kLeafHalf = 32768;
+
 template <typename V, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
                                                            const V* __restrict__ in, V* __restrict__ out,
@@ -165,12 +175,15 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
                                                            uint16_t* __restrict__ scratch, uint32_t mmax) {
   extern __shared__ uint32_t sh[];
   __shared__ uint32_t warp_tot[BLOCK / 32];
-  uint16_t* c16 = reinterpret_cast<uint16_t*>(sh);
-  const uint32_t ms = (mmax + 1) & ~1u;  // even stride: Hg is copied as 32-bit words
-  uint16_t* bucket = scratch + (uint64_t)blockIdx.x * 3 * ms;
-  uint16_t* Nn = bucket + ms;
+  const uint32_t half = mmax < kLeafHalf ? mmax : kLeafHalf;
+  const uint32_t cw = (half + 1) >> 1;                           // cursor words
+  uint16_t* cur = reinterpret_cast<uint16_t*>(sh);               // [half]
+  uint16_t* bkt = reinterpret_cast<uint16_t*>(sh + cw);          // [mmax] buckets; later H
+  const uint32_t ms = (mmax + 1) & ~1u;
+  uint16_t* Nn = scratch + (uint64_t)blockIdx.x * 2 * ms;
   uint16_t* Hg = Nn + ms;
-  const uint32_t tid = threadIdx.x;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr uint32_t NW = BLOCK / 32;
 
   for (uint64_t g = blockIdx.x; g < nleaves; g += gridDim.x) {
     const LeafDesc L = leaf_desc(J, E, g);
@@ -190,129 +203,72 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
         l2_prefetch(draws + Ln.lo, (size_t)(Ln.hi - Ln.lo) * 2);
       }
     }
-    const uint32_t nwords = (m + 1) >> 1;
-    for (uint32_t w = tid; w < nwords; w += BLOCK) {
-      sh[w] = 0;
-      reinterpret_cast<uint32_t*>(Hg)[w] = 0;  // H(p) = none unless set in step 4
-    }
-    __syncthreads();
-    // 1. histogram of targets (steps s = 1 .. m-1; dr[0] is unused); draws
-    //    are read 8 at a time when the leaf is 16-byte aligned
-    const bool vec = ((((uintptr_t)dr) & 15) == 0);
-    if (vec) {
-      const uint4* dv = reinterpret_cast<const uint4*>(dr);
-      const uint32_t nv = m >> 3;
-#pragma unroll 2
-      for (uint32_t q = tid; q < nv; q += BLOCK) {
-        const uint4 w = dv[q];
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int h = 0; h < 8; ++h) {
-          const uint32_t j = (ws[h >> 1] >> ((h & 1) << 4)) & 0xFFFFu;
-          if (q != 0 || h != 0) atomicAdd(&sh[j >> 1], 1u << ((j & 1) << 4));
-        }
-      }
-      for (uint32_t s = (nv << 3) + tid; s < m; s += BLOCK) {
-        if (s == 0) continue;
-        const uint32_t j = dr[s];
-        atomicAdd(&sh[j >> 1], 1u << ((j & 1) << 4));
-      }
-    } else {
+    for (uint32_t T0 = 0; T0 < m; T0 += kLeafHalf) {
+      const uint32_t nt = min(kLeafHalf, m - T0);  // targets [T0, T0+nt)
+      for (uint32_t w = tid; w < ((nt + 1) >> 1); w += BLOCK) sh[w] = 0;
+      __syncthreads();
+      // 1. histogram of this half's targets (steps s = 1 .. m-1)
 #pragma unroll 4
       for (uint32_t s = 1 + tid; s < m; s += BLOCK) {
-        const uint32_t j = dr[s];
-        atomicAdd(&sh[j >> 1], 1u << ((j & 1) << 4));
+        const uint32_t j = (uint32_t)dr[s] - T0;
+        if (j < nt) atomicAdd(&sh[j >> 1], 1u << ((j & 1) << 4));
       }
-    }
-    __syncthreads();
-    // 2. bucket starts
-    scan_counts16(c16, m, warp_tot);
-    __syncthreads();
-    // 3. scatter step ids into their target's bucket (order inside a bucket is arbitrary)
-    if (vec) {
-      const uint4* dv = reinterpret_cast<const uint4*>(dr);
-      const uint32_t nv = m >> 3;
-#pragma unroll 2
-      for (uint32_t q = tid; q < nv; q += BLOCK) {
-        const uint4 w = dv[q];
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int h = 0; h < 8; ++h) {
-          const uint32_t j = (ws[h >> 1] >> ((h & 1) << 4)) & 0xFFFFu;
-          if (q != 0 || h != 0) {
-            const uint32_t sh16 = (j & 1) << 4;
-            const uint32_t old = atomicAdd(&sh[j >> 1], 1u << sh16);
-            bucket[(old >> sh16) & 0xFFFFu] = (uint16_t)((q << 3) + h);
-          }
-        }
-      }
-      for (uint32_t s = (nv << 3) + tid; s < m; s += BLOCK) {
-        if (s == 0) continue;
-        const uint32_t j = dr[s];
-        const uint32_t sh16 = (j & 1) << 4;
-        const uint32_t old = atomicAdd(&sh[j >> 1], 1u << sh16);
-        bucket[(old >> sh16) & 0xFFFFu] = (uint16_t)s;
-      }
-    } else {
+      __syncthreads();
+      if (g_leaf_stop <= 1) continue;
+      // 2. bucket starts
+      scan_counts16(cur, nt, warp_tot);
+      __syncthreads();
+      if (g_leaf_stop <= 2) continue;
+      // 3. scatter step ids into their target's bucket (shared memory)
 #pragma unroll 4
       for (uint32_t s = 1 + tid; s < m; s += BLOCK) {
-        const uint32_t j = dr[s];
-        const uint32_t sh16 = (j & 1) << 4;
-        const uint32_t old = atomicAdd(&sh[j >> 1], 1u << sh16);
-        bucket[(old >> sh16) & 0xFFFFu] = (uint16_t)s;
+        const uint32_t j = (uint32_t)dr[s] - T0;
+        if (j < nt) {
+          const uint32_t sh16 = (j & 1) << 4;
+          const uint32_t old = atomicAdd(&sh[j >> 1], 1u << sh16);
+          bkt[(old >> sh16) & 0xFFFFu] = (uint16_t)s;
+        }
       }
-    }
-    __syncthreads();
-    // 4. one lane per bucket entry e (a step, target p = j_e): scan p's bucket
-    //    (mean size-biased length 3) for N(e) = min{e' > e} and for whether e
-    //    is H(p) = min{e' > p}.  No sorting, no per-target divergence.
-    //    Batches of 8 entries per thread keep 8 (then 32) L2 loads in flight
-    //    instead of a chain of dependent loads per entry.
-    for (uint32_t a0 = tid; a0 + 1 < m; a0 += 8 * BLOCK) {
-      uint32_t e[8], p[8], st[8], en[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t a = a0 + k * BLOCK;
-        e[k] = (a + 1 < m) ? (uint32_t)bucket[a] : 0u;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) p[k] = (a0 + k * BLOCK + 1 < m) ? (uint32_t)dr[e[k]] : 0u;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        en[k] = c16[p[k]];
-        st[k] = p[k] ? (uint32_t)c16[p[k] - 1] : 0u;
-      }
-      uint32_t best[8], between[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {  // first 4 entries of every bucket, all loads in flight
-        best[k] = 0xFFFFFFFFu; between[k] = 0;
-        uint32_t x[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = (st[k] + u < en[k]) ? (uint32_t)bucket[st[k] + u] : 0u;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (st[k] + u < en[k]) {
-            best[k] = (x[u] > e[k] && x[u] < best[k]) ? x[u] : best[k];
-            between[k] += (x[u] > p[k] && x[u] < e[k]) ? 1u : 0u;
+      __syncthreads();
+      if (g_leaf_stop <= 3) continue;
+      // 4. per target (lane-consecutive targets, warps interleaved): sort the
+      //    bucket in place (insertion; buckets hold ~1 step, ln(m/p) near 0),
+      //    link successors N, H(p) = first step > p targeting p.
+      for (uint32_t base = wid * 32; base < nt; base += NW * 32) {
+        const uint32_t pl = base + lane;
+        if (pl < nt) {
+          const uint32_t p = T0 + pl;
+          const uint32_t en = cur[pl];
+          const uint32_t st = pl ? (uint32_t)cur[pl - 1] : 0u;
+          for (uint32_t a = st + 1; a < en; ++a) {
+            const uint16_t v = bkt[a];
+            uint32_t b = a;
+            while (b > st && bkt[b - 1] > v) { bkt[b] = bkt[b - 1]; --b; }
+            bkt[b] = v;
           }
+          uint32_t H = 0;
+          if (en > st) {
+            uint32_t prev = bkt[st];
+            H = (prev > p) ? prev : 0u;
+            for (uint32_t a = st + 1; a < en; ++a) {
+              const uint32_t cur_s = bkt[a];
+              if (H == 0) H = cur_s;  // first step after a self-step (prev == p)
+              Nn[prev] = (uint16_t)cur_s;
+              prev = cur_s;
+            }
+            Nn[prev] = 0;
+          }
+          Hg[p] = (uint16_t)H;
         }
       }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        for (uint32_t b = st[k] + 4; b < en[k]; ++b) {  // long buckets (targets near 0)
-          const uint32_t x = bucket[b];
-          best[k] = (x > e[k] && x < best[k]) ? x : best[k];
-          between[k] += (x > p[k] && x < e[k]) ? 1u : 0u;
-        }
-        if (a0 + k * BLOCK + 1 < m) {
-          Nn[e[k]] = (uint16_t)(best[k] == 0xFFFFFFFFu ? 0u : best[k]);
-          if (e[k] > p[k] && between[k] == 0) Hg[p[k]] = (uint16_t)e[k];
-        }
-      }
+      __syncthreads();
     }
+    if (g_leaf_stop <= 4) continue;
+    // H of every target into shared memory (over the bucket area)
+    for (uint32_t w = tid; w < ((m + 1) >> 1); w += BLOCK)
+      reinterpret_cast<uint32_t*>(bkt)[w] = reinterpret_cast<const uint32_t*>(Hg)[w];
     __syncthreads();
-    for (uint32_t w = tid; w < nwords; w += BLOCK) sh[w] = reinterpret_cast<const uint32_t*>(Hg)[w];
-    __syncthreads();
+    const uint16_t* Hs = bkt;
     // 5. chase and gather: final[i] = orig[W(N(i))] or orig[j_i]; final[0] = orig[W(0)]
     //    (batches of 8 outputs per thread: the N/draw loads, then the data
     //    gathers, are in flight together)
@@ -333,7 +289,7 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
           src = d[k];
         } else {
           uint32_t y = x[k], h;
-          while ((h = c16[y]) != 0) y = h;
+          while ((h = Hs[y]) != 0) y = h;
           src = y;
         }
         if (i < m) v[k] = src_in[src];
@@ -371,6 +327,8 @@ __global__ void leaf_serial_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
 }
 
 // ---------------------------------------------------------------- launchers
+void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int)); }
+
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
                           unsigned long long* bits, cudaStream_t st) {
   if (!nleaves) return;
@@ -382,15 +340,20 @@ void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nle
   count_launch();
 }
 
+static size_t leaf_apply_smem(uint32_t mmax) {
+  const uint32_t half = mmax < kLeafHalf ? mmax : kLeafHalf;
+  return (size_t)((half + 1) / 2) * 4 + (size_t)((mmax + 1) / 2) * 4;
+}
+
 template <typename V>
 static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, const void* in, void* out,
                          const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid,
                          cudaStream_t st) {
-  size_t smem = (size_t)((mmax + 1) / 2) * 4;
+  size_t smem = leaf_apply_smem(mmax);
   if (mmax > 8192) {
-    auto k = leaf_apply_kernel<V, 512>;
+    auto k = leaf_apply_kernel<V, 1024>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax);
+    k<<<grid, 1024, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax);
   } else {
     auto k = leaf_apply_kernel<V, 256>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -402,7 +365,7 @@ static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nlea
 uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms) {
   // Persistent CTAs: as many as fit (the per-CTA scratch is reused per leaf and
   // stays L2-resident).
-  size_t smem = (size_t)((mmax + 1) / 2) * 4;
+  size_t smem = leaf_apply_smem(mmax);
   size_t fit = (size_t)(220 * 1024) / (smem + 2048);
   int per_sm = (int)std::max((size_t)1, std::min(fit, (size_t)(mmax > 8192 ? 2 : 8)));
   uint64_t g = (uint64_t)num_sms * per_sm;

@@ -18,6 +18,8 @@ void launch_leaf_apply(int eb, const ArrayJob& J, const ExplicitTask& E, uint64_
 void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, void* out,
                         unsigned long long* bits, cudaStream_t st);
 
+void debug_set_leaf_stop(int v);
+
 // merge.cu
 struct LevelTail {            // device-side view used by the all-levels tail decoder
   PairPlan* plans;
