@@ -320,9 +320,9 @@ __device__ __forceinline__ uint64_t warp_rank(const StreamDesc& sd, const uint64
 // totals give every one its rank'.  One F load per position, one B load + one
 // F store per one, one output store per position -- all coalesced.
 template <typename V, int BLOCK, int CPW>
-__device__ __forceinline__ void segment_tile(V* __restrict__ pio, V* __restrict__ pout, const StreamDesc& sd,
-                                             uint64_t n1, uint64_t t, uint64_t p0, uint32_t len, uint64_t rank0,
-                                             uint32_t* wsum) {
+__device__ __forceinline__ uint32_t segment_tile(V* __restrict__ pio, V* __restrict__ pout, const StreamDesc& sd,
+                                                 uint64_t n1, uint64_t t, uint64_t p0, uint32_t len, uint64_t rank0,
+                                                 uint32_t* wsum) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t wbase = wid * 32 * CPW;
   uint32_t mword = 0;
@@ -348,9 +348,12 @@ __device__ __forceinline__ void segment_tile(V* __restrict__ pio, V* __restrict_
   const uint32_t round_base = x - cnt;
   if (lane == 31) wsum[wid] = x;
   __syncthreads();
-  uint32_t before = 0;
+  uint32_t before = 0, total = 0;
 #pragma unroll
-  for (int w = 0; w < BLOCK / 32; ++w) before += (w < (int)wid) ? wsum[w] : 0u;
+  for (int w = 0; w < BLOCK / 32; ++w) {
+    before += (w < (int)wid) ? wsum[w] : 0u;
+    total += wsum[w];
+  }
   const uint64_t qbase = n1 + rank0 + before;  // position of this warp's first B element
   const uint32_t ltmask = ~(0xffffffffu >> lane);
   // all loads of the tile first (independent, in flight together), then all
@@ -382,25 +385,27 @@ __device__ __forceinline__ void segment_tile(V* __restrict__ pio, V* __restrict_
       pout[p] = f[k];
     }
   }
+  return total;
 }
 
-template <typename V, int BLOCK, int CPW>
-__global__ void __launch_bounds__(BLOCK, 4) merge_segment_kernel(V* __restrict__ in, V* __restrict__ out,
-                                                              const PairPlan* __restrict__ plans,
-                                                              const uint64_t* __restrict__ rank,
-                                                              const uint64_t* __restrict__ segs, uint32_t h,
-                                                              uint32_t tpp) {
+template <typename V, int BLOCK, int CPW, int Q, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) merge_segment_kernel(V* __restrict__ in, V* __restrict__ out,
+                                                                 const PairPlan* __restrict__ plans,
+                                                                 const uint64_t* __restrict__ rank,
+                                                                 const uint64_t* __restrict__ segs, uint32_t h,
+                                                                 uint32_t tpp) {
+  // Q consecutive tiles per CTA: the plan loads and the rank-table query are
+  // paid once, later tiles carry the rank from the block totals.
   constexpr uint32_t T = BLOCK * CPW;
-  __shared__ uint32_t wsum[BLOCK / 32];
+  __shared__ uint32_t wsum[2][BLOCK / 32];
   __shared__ uint64_t rank0_s;
   const uint64_t g = blockIdx.x / tpp, tau = blockIdx.x - g * tpp;
   const PairPlan* Pp = plans + g;
   if (h >= Pp->nseg) return;
   const uint64_t* sg = segs + g * kSMax;
   const uint64_t S0 = sg[h], S1 = (h + 1 < Pp->nseg) ? sg[h + 1] : Pp->X;
-  const uint64_t p0 = S0 + tau * T;
+  uint64_t p0 = S0 + tau * (uint64_t)(T * Q);
   if (p0 >= S1) return;
-  const uint32_t len = (uint32_t)min((uint64_t)T, S1 - p0);
   const uint64_t n1 = Pp->n1, t = Pp->t;
   const StreamDesc sd = Pp->sd;
   if (threadIdx.x < 32) {
@@ -410,7 +415,15 @@ __global__ void __launch_bounds__(BLOCK, 4) merge_segment_kernel(V* __restrict__
     if (threadIdx.x == 0) rank0_s = r0;
   }
   __syncthreads();
-  segment_tile<V, BLOCK, CPW>(in + Pp->s, out + Pp->s, sd, n1, t, p0, len, rank0_s, wsum);
+  uint64_t rk = rank0_s;
+  V* pio = in + Pp->s;
+  V* pout = out + Pp->s;
+#pragma unroll 1
+  for (int qi = 0; qi < Q && p0 < S1; ++qi) {
+    const uint32_t len = (uint32_t)min((uint64_t)T, S1 - p0);
+    rk += segment_tile<V, BLOCK, CPW>(pio, pout, sd, n1, t, p0, len, rk, wsum[qi & 1]);
+    p0 += T;
+  }
 }
 
 // The remaining (small) segments of every pair, one CTA per pair, in order.
@@ -465,6 +478,21 @@ constexpr int kSegBlock = 256;
 constexpr int kSegCPW = 8;  // 2048 positions per tile
 uint32_t merge_tile(int eb) { (void)eb; return kSegBlock * kSegCPW; }
 
+// segment-kernel shape (tuning knob, see sk_debug_set key 2): CPW chunks per
+// warp (tile = 256*CPW positions), Q tiles per CTA, min CTAs per SM
+static int g_seg_variant = 0;
+void debug_set_seg_variant(int v) { g_seg_variant = v; }
+
+template <typename V, int CPW, int Q, int MINB>
+static void seg_launch(void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
+                       const uint64_t* segs, uint32_t h, uint64_t seglen, cudaStream_t st) {
+  constexpr uint32_t T = kSegBlock * CPW;
+  const uint32_t tpp = (uint32_t)((seglen + T * Q - 1) / (T * Q));
+  merge_segment_kernel<V, kSegBlock, CPW, Q, MINB><<<(unsigned)(npairs * tpp), kSegBlock, 0, st>>>(
+      (V*)in, (V*)out, plans, rank, segs, h, tpp);
+  count_launch();
+}
+
 template <typename V>
 static void merge_round_t(void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
                           const uint64_t* segs, const uint64_t* seglen_max_host, cudaStream_t st) {
@@ -472,10 +500,16 @@ static void merge_round_t(void* in, void* out, const PairPlan* plans, uint64_t n
   constexpr uint32_t T = kSegBlock * kSegCPW;
   uint32_t h = 0;
   for (; h < (uint32_t)kSMax && seglen_max_host[h] > T; ++h) {
-    const uint32_t tpp = (uint32_t)((seglen_max_host[h] + T - 1) / T);
-    merge_segment_kernel<V, kSegBlock, kSegCPW><<<(unsigned)(npairs * tpp), kSegBlock, 0, st>>>(
-        (V*)in, (V*)out, plans, rank, segs, h, tpp);
-    count_launch();
+    const uint64_t L = seglen_max_host[h];
+    switch (g_seg_variant) {
+      case 1: seg_launch<V, 4, 4, 8>(in, out, plans, npairs, rank, segs, h, L, st); break;
+      case 2: seg_launch<V, 4, 8, 8>(in, out, plans, npairs, rank, segs, h, L, st); break;
+      case 3: seg_launch<V, 8, 4, 4>(in, out, plans, npairs, rank, segs, h, L, st); break;
+      case 4: seg_launch<V, 16, 2, 2>(in, out, plans, npairs, rank, segs, h, L, st); break;
+      case 5: seg_launch<V, 8, 2, 4>(in, out, plans, npairs, rank, segs, h, L, st); break;
+      case 6: seg_launch<V, 4, 16, 8>(in, out, plans, npairs, rank, segs, h, L, st); break;
+      default: seg_launch<V, 8, 8, 4>(in, out, plans, npairs, rank, segs, h, L, st); break;
+    }
   }
   merge_tail_kernel<V, kSegBlock, kSegCPW><<<(unsigned)npairs, kSegBlock, 0, st>>>((V*)in, (V*)out, plans, rank,
                                                                                  segs, h);
