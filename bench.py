@@ -8,7 +8,7 @@ bit-exact with the reference) of the resident 4 GiB array.  Timing: CUDA
 events on the launching stream, barrier + synchronize on both sides, max over
 ranks.  The array (4 GiB) is 32x the L2, so no flush is needed between steps.
 
-Extra keys: roofline (dominant kernel = the merge-round window kernel),
+Extra keys: roofline (dominant kernel = one merge round, segment-pass kernels),
 cpu_baseline (the C oracle port on the host cores, bounded sample), e2e
 (through the C ABI host entry with pinned host buffers, H2D+D2H inside the
 timed region), gpu_launches, clocks.
@@ -200,8 +200,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1508_03167_b200 as sk
     from paper_1508_03167_b200 import _lib
+    from paper_1508_03167_b200 import distributed as D
     lib = _lib.load()
-    n = 1 << args.log2n
+    n = 1 << args.log2n           # elements per GPU (weak scaling)
+    n_total = n * world
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
     x = torch.randint(-2 ** 31, 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
     stream = torch.cuda.current_stream()
@@ -209,13 +211,20 @@ def main():
     bits = ctypes.c_uint64(0)
 
     def step():
-        _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), 4, n, 65536, 0, None, sp))
+        if world == 1:
+            _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), 4, n, 65536, 0, None, sp))
+        else:  # contiguous shards of one n_total array; spanning rounds exchange over NCCL
+            D.merge_shuffle_sharded(x, n_total, 65536, 0)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     # one checked step: bits equal the reference's for this n (seed 0)
-    _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), 4, n, 65536, 0, ctypes.byref(bits), sp))
+    if world == 1:
+        _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), 4, n, 65536, 0, ctypes.byref(bits),
+                                                 sp))
+    else:
+        bits.value = D.merge_shuffle_sharded(x, n_total, 65536, 0)
 
     lib.sk_profile_enable(1)
     l0 = lib.sk_launch_count()
@@ -242,47 +251,64 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = world * n / (ms_per_step * 1e-3) / 1e9
+    value = n_total / (ms_per_step * 1e-3) / 1e9
 
-    # roofline: merge-round window kernel; algorithmic bytes per launch = one
-    # read + one write of the array (2 * 4 B * n)
+    # roofline: the dominant kernel is one merge round (merge_segment_kernel
+    # launches + merge_tail_kernel, stage 2); algorithmic bytes per round = one
+    # read + one write of the shard (2 * 4 B * n).
+    from paper_1508_03167_b200.shufflers import merge_plan
+    c_tot = merge_plan(n_total, 65536)[0]
+    local_rounds = c_tot - (world.bit_length() - 1)
     merge_ms = stage_ms[2]
-    merge_launches = max(1, stage_l[2])
-    per_launch_ms = merge_ms / merge_launches
+    rounds = max(1, local_rounds * args.steps)
+    per_round_ms = merge_ms / rounds
     alg_bytes = 2 * 4 * n
-    achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
+    achieved = alg_bytes / (per_round_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
     tr = traffic_from_profile()
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": tr.get("bytes_per_launch") if tr else None,
-            "peak_source": peak_kind, "kernel": "merge_level_kernel (one merge round)",
-            "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": round(per_launch_ms, 4),
+            "frac": round(achieved / peak, 4), "traffic": tr.get("bytes_per_round") if tr else None,
+            "peak_source": peak_kind,
+            "kernel": "one merge round (merge_segment_kernel launches + merge_tail_kernel)",
+            "algorithmic_bytes_per_round": alg_bytes, "avg_round_ms": round(per_round_ms, 4),
+            "launches_per_round": round(stage_l[2] / rounds, 2),
             "stage_ms_per_step": {k: round(stage_ms[i] / args.steps, 4) for i, k in
-                                  enumerate(["leaf_decode", "leaf_apply", "merge_window", "identity+tail",
+                                  enumerate(["leaf_decode", "leaf_apply", "merge_rounds", "identity+tail",
                                              "final_copy"])},
             "passes_per_step": round(ms_per_step / (alg_bytes / (peak * 1e9) * 1e3), 2)}
 
-    # e2e through the C ABI host entry (pinned host buffers, H2D + D2H inside)
+    # e2e through the public API with host buffers (pinned), H2D + D2H inside
     e2e = None
     if args.e2e_steps > 0:
         host = torch.empty(n, dtype=torch.int32, pin_memory=True)
         host.copy_(x.cpu())
         hp = ctypes.c_void_p(host.data_ptr())
-        _lib.check(lib.sk_merge_shuffle_parallel_host(hp, 4, n, 65536, 0, None, sp))  # warm
+
+        def e2e_step():
+            if world == 1:  # C ABI host entry: copy in, shuffle, copy out, sync
+                _lib.check(lib.sk_merge_shuffle_parallel_host(hp, 4, n, 65536, 0, ctypes.byref(bits), sp))
+            else:
+                x.copy_(host, non_blocking=True)
+                bits.value = D.merge_shuffle_sharded(x, n_total, 65536, 0)
+                host.copy_(x, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+
+        e2e_step()  # warm
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            _lib.check(lib.sk_merge_shuffle_parallel_host(hp, 4, n, 65536, 0, ctypes.byref(bits), sp))
+            e2e_step()
         el = time.perf_counter() - t0
         if dist:
             t = torch.tensor([el], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": round(world * n * args.e2e_steps / el / 1e9, 4), "unit": UNIT,
-               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n + 8,
-               "path": "sk_merge_shuffle_parallel_host (C ABI), pinned host buffer"}
+        e2e = {"value": round(n_total * args.e2e_steps / el / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * n_total, "d2h_bytes_per_step": 4 * n_total + 8 * world,
+               "path": ("sk_merge_shuffle_parallel_host (C ABI), pinned host buffer" if world == 1 else
+                        "per rank: pinned host shard -> device, merge_shuffle_sharded, device -> host")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -293,10 +319,12 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u32",
                 "data": "synthetic: uniform-random 32-bit payload (torch.Generator seed 1234+rank)",
-                "config": {"workload": f"merge_shuffle_parallel n=2^{args.log2n} uint32 uniform payload, "
-                                       "cutoff 65536 (16384 leaves, 14 merge rounds), seed 0",
+                "config": {"workload": f"merge_shuffle_parallel n=2^{args.log2n}*{world} uint32 uniform payload, "
+                                       f"cutoff 65536 ({1 << c_tot} leaves, {c_tot} merge rounds), seed 0",
                            "n_per_gpu": n, "elem_bytes": 4, "cutoff": 65536, "seed": 0,
-                           "parallelism": "replicas" if world > 1 else "1 GPU",
+                           "n_total": n_total,
+                           "parallelism": (f"{world} contiguous shards; top {world.bit_length() - 1} rounds "
+                                           "exchange over NCCL all-gather") if world > 1 else "1 GPU",
                            "l2": "input 4 GiB >> 126 MB L2; no flush needed",
                            "bits_per_shuffle": int(bits.value)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

@@ -48,6 +48,17 @@ int sk_merge_shuffle_parallel(void *data, int elem_bytes, uint64_t n, uint64_t c
 int sk_merge_shuffle_parallel_host(void *host_data, int elem_bytes, uint64_t n, uint64_t cutoff, uint64_t seed,
                                    uint64_t *bits_out, void *stream);
 
+/* One GPU's share of merge_shuffle_parallel on an n_total-element array that is
+ * sharded contiguously by leaf blocks (multi-GPU, SURVEY.md §8 e): `data` holds
+ * global elements [(n*blk0)>>c, (n*(blk0+nblk))>>c); runs the leaves blk0 ..
+ * blk0+nblk-1 and merge rounds 1..`rounds` whose pairs lie inside the shard
+ * (same substream indices as the whole-array schedule).  nblk is a power of
+ * two dividing blk0; rounds <= log2(nblk).  *bits_out = bits of those tasks.
+ * The remaining (cross-shard) rounds are driven by
+ * paper_1508_03167_b200.distributed with sk_merge_range. */
+int sk_merge_shuffle_shard(void *data, int elem_bytes, uint64_t n_total, uint64_t cutoff, uint64_t seed,
+                           uint64_t blk0, uint64_t nblk, int rounds, uint64_t *bits_out, void *stream);
+
 /* `batch` independent arrays of `len` elements, back to back; array t is
  * shuffled as merge_shuffle_parallel with BitSource(substream_seed(seed, t))
  * (the per-trial key of _kernels.py:219-220 and cli.py:136).

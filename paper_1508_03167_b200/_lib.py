@@ -21,6 +21,7 @@ _u64p = ctypes.POINTER(ctypes.c_uint64)
 SIGNATURES = {
     "sk_merge_shuffle_parallel": (_int, [_vp, _int, _u64, _u64, _u64, _u64p, _vp]),
     "sk_merge_shuffle_parallel_host": (_int, [_vp, _int, _u64, _u64, _u64, _u64p, _vp]),
+    "sk_merge_shuffle_shard": (_int, [_vp, _int, _u64, _u64, _u64, _u64, _u64, _int, _u64p, _vp]),
     "sk_batched_shuffle": (_int, [_vp, _int, _u64, _u64, _u64, _u64, _u64p, _vp]),
     "sk_fy_range": (_int, [_vp, _int, _u64, _u64, _u64p, _vp]),
     "sk_merge_range": (_int, [_vp, _int, _u64, _u64, _u64, _u64p, _vp]),

@@ -225,7 +225,7 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
   uint64_t nbits_key = 1;
   {
     uint64_t mx = 0;
-    for (auto& L : lv) mx = std::max(mx, (uint64_t)L.LJ.J.batch * L.LJ.J.len);
+    for (auto& L : lv) mx = std::max(mx, (uint64_t)L.LJ.J.batch * L.LJ.J.len);  // global positions < this
     if (lv[0].LJ.E.active) mx = lv[0].LJ.E.lo + lv[0].LJ.E.n1 + lv[0].LJ.E.n2;
     while ((1ULL << nbits_key) <= mx && nbits_key < 64) ++nbits_key;
   }
@@ -294,12 +294,12 @@ static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* oth
 static std::vector<LevelBufs> make_levels(const ArrayJob& J, int eb) {
   std::vector<LevelBufs> lv;
   (void)eb;
-  for (int r = 1; r <= J.c; ++r) {
+  for (int r = 1; r <= J.rmax; ++r) {
     LevelBufs L;
     L.LJ.J = J;
     L.LJ.E = ExplicitTask{};
     L.LJ.r = r;
-    L.npairs = J.batch << (J.c - r);
+    L.npairs = J.batch << (J.lognblk - r);
     L.LJ.npairs = L.npairs;
     uint64_t Nmax = (J.len >> (J.c - r)) + 2;
     L.sbs = (Nmax + 1 + 511) / 512 + 1;
@@ -310,14 +310,16 @@ static std::vector<LevelBufs> make_levels(const ArrayJob& J, int eb) {
 
 // The whole tasked schedule for a batch of arrays (batch = 1: one array).
 static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d_bits, cudaStream_t st) {
-  const uint64_t ntot = J.batch * J.len;
+  const uint64_t ntot = (J.lognblk == J.c && J.blk0 == 0)
+                            ? J.batch * J.len
+                            : bound_at(J.len, J.blk0 + (1ULL << J.lognblk), J.c) - bound_at(J.len, J.blk0, J.c);
   if (ntot == 0) return;
   setup_pool_once();
   Arena A;
   cudaStream_t ps = side_stream();
   std::vector<LevelBufs> lv = make_levels(J, eb);
   void* scratch = A.alloc<unsigned char>(ntot * eb, st);
-  const uint64_t nleaves = J.batch * J.q;
+  const uint64_t nleaves = J.batch << J.lognblk;
   const uint64_t mmax = (J.len + J.q - 1) >> J.c;  // largest leaf: ceil(len / q)
   ExplicitTask E0{};
   try {
@@ -407,7 +409,7 @@ static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t
   std::vector<LevelBufs> lv(1);
   LevelBufs& L = lv[0];
   uint64_t N = l - j;
-  L.LJ.J = ArrayJob{1, N, 1, 0, 0, 0};
+  L.LJ.J = make_job(1, N, 0, 0, 0);
   L.LJ.E = ExplicitTask{1, j, k - j, l - k, sd};
   L.LJ.r = 1;
   L.LJ.npairs = 1;
@@ -447,7 +449,7 @@ static void run_single_leaf(int eb, void* data, uint64_t lo, uint64_t hi, const 
   setup_pool_once();
   Arena A;
   uint64_t m = hi - lo;
-  ArrayJob J{1, m, 1, 0, 0, 0};
+  ArrayJob J = make_job(1, m, 0, 0, 0);
   ExplicitTask E{1, lo, m, 0, sd};
   try {
     if (m <= 65536) {
@@ -556,7 +558,7 @@ int sk_merge_shuffle_parallel(void* data, int elem_bytes, uint64_t n, uint64_t c
   CK(cudaMallocAsync((void**)&d_bits, 8, st));
   CK(cudaMemsetAsync(d_bits, 0, 8, st));
   int c = plan_c(n, cutoff);
-  ArrayJob J{1, n, 1ULL << c, c, 0, seed};
+  ArrayJob J = make_job(1, n, c, 0, seed);
   try {
     run_job(elem_bytes, data, J, d_bits, st);
     fetch_bits(d_bits, bits_out, 1, st);
@@ -590,6 +592,36 @@ int sk_merge_shuffle_parallel_host(void* host_data, int elem_bytes, uint64_t n, 
   SK_CATCH
 }
 
+int sk_merge_shuffle_shard(void* data, int elem_bytes, uint64_t n_total, uint64_t cutoff, uint64_t seed,
+                           uint64_t blk0, uint64_t nblk, int rounds, uint64_t* bits_out, void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (cutoff == 0) cutoff = 65536;
+  const int c = plan_c(n_total, cutoff);
+  int lg = 0;
+  while ((1ULL << lg) < nblk) ++lg;
+  if (nblk == 0 || (1ULL << lg) != nblk || blk0 % nblk || blk0 + nblk > (1ULL << c) || rounds < 0 || rounds > lg) {
+    set_err("shard: nblk must be a power of two dividing blk0, within 2^c blocks; rounds <= log2(nblk)");
+    return SK_EINVAL;
+  }
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  unsigned long long* d_bits;
+  CK(cudaMallocAsync((void**)&d_bits, 8, st));
+  CK(cudaMemsetAsync(d_bits, 0, 8, st));
+  ArrayJob J = make_job(1, n_total, c, 0, seed);
+  J.blk0 = blk0; J.lognblk = lg; J.rmax = rounds; J.elem0 = bound_at(n_total, blk0, c);
+  try {
+    run_job(elem_bytes, data, J, d_bits, st);
+    fetch_bits(d_bits, bits_out, 1, st);
+  } catch (...) {
+    cudaFreeAsync(d_bits, st);
+    throw;
+  }
+  CK(cudaFreeAsync(d_bits, st));
+  SK_CATCH
+}
+
 int sk_batched_shuffle(void* data, int elem_bytes, uint64_t batch, uint64_t len, uint64_t cutoff, uint64_t seed,
                        uint64_t* bits_out, void* stream) {
   if (int e = check_eb(elem_bytes)) return e;
@@ -602,7 +634,7 @@ int sk_batched_shuffle(void* data, int elem_bytes, uint64_t batch, uint64_t len,
   CK(cudaMallocAsync((void**)&d_bits, (batch ? batch : 1) * 8, st));
   CK(cudaMemsetAsync(d_bits, 0, (batch ? batch : 1) * 8, st));
   int c = plan_c(len, cutoff);
-  ArrayJob J{batch, len, 1ULL << c, c, 1, seed};
+  ArrayJob J = make_job(batch, len, c, 1, seed);
   try {
     run_job(elem_bytes, data, J, d_bits, st);
     fetch_bits(d_bits, bits_out, batch, st);

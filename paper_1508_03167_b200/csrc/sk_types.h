@@ -18,7 +18,22 @@ struct ArrayJob {
   int c;           // merge rounds
   int keymode;
   uint64_t seed;
+  // shard of the schedule (multi-GPU): blocks [blk0, blk0 + 2^lognblk) of each
+  // array, rounds 1..rmax; element 0 of the buffer is global element elem0.
+  // A whole job has blk0 = 0, lognblk = c, rmax = c, elem0 = 0.
+  uint64_t blk0;
+  int lognblk;
+  int rmax;
+  uint64_t elem0;
 };
+
+__host__ __device__ __forceinline__ ArrayJob make_job(uint64_t batch, uint64_t len, int c, int keymode,
+                                                       uint64_t seed) {
+  ArrayJob J;
+  J.batch = batch; J.len = len; J.q = 1ULL << c; J.c = c; J.keymode = keymode; J.seed = seed;
+  J.blk0 = 0; J.lognblk = c; J.rmax = c; J.elem0 = 0;
+  return J;
+}
 
 __host__ __device__ __forceinline__ uint64_t array_key(const ArrayJob& J, uint64_t a) {
   return J.keymode ? substream_seed(J.seed, a) : J.seed;
@@ -66,8 +81,8 @@ __host__ __device__ __forceinline__ LeafDesc leaf_desc(const ArrayJob& J, const 
     L.lo = E.lo; L.hi = E.lo + E.n1; L.array = 0; L.sd = E.sd;
     return L;
   }
-  uint64_t a = g >> J.c, i = g & (J.q - 1);
-  uint64_t base = a * J.len;
+  uint64_t a = g >> J.lognblk, i = J.blk0 + (g & ((1ULL << J.lognblk) - 1));
+  uint64_t base = a * J.len - J.elem0;
   L.lo = base + bound_at(J.len, i, J.c);
   L.hi = base + bound_at(J.len, i + 1, J.c);
   L.array = a;
@@ -93,10 +108,10 @@ __host__ __device__ __forceinline__ void pair_geom(const LevelJob& LJ, uint64_t 
     return;
   }
   const ArrayJob& J = LJ.J;
-  int sh = J.c - LJ.r;  // pairs per array = 2^sh
+  int sh = J.lognblk - LJ.r;  // pairs per array (shard) = 2^sh
   uint64_t a = g >> sh, k = g & ((1ULL << sh) - 1);
-  uint64_t i = k << LJ.r, p = 1ULL << (LJ.r - 1);
-  uint64_t base = a * J.len;
+  uint64_t i = J.blk0 + (k << LJ.r), p = 1ULL << (LJ.r - 1);
+  uint64_t base = a * J.len - J.elem0;
   uint64_t j = bound_at(J.len, i, J.c), kk = bound_at(J.len, i + p, J.c), l = bound_at(J.len, i + 2 * p, J.c);
   s = base + j; n1 = kk - j; n2 = l - kk;
   sd = fresh_stream(substream_seed(array_key(J, a), (uint64_t)LJ.r * J.q + i));

@@ -192,3 +192,26 @@ def test_determinism_and_seed_sensitivity():
     b, _ = gpu_perm(300_000, 1000, 5, torch.int32)
     c, _ = gpu_perm(300_000, 1000, 6, torch.int32)
     assert torch.equal(a, b) and not torch.equal(a, c)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_schedule_on_one_gpu(world):
+    # the multi-GPU schedule (per-shard C-ABI calls + spanning-round merges),
+    # executed shard by shard on one device, equals the single-GPU result
+    from paper_1508_03167_b200 import distributed as D
+    n, cutoff, seed = (1 << 20) + 12345, 32768, 17
+    data = torch.arange(n, dtype=torch.int32, device="cuda")
+    bits = D.simulate_sharded(data, n, cutoff, seed, world)
+    ref, rbits = O.merge_shuffle_perm(n, cutoff, seed)
+    assert bits == rbits
+    assert np.array_equal(data.cpu().numpy(), ref.astype(np.int32))
+
+
+def test_config4_sharded_2p24_uint64_golden():
+    # BASELINE config 4: 8-way sharded code path, bit-exact on a 2^24 run
+    from paper_1508_03167_b200 import distributed as D
+    case = [c for c in G["merge_shuffle_parallel"] if c["n"] == (1 << 24)][0]
+    data = torch.arange(1 << 24, dtype=torch.int64, device="cuda")
+    bits = D.simulate_sharded(data, 1 << 24, None, case["seed"], 8)
+    assert bits == case["bits"]
+    assert sha(data.cpu().numpy().astype("<u8")) == case["sha_u64"]
