@@ -176,7 +176,7 @@ def run_reference(args, rank, world):
     n = 1 << args.log2n
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(n / (v * 1e9) * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"merge_shuffle_parallel n=2^{args.log2n} uint32 uniform payload, cutoff 65536",
                        "n": n, "elem_bytes": 4, "cutoff": 65536, "seed": 0, "parallelism": "host threads"},
@@ -202,8 +202,10 @@ def main():
     from paper_1508_03167_b200 import _lib
     from paper_1508_03167_b200 import distributed as D
     lib = _lib.load()
-    n = 1 << args.log2n           # elements per GPU (weak scaling)
-    n_total = n * world
+    # BASELINE config 3: ONE n = 2^30 array sharded contiguously over the
+    # ranks (strong scaling); each rank holds n_total / world elements
+    n_total = 1 << args.log2n
+    n = n_total // world
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
     x = torch.randint(-2 ** 31, 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g)
     stream = torch.cuda.current_stream()
@@ -317,15 +319,15 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                "scaling": "strong", "vs_baseline": None, "dtype": "u32",
                 "data": "synthetic: uniform-random 32-bit payload (torch.Generator seed 1234+rank)",
-                "config": {"workload": f"merge_shuffle_parallel n=2^{args.log2n}*{world} uint32 uniform payload, "
+                "config": {"workload": f"merge_shuffle_parallel n=2^{args.log2n} uint32 uniform payload over {world} GPU(s), "
                                        f"cutoff 65536 ({1 << c_tot} leaves, {c_tot} merge rounds), seed 0",
                            "n_per_gpu": n, "elem_bytes": 4, "cutoff": 65536, "seed": 0,
                            "n_total": n_total,
                            "parallelism": (f"{world} contiguous shards; top {world.bit_length() - 1} rounds "
                                            "exchange over NCCL all-gather") if world > 1 else "1 GPU",
-                           "l2": "input 4 GiB >> 126 MB L2; no flush needed",
+                           "l2": f"input {4 * n >> 20} MiB per GPU >> 126 MB L2; no flush needed",
                            "bits_per_shuffle": int(bits.value)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary()}

@@ -94,8 +94,8 @@ int sk_version(void);
 uint64_t sk_launch_count(void);       /* kernels launched by this library so far */
 void sk_profile_enable(int on);       /* record CUDA events around the data-path stages */
 /* stage times (ms, summed) and launch counts since enable: stage 0 leaf decode,
- * 1 leaf apply, 2 merge rounds (window kernel + identity region + tail apply),
- * 3 final copy; returns number of stages written.  Synchronizes. */
+ * 1 leaf apply, 2 merge rounds (segment-pass kernels), 3 identity region + tail
+ * apply, 4 final copy; returns number of stages written.  Synchronizes. */
 int sk_profile_read(double *ms_out, uint64_t *launches_out, int max_stages);
 
 #ifdef __cplusplus
