@@ -35,13 +35,18 @@ __device__ __forceinline__ uint64_t leaf_word(const StreamDesc& sd, uint64_t w) 
   return chunk(sd, w);
 }
 
+// Blocks of kDecodeBlock lanes: the decode is latency-bound with about one
+// warp per SM sub-partition, so each block's warps must land on distinct
+// schedulers (single-warp blocks were observed to share them).
+constexpr int kDecodeBlock = 128;
+
 template <bool FRESH>
-__global__ void __launch_bounds__(32) leaf_decode16_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
-                                                           uint16_t* __restrict__ draws,
-                                                           unsigned long long* __restrict__ bits) {
-  __shared__ uint32_t ring[16][32];
+__global__ void __launch_bounds__(kDecodeBlock) leaf_decode16_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
+                                                                     uint16_t* __restrict__ draws,
+                                                                     unsigned long long* __restrict__ bits) {
+  __shared__ uint32_t ring[16][kDecodeBlock];
   const uint32_t lane = threadIdx.x;
-  const uint64_t g = (uint64_t)blockIdx.x * 32 + lane;
+  const uint64_t g = (uint64_t)blockIdx.x * kDecodeBlock + lane;
   LeafDesc L;
   uint32_t m = 0;
   if (g < nleaves) {
@@ -71,6 +76,14 @@ __global__ void __launch_bounds__(32) leaf_decode16_kernel(ArrayJob J, ExplicitT
   uint32_t pos = 0;
   uint32_t lb = 31 - __clz(i | 1), v = 1, c = 0;
   uint32_t nb = 0;
+  // Draws are packed eight at a time (16-byte stores, most recent draw in the
+  // low bits) except in the 16-byte chunk holding draw m-1, whose upper bytes
+  // belong to the next leaf: those go out as single 16-bit stores.  Per-lane
+  // scattered 16-bit stores cost one L1 wavefront each and sat on the decode's
+  // critical path.
+  uint16_t* const head = reinterpret_cast<uint16_t*>(reinterpret_cast<uintptr_t>(wp) & ~(uintptr_t)15);
+  uint64_t plo = 0, phi = 0;
+  uint16_t* pend = head;  // draws in [wp + 1, pend) are packed, not yet stored
   while (__any_sync(0xffffffffu, i != 0)) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -92,10 +105,18 @@ __global__ void __launch_bounds__(32) leaf_decode16_kernel(ArrayJob J, ExplicitT
       const uint32_t x = __funnelshift_l(B, A, pos);
       const uint32_t cc = (c << k) | (x >> (32 - k));
       const uint32_t acc = (act && cc < b) ? 1u : 0u;
-      // predicated 16-bit store through a running pointer (wp == &dr[i])
-      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.global.u16 [%1], %2;\n}" ::"r"(acc), "l"(wp),
-                   "h"((unsigned short)cc)
-                   : "memory");
+      // predicated stores through a running pointer (wp == &dr[i])
+      const bool inhead = wp >= head;
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.global.u16 [%1], %2;\n}" ::"r"(
+                       inhead ? acc : 0u),
+                   "l"(wp), "h"((unsigned short)cc));
+      const bool push = acc && !inhead;
+      phi = push ? ((phi << 16) | (plo >> 48)) : phi;
+      plo = push ? ((plo << 16) | cc) : plo;
+      const uint32_t fl = (push && ((reinterpret_cast<uintptr_t>(wp) & 15) == 0)) ? 1u : 0u;
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.global.v2.u64 [%1], {%2, %3};\n}" ::"r"(fl),
+                   "l"(wp), "l"(plo), "l"(phi));
+      pend = fl ? wp : pend;
       wp -= acc;
       c = acc ? 0u : cc - b;
       v = acc ? 1u : (v << k) - b;
@@ -114,7 +135,12 @@ __global__ void __launch_bounds__(32) leaf_decode16_kernel(ArrayJob J, ExplicitT
       rd += cross ? 1u : 0u;
     }
   }
-  if (m >= 2) atomicAdd(&bits[L.array], (unsigned long long)nb);
+  if (m >= 2) {
+    // the last (< 8) packed draws: dr[1 ..], dr[1] in the low bits
+    const long rem = (long)(pend - (dr + 1));
+    for (long k = 0; k < rem; ++k) dr[1 + k] = (uint16_t)(k < 4 ? plo >> (16 * k) : phi >> (16 * (k - 4)));
+    atomicAdd(&bits[L.array], (unsigned long long)nb);
+  }
 }
 
 // Warp-segmented exclusive scan over `m` 16-bit counters packed in smem.
@@ -332,11 +358,11 @@ void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
                           unsigned long long* bits, cudaStream_t st) {
   if (!nleaves) return;
-  unsigned blocks = (unsigned)((nleaves + 31) / 32);
+  unsigned blocks = (unsigned)((nleaves + kDecodeBlock - 1) / kDecodeBlock);
   if (E.active && E.sd.plen != 0)
-    leaf_decode16_kernel<false><<<blocks, 32, 0, st>>>(J, E, nleaves, draws, bits);
+    leaf_decode16_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
   else
-    leaf_decode16_kernel<true><<<blocks, 32, 0, st>>>(J, E, nleaves, draws, bits);
+    leaf_decode16_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
   count_launch();
 }
 
