@@ -128,6 +128,8 @@ struct LevelBufs {
   uint64_t* segs = nullptr;                 // npairs x kSMax segment boundaries
   unsigned long long* seglen_max = nullptr;  // kSMax: longest segment h over pairs
   uint64_t seglen_host[kSMax] = {};
+  uint64_t* chains = nullptr;               // per tile: window starts of the tree merge
+  uint32_t tpp = 1;                          // tree tiles per pair
   // tails
   uint64_t total = 0;
   uint64_t* rec_key = nullptr;
@@ -172,11 +174,13 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
     L.segs = A.alloc<uint64_t>(L.npairs * kSMax, ps);
     L.seglen_max = A.alloc<unsigned long long>(kSMax, ps);
     CK(cudaMemsetAsync(L.seglen_max, 0, kSMax * 8, ps));
+    L.chains = A.alloc<uint64_t>(tree_chain_words(L.npairs, L.tpp), ps);
   }
   for (auto& L : lv) {
     uint64_t* csum = A.alloc<uint64_t>(rank_scan_scratch(L.npairs, L.sbs), ps);
     launch_rank_tables(L.LJ, L.sbs, L.rank, csum, ps);
     launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, L.segs, L.seglen_max, ps);
+    launch_tree_chains(eb, L.plans, L.npairs, L.rank, L.tpp, L.chains, ps);
   }
   CK(cudaGetLastError());
   // (the host synchronization below also orders the data stream's merge
@@ -277,7 +281,7 @@ static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* oth
   for (auto& L : lv) {
     {
       StageTimer tm(2, st);
-      launch_merge_round(eb, cur, other, L.plans, L.npairs, L.rank, L.segs, L.seglen_host, st);
+      launch_merge_round(eb, cur, other, L.plans, L.npairs, L.rank, L.segs, L.seglen_host, L.chains, L.tpp, st);
     }
     {
       StageTimer tm(3, st);
@@ -293,7 +297,6 @@ static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* oth
 
 static std::vector<LevelBufs> make_levels(const ArrayJob& J, int eb) {
   std::vector<LevelBufs> lv;
-  (void)eb;
   for (int r = 1; r <= J.rmax; ++r) {
     LevelBufs L;
     L.LJ.J = J;
@@ -301,6 +304,7 @@ static std::vector<LevelBufs> make_levels(const ArrayJob& J, int eb) {
     L.LJ.r = r;
     L.npairs = J.batch << (J.lognblk - r);
     L.LJ.npairs = L.npairs;
+    L.tpp = tree_tiles_per_pair(L.LJ, eb);
     uint64_t Nmax = (J.len >> (J.c - r)) + 2;
     L.sbs = (Nmax + 1 + 511) / 512 + 1;
     lv.push_back(L);
@@ -415,6 +419,7 @@ static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t
   L.LJ.npairs = 1;
   L.npairs = 1;
   L.sbs = (N + 1 + 511) / 512 + 1;
+  L.tpp = tree_tiles_per_pair(L.LJ, eb);
   try {
     unsigned char* scratch = A.alloc<unsigned char>(N * eb, st);
     fork_side(st, ps);
@@ -422,7 +427,7 @@ static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t
     // kernels address elements by absolute index; shift the scratch base so
     // index j lands on scratch[0].
     void* out_base = (void*)(scratch - j * eb);
-    launch_merge_round(eb, data, out_base, L.plans, 1, L.rank, L.segs, L.seglen_host, st);
+    launch_merge_round(eb, data, out_base, L.plans, 1, L.rank, L.segs, L.seglen_host, L.chains, L.tpp, st);
     launch_copy_tail_region(eb, data, out_base, L.plans, 1, st);
     CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
     launch_tail_apply(eb, out_base, L.dst, L.src, L.tmp, 2 * L.total, st);

@@ -179,14 +179,6 @@ __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
   a = lo; b = hi;
 }
 
-// TMA bulk prefetch of [p, p+bytes) (16-byte aligned interior) into L2.
-__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
-  const uintptr_t a0 = ((uintptr_t)p + 15) & ~(uintptr_t)15;
-  const uintptr_t a1 = ((uintptr_t)p + bytes) & ~(uintptr_t)15;
-  if (a1 > a0)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
-}
-
 // Leaf apply.  Targets are handled in halves of <= 32768 so that both the
 // 16-bit bucket cursors (64 KB) and the bucket array itself (<= 128 KB) live in
 // shared memory: histogram, scan, scatter and the per-target bucket sort are

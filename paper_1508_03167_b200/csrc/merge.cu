@@ -474,6 +474,438 @@ __global__ void __launch_bounds__(BLOCK) merge_tail_kernel(V* __restrict__ in, V
   }
 }
 
+// ------------------------------------------------------- merge round (tree)
+// One CTA per tile of segment 0 follows the tile through every segment: the
+// tile [a_0, b_0) of A positions, then the windows [a_{h+1}, b_{h+1}) =
+// [n1 + rank'(a_h), n1 + rank'(b_h)) -- the positions that receive its
+// carried A elements, which are also the B slots its ones consume.  The
+// windows of all tiles partition [0, X); a CTA reads in[] over its windows
+// once, writes out[] over them once, and carries the A elements from one
+// window to the next in shared memory: one read and one write per element
+// per round (the segment-pass kernel parks them in HBM: 1.5 + 1.5).  The
+// window starts a_h are data independent and precomputed per tile
+// (tree_chain_kernel, side stream); the CTA works window by window in
+// 2048-position chunks while a window has more than 32 positions, then one
+// warp finishes the short windows without block barriers.
+constexpr int kTreeBlock = 256;
+constexpr int kTreeCPW = 8;
+constexpr uint32_t kTreeChunk = kTreeBlock * kTreeCPW;
+constexpr int kTreeD = 24;  // stored window starts per tile (deeper ones are computed)
+
+uint32_t tree_tiles_per_pair(const LevelJob& LJ, int eb) {
+  uint64_t n1max;
+  if (LJ.E.active) n1max = LJ.E.n1;
+  else n1max = (1ULL << (LJ.r - 1)) * ((LJ.J.len + LJ.J.q - 1) >> LJ.J.c);
+  const uint64_t T0 = tree_tile(eb);
+  return (uint32_t)std::max<uint64_t>(1, (n1max + T0 - 1) / T0);
+}
+
+uint64_t tree_chain_words(uint64_t npairs, uint32_t tpp) { return npairs * (tpp + 1) * kTreeD; }
+
+__global__ void tree_chain_kernel(const PairPlan* __restrict__ plans, uint64_t npairs,
+                                  const uint64_t* __restrict__ rank, uint32_t tpp, uint32_t T0,
+                                  uint64_t* __restrict__ chains) {
+  const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= npairs * (tpp + 1)) return;
+  const uint64_t g = idx / (tpp + 1), tau = idx - g * (tpp + 1);
+  const PairPlan* Pp = plans + g;
+  const uint64_t n1 = Pp->n1, t = Pp->t;
+  const StreamDesc sd = Pp->sd;
+  const uint64_t* R = rank + Pp->rank_off;
+  uint64_t a = min(tau * (uint64_t)T0, n1);
+  uint64_t* o = chains + idx * kTreeD;
+  for (int h = 0; h < kTreeD; ++h) {
+    o[h] = a;
+    a = n1 + rank_bits(sd, R, a < t ? a : t);
+  }
+}
+
+void launch_tree_chains(int eb, const PairPlan* plans, uint64_t npairs, const uint64_t* rank, uint32_t tpp,
+                        uint64_t* chains, cudaStream_t st) {
+  if (!npairs) return;
+  const uint64_t n = npairs * (tpp + 1);
+  tree_chain_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(plans, npairs, rank, tpp, tree_tile(eb), chains);
+  count_launch();
+}
+
+// One chunk of a window: positions [p0, p0 + len), fbase = index of p0 in the
+// window (its F slot), bq = position of the chunk's first B element, obase =
+// F slot of the chunk's first one in the next window.  Window 0 reads F from
+// in[]; deeper windows from shared memory, compacted in place (a barrier
+// separates the chunk's loads from its stores).  Returns the chunk's ones.
+template <typename V, bool L0>
+__device__ __forceinline__ uint32_t tree_chunk(const V* __restrict__ pin, V* __restrict__ pout, V* Fs,
+                                               const StreamDesc& sd, uint64_t t, uint64_t p0, uint32_t len,
+                                               uint32_t fbase, uint64_t bq, uint32_t obase, uint32_t* wsum) {
+  constexpr int CPW = kTreeCPW;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t wbase = wid * 32 * CPW;
+  uint32_t mword = 0;
+  if (lane < (uint32_t)CPW) {
+    const uint32_t i = wbase + lane * 32;
+    if (i < len) {
+      const uint64_t p = p0 + i;
+      if (p < t) {
+        uint32_t nv = min(32u, len - i);
+        const uint64_t nt = t - p;
+        if (nt < nv) nv = (uint32_t)nt;
+        const uint32_t b = (uint32_t)(bits64_at(sd, p) >> 32);
+        mword = (nv == 32) ? b : (b & ~(0xffffffffu >> nv));
+      }
+    }
+  }
+  const uint32_t cnt = __popc(mword);
+  uint32_t x = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  const uint32_t round_base = x - cnt;
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  uint32_t before = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kTreeBlock / 32; ++w) {
+    before += (w < (int)wid) ? wsum[w] : 0u;
+    total += wsum[w];
+  }
+  const uint32_t ltmask = ~(0xffffffffu >> lane);
+  V f[CPW], b[CPW];
+  uint32_t qo[CPW];
+  uint32_t onemask = 0, inmask = 0;
+#pragma unroll
+  for (int k = 0; k < CPW; ++k) {
+    const uint32_t i = wbase + 32 * k + lane;
+    const uint32_t m = __shfl_sync(0xffffffffu, mword, k);
+    const uint32_t rb = __shfl_sync(0xffffffffu, round_base, k);
+    const bool in_t = i < len;
+    const bool one = in_t && ((m >> (31 - lane)) & 1u);
+    qo[k] = before + rb + __popc(m & ltmask);
+    inmask |= (in_t ? 1u : 0u) << k;
+    onemask |= (one ? 1u : 0u) << k;
+    if (in_t) f[k] = L0 ? pin[p0 + i] : Fs[fbase + i];
+    if (one) b[k] = pin[bq + qo[k]];
+  }
+  __syncthreads();  // loads of F (and of wsum) complete before the in-place stores
+#pragma unroll
+  for (int k = 0; k < CPW; ++k) {
+    const uint64_t p = p0 + wbase + 32 * k + lane;
+    if ((onemask >> k) & 1u) {
+      pout[p] = b[k];
+      Fs[obase + qo[k]] = f[k];
+    } else if ((inmask >> k) & 1u) {
+      pout[p] = f[k];
+    }
+  }
+  return total;
+}
+
+// Window-by-window fallback (F carried in a T0-element shared buffer): used
+// when a tile's windows do not fit the staging buffer or its chain is deeper
+// than the stored kTreeD starts.  Never taken for pseudo-random bit streams
+// in practice; kept exact for every input.
+template <typename V>
+__device__ void tree_windows_direct(const V* __restrict__ pin, V* __restrict__ pout, V* Fs, const StreamDesc& sd,
+                                    const uint64_t* R, uint64_t n1, uint64_t t, const uint64_t* ach,
+                                    const uint64_t* bch, uint32_t* wsum, uint64_t* nxt, V* wF) {
+  uint64_t a = ach[0], b = bch[0];
+  int h = 0;
+  while (b - a > 32) {
+    uint64_t a1, b1;
+    if (h + 1 < kTreeD) {
+      a1 = ach[h + 1];
+      b1 = bch[h + 1];
+    } else {
+      if (threadIdx.x < 32) {
+        const uint64_t ra = warp_rank(sd, R, a < t ? a : t, threadIdx.x);
+        const uint64_t rb = warp_rank(sd, R, b < t ? b : t, threadIdx.x);
+        if (threadIdx.x == 0) { nxt[0] = n1 + ra; nxt[1] = n1 + rb; }
+      }
+      __syncthreads();
+      a1 = nxt[0];
+      b1 = nxt[1];
+    }
+    uint32_t done = 0;
+    for (uint64_t p0 = a; p0 < b; p0 += kTreeChunk) {
+      const uint32_t len = (uint32_t)min((uint64_t)kTreeChunk, b - p0);
+      if (h == 0)
+        done += tree_chunk<V, true>(pin, pout, Fs, sd, t, p0, len, (uint32_t)(p0 - a), a1 + done, done, wsum);
+      else
+        done += tree_chunk<V, false>(pin, pout, Fs, sd, t, p0, len, (uint32_t)(p0 - a), a1 + done, done, wsum);
+      __syncthreads();  // F slots and wsum settled before the next chunk
+    }
+    a = a1;
+    b = b1;
+    ++h;
+  }
+  if (threadIdx.x >= 32) return;
+  // short windows: one warp, F in registers, no block barriers
+  const uint32_t lane = threadIdx.x;
+  V f{};
+  if (lane < b - a) f = (h == 0) ? pin[a + lane] : Fs[lane];
+  const uint32_t ltmask = ~(0xffffffffu >> lane);
+  while (a < b) {
+    uint64_t a1, b1;
+    if (h + 1 < kTreeD) {
+      a1 = ach[h + 1];
+      b1 = bch[h + 1];
+    } else {
+      a1 = n1 + warp_rank(sd, R, a < t ? a : t, lane);
+      b1 = n1 + warp_rank(sd, R, b < t ? b : t, lane);
+    }
+    const uint32_t L = (uint32_t)(b - a);
+    uint32_t w = 0;
+    if (a < t) {
+      w = (uint32_t)(bits64_at(sd, a) >> 32);
+      uint64_t nv = t - a;
+      if (nv > L) nv = L;
+      if (nv < 32) w &= ~(0xffffffffu >> nv);
+    }
+    const bool one = (w >> (31 - lane)) & 1u;
+    const uint32_t r = __popc(w & ltmask);
+    if (one) {
+      pout[a + lane] = pin[a1 + r];
+      wF[r] = f;
+    } else if (lane < L) {
+      pout[a + lane] = f;
+    }
+    __syncwarp();
+    f = wF[lane];
+    __syncwarp();
+    a = a1;
+    b = b1;
+    ++h;
+  }
+}
+
+template <typename V>
+struct TreeCfg {
+  static constexpr uint32_t T0 = sizeof(V) == 4 ? 4096u : 2048u;      // positions of window 0 per CTA
+  static constexpr uint32_t E = 16 / sizeof(V);                       // elements per 16 bytes
+  // windows total ~2*T0 +- O(sqrt(T0)) for a random stream; a tile that does
+  // not fit takes the direct path
+  static constexpr uint32_t SCAP = T0 * 17 / 8 + 2 * E * kTreeD;       // staged elements (all windows)
+  static constexpr uint32_t GCAP = SCAP / 32 + kTreeD;                 // 32-position groups
+  static constexpr size_t SMEM = (size_t)SCAP * sizeof(V) + GCAP * 16;  // stage | group descriptors
+};
+
+uint32_t tree_tile(int eb) { return eb == 4 ? TreeCfg<uint32_t>::T0 : TreeCfg<unsigned long long>::T0; }
+
+// Staged tree merge.  One CTA per window-0 tile:
+//  1. window starts a_h / ends b_h (precomputed chains), staging layout by a
+//     warp scan;
+//  2. TMA bulk copies of in[a_h, b_h) for every window into shared memory
+//     (16-byte aligned interiors; the ragged ends by plain loads);
+//  3. the bits of every window as 32-position groups and one block scan for
+//     the ones' ranks (a group descriptor: mask, stage index of the group's
+//     first position and of its first one's B slot);
+//  4. the in-place swap merge itself, window after window: the one at stage
+//     position i of window h swaps with slot rank(i) of window h+1 (the
+//     reference's swap(a[i], a[mid]) with mid = n1 + rank'(i)); swaps of one
+//     window touch distinct slots, so a window is one parallel step;
+//  5. TMA bulk stores of every window from shared memory to out[].
+// Each element is read once and written once; no global round trip between.
+template <typename V>
+__global__ void __launch_bounds__(kTreeBlock, 4) merge_tree_kernel(const V* __restrict__ in, V* __restrict__ out,
+                                                                const PairPlan* __restrict__ plans,
+                                                                const uint64_t* __restrict__ rank,
+                                                                const uint64_t* __restrict__ chains, uint32_t tpp) {
+  using C = TreeCfg<V>;
+  extern __shared__ __align__(128) unsigned char tree_smem[];
+  V* stage = reinterpret_cast<V*>(tree_smem);
+  // group descriptor: x = ones mask, y = stage index of the group's first
+  // position, z = stage index of the B slot of its first one
+  uint4* gdesc = reinterpret_cast<uint4*>(stage + C::SCAP);
+  __shared__ uint32_t wsum[kTreeBlock / 32];
+  __shared__ uint64_t ach[kTreeD], bch[kTreeD], nxt[2];
+  __shared__ uint32_t stoff[kTreeD], goff[kTreeD + 1], gpre_s[C::GCAP];
+  __shared__ uint32_t ilo_s[kTreeD], ihi_s[kTreeD];
+  __shared__ int nwin_s;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ V wF[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t g = blockIdx.x / tpp, tau = blockIdx.x - g * tpp;
+  const PairPlan* Pp = plans + g;
+  const uint64_t n1 = Pp->n1;
+  if (tau * (uint64_t)C::T0 >= n1) return;
+  const uint64_t t = Pp->t;
+  const StreamDesc sd = Pp->sd;
+  const uint64_t* R = rank + Pp->rank_off;
+  const V* pin = in + Pp->s;
+  V* pout = out + Pp->s;
+  if (wid == 0) {
+    // 1. windows: lane h owns window h
+    const uint64_t* ca = chains + (g * (tpp + 1) + tau) * kTreeD;
+    uint64_t a = 0, b = 0;
+    if (lane < (uint32_t)kTreeD) {
+      a = ca[lane];
+      b = ca[kTreeD + lane];
+      ach[lane] = a;
+      bch[lane] = b;
+    }
+    const uint32_t emp = __ballot_sync(0xffffffffu, lane < (uint32_t)kTreeD && a == b);
+    const uint32_t nw = emp ? (uint32_t)(__ffs(emp) - 1) : (uint32_t)kTreeD;
+    const bool act = lane < nw;
+    const uint64_t len = act ? b - a : 0;
+    const bool big = len > C::SCAP;
+    uint32_t mis = 0, reg = 0, gc = 0, lo = 0, hi = 0, bytes = 0;
+    if (act && !big) {
+      const uintptr_t A0 = reinterpret_cast<uintptr_t>(pin + a), A1 = reinterpret_cast<uintptr_t>(pin + b);
+      mis = (uint32_t)((A0 & 15) / sizeof(V));
+      reg = (mis + (uint32_t)len + C::E - 1) & ~(C::E - 1);
+      gc = (uint32_t)((len + 31) >> 5);
+      const uintptr_t I0 = (A0 + 15) & ~(uintptr_t)15, I1 = A1 & ~(uintptr_t)15;
+      if (I1 > I0) {
+        lo = (uint32_t)((I0 - A0) / sizeof(V));
+        hi = (uint32_t)((I1 - A0) / sizeof(V));
+        bytes = (uint32_t)(I1 - I0);
+      }
+    }
+    uint32_t sreg = reg, sgc = gc, sby = bytes;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y1 = __shfl_up_sync(0xffffffffu, sreg, o);
+      const uint32_t y2 = __shfl_up_sync(0xffffffffu, sgc, o);
+      const uint32_t y3 = __shfl_up_sync(0xffffffffu, sby, o);
+      if (lane >= (uint32_t)o) { sreg += y1; sgc += y2; sby += y3; }
+    }
+    const uint32_t treg = __shfl_sync(0xffffffffu, sreg, 31), tgc = __shfl_sync(0xffffffffu, sgc, 31);
+    const uint32_t tby = __shfl_sync(0xffffffffu, sby, 31);
+    const bool ok = nw < (uint32_t)kTreeD && !__any_sync(0xffffffffu, big) && treg <= C::SCAP && tgc <= C::GCAP;
+    if (act) {
+      stoff[lane] = sreg - reg + mis;
+      goff[lane] = sgc - gc;
+      ilo_s[lane] = hi > lo ? lo : (uint32_t)len;
+      ihi_s[lane] = hi > lo ? hi : (uint32_t)len;
+    }
+    if (lane == 0) {
+      goff[nw] = tgc;
+      nwin_s = ok ? (int)nw : -1;
+      if (ok) {
+        mbar_init(&bar, 1);
+        mbar_arrive_expect_tx(&bar, tby);
+      }
+    }
+    __syncwarp();
+    if (ok && act && hi > lo) bulk_g2s(stage + (sreg - reg + mis) + lo, pin + a + lo, bytes, &bar);
+  }
+  __syncthreads();
+  const int nw = nwin_s;
+  if (nw < 0) {
+    tree_windows_direct<V>(pin, pout, stage, sd, R, n1, t, ach, bch, wsum, nxt, wF);
+    return;
+  }
+  const uint32_t ngroups = goff[nw];
+  // ragged ends (outside the 16-byte aligned interiors) by plain loads, a warp
+  // per window; they complete while the bits are being ranked
+  for (int h = wid; h < nw; h += kTreeBlock / 32) {
+    const uint32_t L = (uint32_t)(bch[h] - ach[h]), lo = ilo_s[h], hi = ihi_s[h];
+    V* st = stage + stoff[h];
+    for (uint32_t i = lane; i < lo; i += 32) st[i] = pin[ach[h] + i];
+    for (uint32_t i = hi + lane; i < L; i += 32) st[i] = pin[ach[h] + i];
+  }
+  // 3. group masks (two consecutive groups per thread) and their ones
+  uint32_t cnt2[2], hh[2], mm[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const uint32_t G = 2 * tid + e;
+    uint32_t m = 0, h = 0;
+    if (G < ngroups) {
+      while (goff[h + 1] <= G) ++h;
+      const uint64_t p = ach[h] + 32ull * (G - goff[h]);
+      if (p < t) {
+        const uint64_t nv = min(bch[h] - p, t - p);
+        m = (uint32_t)(bits64_at(sd, p) >> 32);
+        if (nv < 32) m &= ~(0xffffffffu >> nv);
+      }
+    }
+    cnt2[e] = __popc(m);
+    hh[e] = h;
+    mm[e] = m;
+  }
+  const uint32_t c2 = cnt2[0] + cnt2[1];
+  uint32_t x = c2;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  uint32_t before = 0;
+#pragma unroll
+  for (int w = 0; w < kTreeBlock / 32; ++w) before += (w < (int)wid) ? wsum[w] : 0u;
+  const uint32_t ex0 = before + x - c2, ex1 = ex0 + cnt2[0];
+  if (2 * tid < ngroups) gpre_s[2 * tid] = ex0;
+  if (2 * tid + 1 < ngroups) gpre_s[2 * tid + 1] = ex1;
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const uint32_t G = 2 * tid + e;
+    if (G < ngroups) {
+      const uint32_t h = hh[e];
+      const uint32_t k = (e ? ex1 : ex0) - gpre_s[goff[h]];  // rank of the group's first one in window h
+      gdesc[G] = make_uint4(mm[e], stoff[h] + 32 * (G - goff[h]), stoff[h + 1] + k, 0u);
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  // 4. the swaps, window by window (the last window has no ones)
+  const uint32_t ltmask = ~(0xffffffffu >> lane);
+  for (int h = 0; h + 1 < nw; ++h) {
+    for (uint32_t G = goff[h] + wid; G < goff[h + 1]; G += kTreeBlock / 32) {
+      const uint4 d = gdesc[G];
+      if ((d.x << lane) >> 31) {
+        const uint32_t ia = d.y + lane, ib = d.z + __popc(d.x & ltmask);
+        const V va = stage[ia], vb = stage[ib];
+        stage[ia] = vb;
+        stage[ib] = va;
+      }
+    }
+    __syncthreads();
+  }
+  // 5. stores: aligned interiors by TMA (one lane per window), ragged ends
+  //    plain; if out[] and in[] differ in alignment mod 16 (sub-array calls),
+  //    every element is stored plainly
+  const bool tma_out = ((reinterpret_cast<uintptr_t>(pout) - reinterpret_cast<uintptr_t>(pin)) & 15) == 0;
+  if (tma_out) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (wid == 0 && lane < (uint32_t)nw && ihi_s[lane] > ilo_s[lane]) {
+      const uint32_t lo = ilo_s[lane];
+      bulk_s2g(pout + ach[lane] + lo, stage + stoff[lane] + lo, (ihi_s[lane] - lo) * (uint32_t)sizeof(V));
+      bulk_commit();
+    }
+  }
+  for (int h = wid; h < nw; h += kTreeBlock / 32) {
+    const uint32_t L = (uint32_t)(bch[h] - ach[h]);
+    const uint32_t lo = tma_out ? ilo_s[h] : L, hi = tma_out ? ihi_s[h] : L;
+    const V* st = stage + stoff[h];
+    for (uint32_t i = lane; i < lo; i += 32) pout[ach[h] + i] = st[i];
+    for (uint32_t i = hi + lane; i < L; i += 32) pout[ach[h] + i] = st[i];
+  }
+  if (tma_out && wid == 0) bulk_wait_read0();  // the shared source must outlive the copies
+}
+
+template <typename V>
+static void merge_tree_t(void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
+                         const uint64_t* chains, uint32_t tpp, cudaStream_t st) {
+  const size_t smem = TreeCfg<V>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(merge_tree_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  merge_tree_kernel<V><<<(unsigned)(npairs * tpp), kTreeBlock, smem, st>>>((const V*)in, (V*)out, plans, rank,
+                                                                             chains, tpp);
+  count_launch();
+}
+
+void launch_merge_tree(int eb, void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
+                       const uint64_t* chains, uint32_t tpp, cudaStream_t st) {
+  if (!npairs) return;
+  if (eb == 4) merge_tree_t<uint32_t>(in, out, plans, npairs, rank, chains, tpp, st);
+  else merge_tree_t<unsigned long long>(in, out, plans, npairs, rank, chains, tpp, st);
+}
+
 constexpr int kSegBlock = 256;
 constexpr int kSegCPW = 8;  // 2048 positions per tile
 uint32_t merge_tile(int eb) { (void)eb; return kSegBlock * kSegCPW; }
@@ -517,9 +949,18 @@ static void merge_round_t(void* in, void* out, const PairPlan* plans, uint64_t n
 }
 
 void launch_merge_round(int eb, void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
-                        const uint64_t* segs, const uint64_t* seglen_max_host, cudaStream_t st) {
+                        const uint64_t* segs, const uint64_t* seglen_max_host, const uint64_t* chains, uint32_t tpp,
+                        cudaStream_t st) {
+  if (g_seg_variant < 100) {  // default: the tree kernel (one read + one write per element)
+    launch_merge_tree(eb, in, out, plans, npairs, rank, chains, tpp, st);
+    return;
+  }
+  // debug variants >= 100: the segment-pass kernels (1.5 + 1.5 passes), shape = variant - 100
+  const int keep = g_seg_variant;
+  g_seg_variant -= 100;
   if (eb == 4) merge_round_t<uint32_t>(in, out, plans, npairs, rank, segs, seglen_max_host, st);
   else merge_round_t<unsigned long long>(in, out, plans, npairs, rank, segs, seglen_max_host, st);
+  g_seg_variant = keep;
 }
 
 // [X, N) is untouched by phase 1 (A queue empty past X).

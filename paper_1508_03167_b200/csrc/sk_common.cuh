@@ -66,6 +66,14 @@ __device__ __forceinline__ uint64_t bits64_at(const StreamDesc& d, uint64_t t) {
   return (a << o) | (b >> (64 - o));
 }
 
+// TMA bulk prefetch of [p, p+bytes) (16-byte aligned interior) into L2.
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
+  const uintptr_t a0 = ((uintptr_t)p + 15) & ~(uintptr_t)15;
+  const uintptr_t a1 = ((uintptr_t)p + bytes) & ~(uintptr_t)15;
+  if (a1 > a0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+}
+
 // Number of one-bits in [0, pos) of a stream whose superblock prefix table R
 // holds ones in [0, 512k) at R[k].
 __device__ __forceinline__ uint64_t rank_bits(const StreamDesc& d, const uint64_t* R, uint64_t pos) {
@@ -228,6 +236,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// shared -> global bulk copy (bulk-group completion), its commit and the wait
+// until the shared source may be reused; generic-proxy smem writes must be
+// fenced (fence_proxy_async_smem) before the copy reads them.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n SK_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra SK_WAIT_%=;\n}" ::"r"(

@@ -36,8 +36,16 @@ void launch_tail_decode(const LevelTail* d_levels, int nlevels, const uint64_t* 
                         unsigned long long* bits, cudaStream_t st);
 
 void launch_merge_round(int eb, void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
-                        const uint64_t* segs, const uint64_t* seglen_max_host, cudaStream_t st);
+                        const uint64_t* segs, const uint64_t* seglen_max_host, const uint64_t* chains, uint32_t tpp,
+                        cudaStream_t st);
 uint32_t merge_tile(int eb);
+uint32_t tree_tile(int eb);
+uint32_t tree_tiles_per_pair(const LevelJob& LJ, int eb);
+uint64_t tree_chain_words(uint64_t npairs, uint32_t tpp);
+void launch_tree_chains(int eb, const PairPlan* plans, uint64_t npairs, const uint64_t* rank, uint32_t tpp,
+                        uint64_t* chains, cudaStream_t st);
+void launch_merge_tree(int eb, void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
+                       const uint64_t* chains, uint32_t tpp, cudaStream_t st);
 void launch_copy_tail_region(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs,
                              cudaStream_t st);
 void launch_iota32(uint32_t* v, uint64_t n, cudaStream_t st);
