@@ -706,7 +706,7 @@ uint32_t tree_tile(int eb) { return eb == 4 ? TreeCfg<uint32_t>::T0 : TreeCfg<un
 //  5. TMA bulk stores of every window from shared memory to out[].
 // Each element is read once and written once; no global round trip between.
 template <typename V>
-__global__ void __launch_bounds__(kTreeBlock, 4) merge_tree_kernel(const V* __restrict__ in, V* __restrict__ out,
+__global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __restrict__ in, V* __restrict__ out,
                                                                 const PairPlan* __restrict__ plans,
                                                                 const uint64_t* __restrict__ rank,
                                                                 const uint64_t* __restrict__ chains, uint32_t tpp) {
@@ -848,9 +848,12 @@ __global__ void __launch_bounds__(kTreeBlock, 4) merge_tree_kernel(const V* __re
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  // 4. the swaps, window by window (the last window has no ones)
+  // 4. the swaps, window by window (the last window has no ones).  Windows
+  //    shrink (|window h+1| = ones of window h); from the first window of at
+  //    most 64 positions on, warp 0 finishes alone with warp barriers.
   const uint32_t ltmask = ~(0xffffffffu >> lane);
-  for (int h = 0; h + 1 < nw; ++h) {
+  int h = 0;
+  for (; h + 1 < nw && goff[h + 1] - goff[h] > 2; ++h) {
     for (uint32_t G = goff[h] + wid; G < goff[h + 1]; G += kTreeBlock / 32) {
       const uint4 d = gdesc[G];
       if ((d.x << lane) >> 31) {
@@ -862,10 +865,25 @@ __global__ void __launch_bounds__(kTreeBlock, 4) merge_tree_kernel(const V* __re
     }
     __syncthreads();
   }
+  if (wid == 0) {
+    for (; h + 1 < nw; ++h) {
+      for (uint32_t G = goff[h]; G < goff[h + 1]; ++G) {
+        const uint4 d = gdesc[G];
+        if ((d.x << lane) >> 31) {
+          const uint32_t ia = d.y + lane, ib = d.z + __popc(d.x & ltmask);
+          const V va = stage[ia], vb = stage[ib];
+          stage[ia] = vb;
+          stage[ib] = va;
+        }
+      }
+      __syncwarp();
+    }
+  }
   // 5. stores: aligned interiors by TMA (one lane per window), ragged ends
   //    plain; if out[] and in[] differ in alignment mod 16 (sub-array calls),
   //    every element is stored plainly
   const bool tma_out = ((reinterpret_cast<uintptr_t>(pout) - reinterpret_cast<uintptr_t>(pin)) & 15) == 0;
+  __syncthreads();
   if (tma_out) {
     fence_proxy_async_smem();
     __syncthreads();
@@ -875,12 +893,12 @@ __global__ void __launch_bounds__(kTreeBlock, 4) merge_tree_kernel(const V* __re
       bulk_commit();
     }
   }
-  for (int h = wid; h < nw; h += kTreeBlock / 32) {
-    const uint32_t L = (uint32_t)(bch[h] - ach[h]);
-    const uint32_t lo = tma_out ? ilo_s[h] : L, hi = tma_out ? ihi_s[h] : L;
-    const V* st = stage + stoff[h];
-    for (uint32_t i = lane; i < lo; i += 32) pout[ach[h] + i] = st[i];
-    for (uint32_t i = hi + lane; i < L; i += 32) pout[ach[h] + i] = st[i];
+  for (int hw = wid; hw < nw; hw += kTreeBlock / 32) {
+    const uint32_t L = (uint32_t)(bch[hw] - ach[hw]);
+    const uint32_t lo = tma_out ? ilo_s[hw] : L, hi = tma_out ? ihi_s[hw] : L;
+    const V* st = stage + stoff[hw];
+    for (uint32_t i = lane; i < lo; i += 32) pout[ach[hw] + i] = st[i];
+    for (uint32_t i = hi + lane; i < L; i += 32) pout[ach[hw] + i] = st[i];
   }
   if (tma_out && wid == 0) bulk_wait_read0();  // the shared source must outlive the copies
 }
