@@ -255,9 +255,9 @@ def main():
     ms_per_step = ms / args.steps
     value = n_total / (ms_per_step * 1e-3) / 1e9
 
-    # roofline: the dominant kernel is one merge round (merge_segment_kernel
-    # launches + merge_tail_kernel, stage 2); algorithmic bytes per round = one
-    # read + one write of the shard (2 * 4 B * n).
+    # roofline: the dominant kernel is the merge round (merge_tree_kernel, one
+    # launch per round, stage 2); algorithmic bytes per round = one read + one
+    # write of the shard (2 * 4 B * n).
     from paper_1508_03167_b200.shufflers import merge_plan
     c_tot = merge_plan(n_total, 65536)[0]
     local_rounds = c_tot - (world.bit_length() - 1)
@@ -271,7 +271,7 @@ def main():
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": tr.get("bytes_per_round") if tr else None,
             "peak_source": peak_kind,
-            "kernel": "one merge round (merge_segment_kernel launches + merge_tail_kernel)",
+            "kernel": "one merge round (merge_tree_kernel, one launch)",
             "algorithmic_bytes_per_round": alg_bytes, "avg_round_ms": round(per_round_ms, 4),
             "launches_per_round": round(stage_l[2] / rounds, 2),
             "stage_ms_per_step": {k: round(stage_ms[i] / args.steps, 4) for i, k in

@@ -74,8 +74,7 @@ __global__ void __launch_bounds__(kDecodeBlock) leaf_decode16_kernel(ArrayJob J,
   uint32_t A = ring[0][lane], B = ring[1][lane], C = ring[2][lane], D = ring[3][lane];
   uint32_t rd = 4;
   uint32_t pos = 0;
-  uint32_t lb = 31 - __clz(i | 1), v = 1, c = 0;
-  uint32_t nb = 0;
+  uint32_t v = 1, c = 0;
   // Draws are packed eight at a time (16-byte stores, most recent draw in the
   // low bits) except in the 16-byte chunk holding draw m-1, whose upper bytes
   // belong to the next leaf: those go out as single 16-bit stores.  Per-lane
@@ -100,7 +99,7 @@ __global__ void __launch_bounds__(kDecodeBlock) leaf_decode16_kernel(ArrayJob J,
       // (i == 0) compute harmlessly but never store or advance
       const bool act = i != 0;
       const uint32_t b = i + 1;
-      uint32_t k = lb + __clz(v) - 31;
+      uint32_t k = __clz(v) - __clz(b);  // smallest k with v << k >= b
       k += ((v << k) < b) ? 1u : 0u;
       const uint32_t x = __funnelshift_l(B, A, pos);
       const uint32_t cc = (c << k) | (x >> (32 - k));
@@ -120,11 +119,8 @@ __global__ void __launch_bounds__(kDecodeBlock) leaf_decode16_kernel(ArrayJob J,
       wp -= acc;
       c = acc ? 0u : cc - b;
       v = acc ? 1u : (v << k) - b;
-      lb -= (acc && i == (1u << lb)) ? 1u : 0u;  // floor(log2(i-1)) drops at powers of two
       i -= acc;
-      const uint32_t kk = act ? k : 0u;
-      nb += kk;
-      pos += kk;
+      pos += act ? k : 0u;
       const bool cross = pos >= 32;
       const uint32_t nxt = ring[rd & 15][lane];
       pos = cross ? pos - 32 : pos;
@@ -139,7 +135,7 @@ __global__ void __launch_bounds__(kDecodeBlock) leaf_decode16_kernel(ArrayJob J,
     // the last (< 8) packed draws: dr[1 ..], dr[1] in the low bits
     const long rem = (long)(pend - (dr + 1));
     for (long k = 0; k < rem; ++k) dr[1 + k] = (uint16_t)(k < 4 ? plo >> (16 * k) : phi >> (16 * (k - 4)));
-    atomicAdd(&bits[L.array], (unsigned long long)nb);
+    atomicAdd(&bits[L.array], 32ull * (rd - 4) + pos);  // bits consumed = halves passed + pos
   }
 }
 
