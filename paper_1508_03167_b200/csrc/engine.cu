@@ -275,21 +275,29 @@ static cudaStream_t side_stream() {
   return ss.s;
 }
 
-// Run rounds 1..c over `cur` (data currently there), ping-ponging with `other`.
-// Returns the buffer holding the result.
+// Run rounds 1..c over `cur` (data currently there); the result lands in
+// `other`.  The tree merge reads every window of a CTA before writing it back
+// (and CTAs own disjoint windows), so rounds 1..c-1 run in place on `cur`
+// and only the last round writes `other` (plus the untouched [X, N) regions).
+// The segment-pass debug kernels park elements in their input and need the
+// ping-pong.  Returns the buffer holding the result.
 static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* other, cudaStream_t st) {
-  for (auto& L : lv) {
+  const bool in_place = merge_tree_active();
+  for (size_t r = 0; r < lv.size(); ++r) {
+    auto& L = lv[r];
+    const bool last = r + 1 == lv.size();
+    void* out = (in_place && !last) ? cur : other;
     {
       StageTimer tm(2, st);
-      launch_merge_round(eb, cur, other, L.plans, L.npairs, L.rank, L.segs, L.seglen_host, L.chains, L.tpp, st);
+      launch_merge_round(eb, cur, out, L.plans, L.npairs, L.rank, L.segs, L.seglen_host, L.chains, L.tpp, st);
     }
     {
       StageTimer tm(3, st);
-      launch_copy_tail_region(eb, cur, other, L.plans, L.npairs, st);
+      if (out != cur) launch_copy_tail_region(eb, cur, out, L.plans, L.npairs, st);
       CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
-      launch_tail_apply(eb, other, L.dst, L.src, L.tmp, 2 * L.total, st);
+      launch_tail_apply(eb, out, L.dst, L.src, L.tmp, 2 * L.total, st);
     }
-    std::swap(cur, other);
+    if (out != cur) std::swap(cur, other);
   }
   CK(cudaGetLastError());
   return cur;

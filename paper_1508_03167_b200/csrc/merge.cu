@@ -932,6 +932,7 @@ uint32_t merge_tile(int eb) { (void)eb; return kSegBlock * kSegCPW; }
 // warp (tile = 256*CPW positions), Q tiles per CTA, min CTAs per SM
 static int g_seg_variant = 0;
 void debug_set_seg_variant(int v) { g_seg_variant = v; }
+bool merge_tree_active() { return g_seg_variant < 100; }
 
 template <typename V, int CPW, int Q, int MINB>
 static void seg_launch(void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,

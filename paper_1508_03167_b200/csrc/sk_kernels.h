@@ -20,6 +20,7 @@ void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64
 
 void debug_set_leaf_stop(int v);
 void debug_set_seg_variant(int v);
+bool merge_tree_active();
 
 // merge.cu
 struct LevelTail {            // device-side view used by the all-levels tail decoder
