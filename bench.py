@@ -277,7 +277,9 @@ def main():
             "stage_ms_per_step": {k: round(stage_ms[i] / args.steps, 4) for i, k in
                                   enumerate(["leaf_decode", "leaf_apply", "merge_rounds", "identity+tail",
                                              "final_copy"])},
-            "passes_per_step": round(ms_per_step / (alg_bytes / (peak * 1e9) * 1e3), 2)}
+            # the whole step: c+1 passes over the shard (leaves + local rounds)
+            "step_passes": local_rounds + 1,
+            "step_frac_of_roofline": round((local_rounds + 1) * alg_bytes / (peak * 1e9) * 1e3 / ms_per_step, 4)}
 
     # e2e through the public API with host buffers (pinned), H2D + D2H inside
     e2e = None
