@@ -528,15 +528,74 @@ void launch_tree_chains(int eb, const PairPlan* plans, uint64_t npairs, const ui
   count_launch();
 }
 
+// Element access of one pair for the tree kernels: FlatAcc = the pair in one
+// buffer (in/out may differ); PeerAcc = the pair split into up to kMaxParts
+// contiguous parts living in different buffers (other GPUs' memory mapped
+// into this one: P2P loads/stores over NVLink), always in place.
+constexpr int kMaxParts = 8;
+
+template <typename V>
+struct FlatAcc {
+  const V* in;
+  V* out;
+  __device__ __forceinline__ V ld(uint64_t p) const { return in[p]; }
+  __device__ __forceinline__ void st(uint64_t p, V v) const { out[p] = v; }
+  __device__ __forceinline__ const V* src(uint64_t p) const { return in + p; }
+  __device__ __forceinline__ V* dst(uint64_t p) const { return out + p; }
+  // [x0, x1) as maximal runs inside one buffer: f(run_start, run_end)
+  template <class F>
+  __device__ __forceinline__ void runs(uint64_t x0, uint64_t x1, F f) const {
+    if (x1 > x0) f(x0, x1);
+  }
+  __device__ __forceinline__ bool same_alignment() const {
+    return ((reinterpret_cast<uintptr_t>(out) - reinterpret_cast<uintptr_t>(in)) & 15) == 0;
+  }
+};
+
+template <typename V>
+struct PeerParts {
+  V* base[kMaxParts];              // element at pair position start[k]
+  uint64_t start[kMaxParts + 1];   // part k = [start[k], start[k+1])
+  int n;
+  int tma;                         // 1: every part position-aligned mod 16 B and starts multiple of 16 B
+};
+
+template <typename V>
+struct PeerAcc {
+  const PeerParts<V>& P;
+  __device__ __forceinline__ int part(uint64_t p) const {
+    int k = 0;
+    while (k + 1 < P.n && p >= P.start[k + 1]) ++k;
+    return k;
+  }
+  __device__ __forceinline__ V* ptr(uint64_t p) const {
+    const int k = part(p);
+    return P.base[k] + (p - P.start[k]);
+  }
+  __device__ __forceinline__ V ld(uint64_t p) const { return *ptr(p); }
+  __device__ __forceinline__ void st(uint64_t p, V v) const { *ptr(p) = v; }
+  __device__ __forceinline__ const V* src(uint64_t p) const { return ptr(p); }
+  __device__ __forceinline__ V* dst(uint64_t p) const { return ptr(p); }
+  template <class F>
+  __device__ __forceinline__ void runs(uint64_t x0, uint64_t x1, F f) const {
+    for (int k = part(x0); k < P.n && x0 < x1; ++k) {
+      const uint64_t e = min(x1, P.start[k + 1]);
+      if (e > x0) f(x0, e);
+      x0 = e;
+    }
+  }
+  __device__ __forceinline__ bool same_alignment() const { return P.tma != 0; }
+};
+
 // One chunk of a window: positions [p0, p0 + len), fbase = index of p0 in the
 // window (its F slot), bq = position of the chunk's first B element, obase =
 // F slot of the chunk's first one in the next window.  Window 0 reads F from
 // in[]; deeper windows from shared memory, compacted in place (a barrier
 // separates the chunk's loads from its stores).  Returns the chunk's ones.
-template <typename V, bool L0>
-__device__ __forceinline__ uint32_t tree_chunk(const V* __restrict__ pin, V* __restrict__ pout, V* Fs,
-                                               const StreamDesc& sd, uint64_t t, uint64_t p0, uint32_t len,
-                                               uint32_t fbase, uint64_t bq, uint32_t obase, uint32_t* wsum) {
+template <typename V, bool L0, class Acc>
+__device__ __forceinline__ uint32_t tree_chunk(const Acc& acc, V* Fs, const StreamDesc& sd, uint64_t t, uint64_t p0,
+                                               uint32_t len, uint32_t fbase, uint64_t bq, uint32_t obase,
+                                               uint32_t* wsum) {
   constexpr int CPW = kTreeCPW;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t wbase = wid * 32 * CPW;
@@ -583,18 +642,18 @@ __device__ __forceinline__ uint32_t tree_chunk(const V* __restrict__ pin, V* __r
     qo[k] = before + rb + __popc(m & ltmask);
     inmask |= (in_t ? 1u : 0u) << k;
     onemask |= (one ? 1u : 0u) << k;
-    if (in_t) f[k] = L0 ? pin[p0 + i] : Fs[fbase + i];
-    if (one) b[k] = pin[bq + qo[k]];
+    if (in_t) f[k] = L0 ? acc.ld(p0 + i) : Fs[fbase + i];
+    if (one) b[k] = acc.ld(bq + qo[k]);
   }
   __syncthreads();  // loads of F (and of wsum) complete before the in-place stores
 #pragma unroll
   for (int k = 0; k < CPW; ++k) {
     const uint64_t p = p0 + wbase + 32 * k + lane;
     if ((onemask >> k) & 1u) {
-      pout[p] = b[k];
+      acc.st(p, b[k]);
       Fs[obase + qo[k]] = f[k];
     } else if ((inmask >> k) & 1u) {
-      pout[p] = f[k];
+      acc.st(p, f[k]);
     }
   }
   return total;
@@ -604,10 +663,10 @@ __device__ __forceinline__ uint32_t tree_chunk(const V* __restrict__ pin, V* __r
 // when a tile's windows do not fit the staging buffer or its chain is deeper
 // than the stored kTreeD starts.  Never taken for pseudo-random bit streams
 // in practice; kept exact for every input.
-template <typename V>
-__device__ void tree_windows_direct(const V* __restrict__ pin, V* __restrict__ pout, V* Fs, const StreamDesc& sd,
-                                    const uint64_t* R, uint64_t n1, uint64_t t, const uint64_t* ach,
-                                    const uint64_t* bch, uint32_t* wsum, uint64_t* nxt, V* wF) {
+template <typename V, class Acc>
+__device__ void tree_windows_direct(const Acc& acc, V* Fs, const StreamDesc& sd, const uint64_t* R, uint64_t n1,
+                                    uint64_t t, const uint64_t* ach, const uint64_t* bch, uint32_t* wsum,
+                                    uint64_t* nxt, V* wF) {
   uint64_t a = ach[0], b = bch[0];
   int h = 0;
   while (b - a > 32) {
@@ -629,9 +688,9 @@ __device__ void tree_windows_direct(const V* __restrict__ pin, V* __restrict__ p
     for (uint64_t p0 = a; p0 < b; p0 += kTreeChunk) {
       const uint32_t len = (uint32_t)min((uint64_t)kTreeChunk, b - p0);
       if (h == 0)
-        done += tree_chunk<V, true>(pin, pout, Fs, sd, t, p0, len, (uint32_t)(p0 - a), a1 + done, done, wsum);
+        done += tree_chunk<V, true>(acc, Fs, sd, t, p0, len, (uint32_t)(p0 - a), a1 + done, done, wsum);
       else
-        done += tree_chunk<V, false>(pin, pout, Fs, sd, t, p0, len, (uint32_t)(p0 - a), a1 + done, done, wsum);
+        done += tree_chunk<V, false>(acc, Fs, sd, t, p0, len, (uint32_t)(p0 - a), a1 + done, done, wsum);
       __syncthreads();  // F slots and wsum settled before the next chunk
     }
     a = a1;
@@ -642,7 +701,7 @@ __device__ void tree_windows_direct(const V* __restrict__ pin, V* __restrict__ p
   // short windows: one warp, F in registers, no block barriers
   const uint32_t lane = threadIdx.x;
   V f{};
-  if (lane < b - a) f = (h == 0) ? pin[a + lane] : Fs[lane];
+  if (lane < b - a) f = (h == 0) ? acc.ld(a + lane) : Fs[lane];
   const uint32_t ltmask = ~(0xffffffffu >> lane);
   while (a < b) {
     uint64_t a1, b1;
@@ -664,10 +723,10 @@ __device__ void tree_windows_direct(const V* __restrict__ pin, V* __restrict__ p
     const bool one = (w >> (31 - lane)) & 1u;
     const uint32_t r = __popc(w & ltmask);
     if (one) {
-      pout[a + lane] = pin[a1 + r];
+      acc.st(a + lane, acc.ld(a1 + r));
       wF[r] = f;
     } else if (lane < L) {
-      pout[a + lane] = f;
+      acc.st(a + lane, f);
     }
     __syncwarp();
     f = wF[lane];
@@ -705,11 +764,9 @@ uint32_t tree_tile(int eb) { return eb == 4 ? TreeCfg<uint32_t>::T0 : TreeCfg<un
 //     window touch distinct slots, so a window is one parallel step;
 //  5. TMA bulk stores of every window from shared memory to out[].
 // Each element is read once and written once; no global round trip between.
-template <typename V>
-__global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __restrict__ in, V* __restrict__ out,
-                                                                const PairPlan* __restrict__ plans,
-                                                                const uint64_t* __restrict__ rank,
-                                                                const uint64_t* __restrict__ chains, uint32_t tpp) {
+template <typename V, class Acc>
+__device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* __restrict__ Pp,
+                                                const uint64_t* __restrict__ rank, const uint64_t* __restrict__ ca) {
   using C = TreeCfg<V>;
   extern __shared__ __align__(128) unsigned char tree_smem[];
   V* stage = reinterpret_cast<V*>(tree_smem);
@@ -724,18 +781,14 @@ __global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __re
   __shared__ __align__(8) uint64_t bar;
   __shared__ V wF[32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint64_t g = blockIdx.x / tpp, tau = blockIdx.x - g * tpp;
-  const PairPlan* Pp = plans + g;
   const uint64_t n1 = Pp->n1;
-  if (tau * (uint64_t)C::T0 >= n1) return;
   const uint64_t t = Pp->t;
   const StreamDesc sd = Pp->sd;
   const uint64_t* R = rank + Pp->rank_off;
-  const V* pin = in + Pp->s;
-  V* pout = out + Pp->s;
+  // TMA needs in[] and out[] (every part) equally aligned mod 16 bytes
+  const bool tma = acc.same_alignment();
   if (wid == 0) {
     // 1. windows: lane h owns window h
-    const uint64_t* ca = chains + (g * (tpp + 1) + tau) * kTreeD;
     uint64_t a = 0, b = 0;
     if (lane < (uint32_t)kTreeD) {
       a = ca[lane];
@@ -750,15 +803,16 @@ __global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __re
     const bool big = len > C::SCAP;
     uint32_t mis = 0, reg = 0, gc = 0, lo = 0, hi = 0, bytes = 0;
     if (act && !big) {
-      const uintptr_t A0 = reinterpret_cast<uintptr_t>(pin + a), A1 = reinterpret_cast<uintptr_t>(pin + b);
+      const uintptr_t A0 = reinterpret_cast<uintptr_t>(acc.src(a));
       mis = (uint32_t)((A0 & 15) / sizeof(V));
       reg = (mis + (uint32_t)len + C::E - 1) & ~(C::E - 1);
       gc = (uint32_t)((len + 31) >> 5);
-      const uintptr_t I0 = (A0 + 15) & ~(uintptr_t)15, I1 = A1 & ~(uintptr_t)15;
-      if (I1 > I0) {
-        lo = (uint32_t)((I0 - A0) / sizeof(V));
-        hi = (uint32_t)((I1 - A0) / sizeof(V));
-        bytes = (uint32_t)(I1 - I0);
+      const uint64_t l0 = (C::E - mis) & (C::E - 1);  // first 16-byte aligned offset
+      const uint64_t l1 = ((mis + len) & ~(uint64_t)(C::E - 1)) - mis;
+      if (tma && l1 > l0 && l1 <= len) {
+        lo = (uint32_t)l0;
+        hi = (uint32_t)l1;
+        bytes = (uint32_t)((l1 - l0) * sizeof(V));
       }
     }
     uint32_t sreg = reg, sgc = gc, sby = bytes;
@@ -786,12 +840,17 @@ __global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __re
       }
     }
     __syncwarp();
-    if (ok && act && hi > lo) bulk_g2s(stage + (sreg - reg + mis) + lo, pin + a + lo, bytes, &bar);
+    if (ok && act && hi > lo) {
+      V* st = stage + (sreg - reg + mis);
+      acc.runs(a + lo, a + hi, [&](uint64_t x0, uint64_t x1) {
+        bulk_g2s(st + (x0 - a), acc.src(x0), (uint32_t)((x1 - x0) * sizeof(V)), &bar);
+      });
+    }
   }
   __syncthreads();
   const int nw = nwin_s;
   if (nw < 0) {
-    tree_windows_direct<V>(pin, pout, stage, sd, R, n1, t, ach, bch, wsum, nxt, wF);
+    tree_windows_direct<V>(acc, stage, sd, R, n1, t, ach, bch, wsum, nxt, wF);
     return;
   }
   const uint32_t ngroups = goff[nw];
@@ -800,8 +859,8 @@ __global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __re
   for (int h = wid; h < nw; h += kTreeBlock / 32) {
     const uint32_t L = (uint32_t)(bch[h] - ach[h]), lo = ilo_s[h], hi = ihi_s[h];
     V* st = stage + stoff[h];
-    for (uint32_t i = lane; i < lo; i += 32) st[i] = pin[ach[h] + i];
-    for (uint32_t i = hi + lane; i < L; i += 32) st[i] = pin[ach[h] + i];
+    for (uint32_t i = lane; i < lo; i += 32) st[i] = acc.ld(ach[h] + i);
+    for (uint32_t i = hi + lane; i < L; i += 32) st[i] = acc.ld(ach[h] + i);
   }
   // 3. group masks (two consecutive groups per thread) and their ones
   uint32_t cnt2[2], hh[2], mm[2];
@@ -879,28 +938,55 @@ __global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __re
       __syncwarp();
     }
   }
-  // 5. stores: aligned interiors by TMA (one lane per window), ragged ends
-  //    plain; if out[] and in[] differ in alignment mod 16 (sub-array calls),
-  //    every element is stored plainly
-  const bool tma_out = ((reinterpret_cast<uintptr_t>(pout) - reinterpret_cast<uintptr_t>(pin)) & 15) == 0;
+  // 5. stores: aligned interiors by TMA (one lane per window), ragged ends plain
   __syncthreads();
-  if (tma_out) {
+  if (tma) {
     fence_proxy_async_smem();
     __syncthreads();
     if (wid == 0 && lane < (uint32_t)nw && ihi_s[lane] > ilo_s[lane]) {
-      const uint32_t lo = ilo_s[lane];
-      bulk_s2g(pout + ach[lane] + lo, stage + stoff[lane] + lo, (ihi_s[lane] - lo) * (uint32_t)sizeof(V));
+      const uint64_t a = ach[lane];
+      const V* st = stage + stoff[lane];
+      acc.runs(a + ilo_s[lane], a + ihi_s[lane], [&](uint64_t x0, uint64_t x1) {
+        bulk_s2g(acc.dst(x0), st + (x0 - a), (uint32_t)((x1 - x0) * sizeof(V)));
+      });
       bulk_commit();
     }
   }
   for (int hw = wid; hw < nw; hw += kTreeBlock / 32) {
     const uint32_t L = (uint32_t)(bch[hw] - ach[hw]);
-    const uint32_t lo = tma_out ? ilo_s[hw] : L, hi = tma_out ? ihi_s[hw] : L;
+    const uint32_t lo = ilo_s[hw], hi = ihi_s[hw];
     const V* st = stage + stoff[hw];
-    for (uint32_t i = lane; i < lo; i += 32) pout[ach[hw] + i] = st[i];
-    for (uint32_t i = hi + lane; i < L; i += 32) pout[ach[hw] + i] = st[i];
+    for (uint32_t i = lane; i < lo; i += 32) acc.st(ach[hw] + i, st[i]);
+    for (uint32_t i = hi + lane; i < L; i += 32) acc.st(ach[hw] + i, st[i]);
   }
-  if (tma_out && wid == 0) bulk_wait_read0();  // the shared source must outlive the copies
+  if (tma && wid == 0) bulk_wait_read0();  // the shared source must outlive the copies
+}
+
+// One CTA per (pair, tile) of a round.
+template <typename V>
+__global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __restrict__ in, V* __restrict__ out,
+                                                                const PairPlan* __restrict__ plans,
+                                                                const uint64_t* __restrict__ rank,
+                                                                const uint64_t* __restrict__ chains, uint32_t tpp) {
+  const uint64_t g = blockIdx.x / tpp, tau = blockIdx.x - g * tpp;
+  const PairPlan* Pp = plans + g;
+  if (tau * (uint64_t)TreeCfg<V>::T0 >= Pp->n1) return;
+  const FlatAcc<V> acc{in + Pp->s, out + Pp->s};
+  merge_tree_tile<V>(acc, Pp, rank, chains + (g * (tpp + 1) + tau) * kTreeD);
+}
+
+// One pair split over peer buffers (in place); this launch takes the tiles
+// tau = part, part + nparts, ...
+template <typename V>
+__global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_peer_kernel(const PeerParts<V> parts,
+                                                                     const PairPlan* __restrict__ plans,
+                                                                     const uint64_t* __restrict__ rank,
+                                                                     const uint64_t* __restrict__ chains,
+                                                                     uint32_t tpp, uint32_t part, uint32_t nparts) {
+  const uint64_t tau = part + (uint64_t)blockIdx.x * nparts;
+  if (tau >= tpp || tau * (uint64_t)TreeCfg<V>::T0 >= plans->n1) return;
+  const PeerAcc<V> acc{parts};
+  merge_tree_tile<V>(acc, plans, rank, chains + tau * kTreeD);
 }
 
 template <typename V>
