@@ -75,6 +75,29 @@ int sk_fy_range(void *data, int elem_bytes, uint64_t lo, uint64_t hi, uint64_t s
 int sk_merge_range(void *data, int elem_bytes, uint64_t j, uint64_t k, uint64_t l, uint64_t state_io[4],
                    void *stream);
 
+/* Multi-GPU exchange step (SURVEY.md §8 e): the merge of one pair [0, n1+n2)
+ * whose elements are split into `nparts` contiguous parts held by different
+ * GPUs; part k = positions [part_starts[k], part_starts[k+1]) at device
+ * address part_bases[k] (this GPU's own buffer or a peer buffer mapped with
+ * sk_ipc_open; P2P over NVLink).  `state` is the pair's bit-source state at
+ * the merge start (a fresh substream_seed(seed, r*q+i) in the parallel
+ * schedule).  phase 1: this GPU merges the tiles of part `part` in place,
+ * reading and writing peers directly (one fused kernel, no staging copy);
+ * phase 2: after every part's phase 1 has completed (a barrier of the
+ * caller), ONE part applies the tail insertion (shufflers.py:188-191) and
+ * returns the pair's bit count in *bits_out.  Result identical to
+ * sk_merge_range on the whole pair. */
+int sk_merge_range_peers(void *const *part_bases, const uint64_t *part_starts, int nparts, int part, int elem_bytes,
+                         uint64_t n1, uint64_t n2, const uint64_t state[4], int phase, uint64_t *bits_out,
+                         void *stream);
+
+/* CUDA IPC plumbing for sk_merge_range_peers: the 64-byte handle and byte
+ * offset of the allocation holding `ptr`; map a peer's allocation (returns its
+ * base; add the offset); unmap. */
+int sk_ipc_get_handle(const void *ptr, void *handle_out, uint64_t *offset_out);
+int sk_ipc_open(const void *handle, void **base_out);
+int sk_ipc_close(void *base);
+
 /* Replaces _kernels.merge_shuffle_inplace (_kernels.py:437-441) /
  * merge_shuffle (shufflers.py:194-217): the sequential single-stream variant.
  * Inherently serial (every task's start offset depends on all earlier tasks);

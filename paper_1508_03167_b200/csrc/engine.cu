@@ -429,17 +429,68 @@ static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t
   L.sbs = (N + 1 + 511) / 512 + 1;
   L.tpp = tree_tiles_per_pair(L.LJ, eb);
   try {
-    unsigned char* scratch = A.alloc<unsigned char>(N * eb, st);
     fork_side(st, ps);
     build_plans(lv, eb, d_bits, A, ps, st);
-    // kernels address elements by absolute index; shift the scratch base so
-    // index j lands on scratch[0].
-    void* out_base = (void*)(scratch - j * eb);
-    launch_merge_round(eb, data, out_base, L.plans, 1, L.rank, L.segs, L.seglen_host, L.chains, L.tpp, st);
-    launch_copy_tail_region(eb, data, out_base, L.plans, 1, st);
-    CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
-    launch_tail_apply(eb, out_base, L.dst, L.src, L.tmp, 2 * L.total, st);
-    CK(cudaMemcpyAsync((unsigned char*)data + j * eb, scratch, N * eb, cudaMemcpyDeviceToDevice, st));
+    if (merge_tree_active()) {  // the tree merge runs in place
+      launch_merge_round(eb, data, data, L.plans, 1, L.rank, L.segs, L.seglen_host, L.chains, L.tpp, st);
+      CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
+      launch_tail_apply(eb, data, L.dst, L.src, L.tmp, 2 * L.total, st);
+    } else {
+      unsigned char* scratch = A.alloc<unsigned char>(N * eb, st);
+      // kernels address elements by absolute index; shift the scratch base so
+      // index j lands on scratch[0].
+      void* out_base = (void*)(scratch - j * eb);
+      launch_merge_round(eb, data, out_base, L.plans, 1, L.rank, L.segs, L.seglen_host, L.chains, L.tpp, st);
+      launch_copy_tail_region(eb, data, out_base, L.plans, 1, st);
+      CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
+      launch_tail_apply(eb, out_base, L.dst, L.src, L.tmp, 2 * L.total, st);
+      CK(cudaMemcpyAsync((unsigned char*)data + j * eb, scratch, N * eb, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaGetLastError());
+  } catch (...) {
+    cudaStreamSynchronize(ps);
+    cudaStreamSynchronize(st);
+    if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+    A.release(st);
+    throw;
+  }
+  cudaEvent_t done;
+  CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  CK(cudaEventRecord(done, ps));
+  CK(cudaStreamWaitEvent(st, done, 0));
+  cudaEventDestroy(done);
+  if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+  A.release(st);
+}
+
+// One pair [0, n1+n2) split over peer buffers (PeerSpan, pair-relative
+// positions).  phase 1: the phase-1 tiles of `part` (in place); phase 2 (one
+// part, after every part's phase 1 has completed): the tail insertion.  Both
+// phases derive the same data-independent plan from the stream.
+static void run_pair_peers(int eb, const PeerSpan& span, uint64_t n1, uint64_t n2, const StreamDesc& sd, int part,
+                           int phase, unsigned long long* d_bits, cudaStream_t st) {
+  setup_pool_once();
+  Arena A;
+  cudaStream_t ps = side_stream();
+  std::vector<LevelBufs> lv(1);
+  LevelBufs& L = lv[0];
+  const uint64_t N = n1 + n2;
+  L.LJ.J = make_job(1, N, 0, 0, 0);
+  L.LJ.E = ExplicitTask{1, 0, n1, n2, sd};
+  L.LJ.r = 1;
+  L.LJ.npairs = 1;
+  L.npairs = 1;
+  L.sbs = (N + 1 + 511) / 512 + 1;
+  L.tpp = tree_tiles_per_pair(L.LJ, eb);
+  try {
+    fork_side(st, ps);
+    build_plans(lv, eb, d_bits, A, ps, st);
+    if (phase == 1) {
+      launch_merge_tree_peer(eb, span, L.plans, L.rank, L.chains, L.tpp, (uint32_t)part, st);
+    } else {
+      CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
+      launch_tail_apply_peer(eb, span, L.dst, L.src, L.tmp, 2 * L.total, st);
+    }
     CK(cudaGetLastError());
   } catch (...) {
     cudaStreamSynchronize(ps);
@@ -706,6 +757,98 @@ int sk_merge_range(void* data, int elem_bytes, uint64_t j, uint64_t k, uint64_t 
   }
   CK(cudaFreeAsync(d_bits, st));
   advance_state(state_io, bits);
+  SK_CATCH
+}
+
+int sk_merge_range_peers(void* const* part_bases, const uint64_t* part_starts, int nparts, int part, int elem_bytes,
+                         uint64_t n1, uint64_t n2, const uint64_t state[4], int phase, uint64_t* bits_out,
+                         void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (!part_bases || !part_starts || !state || nparts < 1 || nparts > 8 || part < 0 || part >= nparts ||
+      (phase != 1 && phase != 2)) {
+    set_err("bad peer span arguments");
+    return SK_EINVAL;
+  }
+  if (part_starts[0] != 0 || part_starts[nparts] != n1 + n2) {
+    set_err("parts must cover [0, n1+n2)");
+    return SK_EINVAL;
+  }
+  for (int k = 0; k < nparts; ++k)
+    if (part_starts[k + 1] < part_starts[k] || !part_bases[k]) {
+      set_err("parts must be ordered and non-null");
+      return SK_EINVAL;
+    }
+  if (state[2] > 63) { set_err("buffered_bits must be < 64"); return SK_EINVAL; }
+  if (bits_out) *bits_out = 0;
+  if (n1 == 0 || n2 == 0) return SK_OK;  // _kernels.py:99-100
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  PeerSpan span{};
+  span.n = nparts;
+  for (int k = 0; k < nparts; ++k) {
+    span.base[k] = part_bases[k];
+    span.start[k] = part_starts[k];
+  }
+  span.start[nparts] = part_starts[nparts];
+  uint64_t sv[4] = {state[0], state[1], state[2], state[3]};
+  unsigned long long* d_bits;
+  CK(cudaMallocAsync((void**)&d_bits, 8, st));
+  CK(cudaMemsetAsync(d_bits, 0, 8, st));
+  uint64_t bits = 0;
+  try {
+    run_pair_peers(elem_bytes, span, n1, n2, desc_from_state(sv), part, phase, d_bits, st);
+    fetch_bits(d_bits, &bits, 1, st);
+  } catch (...) {
+    cudaFreeAsync(d_bits, st);
+    throw;
+  }
+  CK(cudaFreeAsync(d_bits, st));
+  if (bits_out && phase == 2) *bits_out = bits;
+  SK_CATCH
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (no libcuda link)
+typedef int (*sk_get_range_fn)(unsigned long long*, size_t*, unsigned long long);
+static sk_get_range_fn get_range_fn() {
+  static sk_get_range_fn f = nullptr;
+  if (!f) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f = (sk_get_range_fn)p;
+  }
+  return f;
+}
+
+int sk_ipc_get_handle(const void* ptr, void* handle_out, uint64_t* offset_out) {
+  if (!ptr || !handle_out || !offset_out) { set_err("null argument"); return SK_EINVAL; }
+  SK_TRY
+  sk_get_range_fn f = get_range_fn();
+  if (!f) { set_err("cuMemGetAddressRange unavailable"); return SK_ECUDA; }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (f(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0) { set_err("cuMemGetAddressRange failed"); return SK_ECUDA; }
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base));
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (uint64_t)((uintptr_t)ptr - (uintptr_t)base);
+  SK_CATCH
+}
+
+int sk_ipc_open(const void* handle, void** base_out) {
+  if (!handle || !base_out) { set_err("null argument"); return SK_EINVAL; }
+  SK_TRY
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  CK(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+  SK_CATCH
+}
+
+int sk_ipc_close(void* base) {
+  SK_TRY
+  CK(cudaIpcCloseMemHandle(base));
   SK_CATCH
 }
 

@@ -990,6 +990,40 @@ __global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_peer_kernel(const Pe
 }
 
 template <typename V>
+static void merge_tree_peer_t(const PeerSpan& ps, const PairPlan* plans, const uint64_t* rank, const uint64_t* chains,
+                              uint32_t tpp, uint32_t part, cudaStream_t st) {
+  PeerParts<V> P{};
+  P.n = ps.n;
+  bool tma = true;
+  const uintptr_t ref = reinterpret_cast<uintptr_t>(ps.base[0]) - ps.start[0] * sizeof(V);
+  for (int k = 0; k < ps.n; ++k) {
+    P.base[k] = reinterpret_cast<V*>(ps.base[k]);
+    P.start[k] = ps.start[k];
+    const uintptr_t z = reinterpret_cast<uintptr_t>(ps.base[k]) - ps.start[k] * sizeof(V);
+    tma = tma && ((z - ref) & 15) == 0 && (ps.start[k] * sizeof(V)) % 16 == 0;
+  }
+  P.start[ps.n] = ps.start[ps.n];
+  P.tma = tma ? 1 : 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(merge_tree_peer_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TreeCfg<V>::SMEM);
+    attr = true;
+  }
+  const uint32_t nparts = (uint32_t)ps.n;
+  const uint32_t grid = (tpp + nparts - 1 - part) / nparts;
+  if (!grid) return;
+  merge_tree_peer_kernel<V><<<grid, kTreeBlock, TreeCfg<V>::SMEM, st>>>(P, plans, rank, chains, tpp, part, nparts);
+  count_launch();
+}
+
+void launch_merge_tree_peer(int eb, const PeerSpan& ps, const PairPlan* plans, const uint64_t* rank,
+                            const uint64_t* chains, uint32_t tpp, uint32_t part, cudaStream_t st) {
+  if (eb == 4) merge_tree_peer_t<uint32_t>(ps, plans, rank, chains, tpp, part, st);
+  else merge_tree_peer_t<unsigned long long>(ps, plans, rank, chains, tpp, part, st);
+}
+
+template <typename V>
 static void merge_tree_t(void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
                          const uint64_t* chains, uint32_t tpp, cudaStream_t st) {
   const size_t smem = TreeCfg<V>::SMEM;
@@ -1178,6 +1212,47 @@ __global__ void tail_scatter_kernel(V* __restrict__ buf, const uint64_t* __restr
                                     const V* __restrict__ tmp, uint64_t n) {
   uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n && dst[k] != kNone) buf[dst[k]] = tmp[k];
+}
+
+// Tail insertion over a pair split across peer buffers (positions are pair
+// relative: the (dst, src) plan of an explicit pair with lo = 0).
+template <typename V>
+__global__ void tail_gather_peer_kernel(const PeerParts<V> P, const uint64_t* __restrict__ dst,
+                                        const uint64_t* __restrict__ src, V* __restrict__ tmp, uint64_t n) {
+  uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const PeerAcc<V> acc{P};
+  if (k < n && dst[k] != kNone) tmp[k] = acc.ld(src[k]);
+}
+template <typename V>
+__global__ void tail_scatter_peer_kernel(const PeerParts<V> P, const uint64_t* __restrict__ dst,
+                                         const V* __restrict__ tmp, uint64_t n) {
+  uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const PeerAcc<V> acc{P};
+  if (k < n && dst[k] != kNone) acc.st(dst[k], tmp[k]);
+}
+
+template <typename V>
+static void tail_apply_peer_t(const PeerSpan& ps, const uint64_t* dst, const uint64_t* src, void* tmp,
+                              uint64_t nslots, cudaStream_t st) {
+  PeerParts<V> P{};
+  P.n = ps.n;
+  for (int k = 0; k < ps.n; ++k) {
+    P.base[k] = reinterpret_cast<V*>(ps.base[k]);
+    P.start[k] = ps.start[k];
+  }
+  P.start[ps.n] = ps.start[ps.n];
+  unsigned b = (unsigned)((nslots + 255) / 256);
+  tail_gather_peer_kernel<V><<<b, 256, 0, st>>>(P, dst, src, (V*)tmp, nslots);
+  tail_scatter_peer_kernel<V><<<b, 256, 0, st>>>(P, dst, (const V*)tmp, nslots);
+  count_launch();
+  count_launch();
+}
+
+void launch_tail_apply_peer(int eb, const PeerSpan& ps, const uint64_t* dst, const uint64_t* src, void* tmp,
+                            uint64_t nslots, cudaStream_t st) {
+  if (!nslots) return;
+  if (eb == 4) tail_apply_peer_t<uint32_t>(ps, dst, src, tmp, nslots, st);
+  else tail_apply_peer_t<unsigned long long>(ps, dst, src, tmp, nslots, st);
 }
 
 void launch_tail_apply(int eb, void* buf, const uint64_t* dst, const uint64_t* src, void* tmp, uint64_t nslots,

@@ -23,6 +23,11 @@ void debug_set_seg_variant(int v);
 bool merge_tree_active();
 
 // merge.cu
+struct PeerSpan {             // a pair split into contiguous parts in different (peer) buffers
+  void* base[8];              // element at pair position start[k] of part k
+  uint64_t start[9];
+  int n;
+};
 struct LevelTail {            // device-side view used by the all-levels tail decoder
   PairPlan* plans;
   uint64_t npairs;
@@ -56,6 +61,10 @@ void launch_tail_plan(const PairPlan* plans, const uint64_t* rec_key, const uint
 void launch_tail_chase(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair,
                        const uint64_t* predx, const uint8_t* keyed, uint64_t total, uint64_t* dst, uint64_t* src,
                        cudaStream_t st);
+void launch_merge_tree_peer(int eb, const PeerSpan& ps, const PairPlan* plans, const uint64_t* rank,
+                            const uint64_t* chains, uint32_t tpp, uint32_t part, cudaStream_t st);
+void launch_tail_apply_peer(int eb, const PeerSpan& ps, const uint64_t* dst, const uint64_t* src, void* tmp,
+                            uint64_t nslots, cudaStream_t st);
 void launch_tail_apply(int eb, void* buf, const uint64_t* dst, const uint64_t* src, void* tmp, uint64_t nslots,
                        cudaStream_t st);
 

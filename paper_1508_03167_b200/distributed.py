@@ -9,11 +9,16 @@ ranks (a power of two dividing q = 2^c), rank r owns leaf blocks
   single-GPU schedule (C ABI sk_merge_shuffle_shard) -- no communication.
 * Rounds c-log2(G)+1 .. c merge pairs spanning 2, 4, .., G ranks.  The pair's
   bit stream is regenerated locally (it is a pure function of the seed and the
-  substream index r*q+i), the pair's elements are all-gathered inside the
-  spanning group, every member runs the merge (sk_merge_range on a fresh
-  substream) and keeps its own slice.  This is the NCCL baseline for the
-  exchange step; a peer-memory gather of only the positions each rank writes
-  (50 / 62.5 / 68.75 % of a shard at spans 2 / 4 / 8) is the planned upgrade.
+  substream index r*q+i), so no bits travel.  Default exchange ("peer"): every
+  rank maps the other ranks' shard buffers (CUDA IPC handles, all-gathered
+  once), and the pair is merged by ONE fused kernel per rank over peer memory
+  (sk_merge_range_peers phase 1: the rank takes every span-th tile of the
+  pair's tree merge, TMA-loading its windows from whichever GPU holds them and
+  storing them back there -- the exchange overlaps the merge tile by tile);
+  after a barrier of the span the first rank applies the tail insertion
+  (phase 2).  Each element crosses NVLink at most once each way.
+  The NCCL baseline ("allgather"): the pair's elements all-gathered inside the
+  spanning group, every member merges the whole pair, keeps its slice.
 
 The result (and the bit count, all-reduced) is identical to the 1-GPU and the
 reference output for the same (n, cutoff, seed).
@@ -56,6 +61,36 @@ class CudaEngine:
                                            self._stream()))
         return int(st[3])
 
+    # -- peer memory (CUDA IPC over NVLink) --------------------------------
+    def peer_handle(self, buf: torch.Tensor) -> bytes:
+        h = (ctypes.c_ubyte * 64)()
+        off = ctypes.c_uint64(0)
+        _lib.check(self.lib.sk_ipc_get_handle(ctypes.c_void_p(buf.data_ptr()), h, ctypes.byref(off)))
+        return bytes(h) + int(off.value).to_bytes(8, "little")
+
+    def open_peer(self, handle: bytes) -> int:
+        base = ctypes.c_void_p(0)
+        h = (ctypes.c_ubyte * 64).from_buffer_copy(handle[:64])
+        _lib.check(self.lib.sk_ipc_open(h, ctypes.byref(base)))
+        self._opened = getattr(self, "_opened", []) + [base.value]
+        return int(base.value) + int.from_bytes(handle[64:72], "little")
+
+    def close_peers(self) -> None:
+        for b in getattr(self, "_opened", []):
+            self.lib.sk_ipc_close(ctypes.c_void_p(b))
+        self._opened = []
+
+    def merge_peers(self, bases: List[int], starts: List[int], part: int, elem_bytes: int, n1: int, n2: int,
+                    sseed: int, phase: int) -> int:
+        n = len(bases)
+        pb = (ctypes.c_void_p * n)(*bases)
+        ps = (ctypes.c_uint64 * (n + 1))(*starts)
+        st = _lib.state_array((sseed, 0, 0, 0))
+        bits = ctypes.c_uint64(0)
+        _lib.check(self.lib.sk_merge_range_peers(pb, ps, n, part, elem_bytes, n1, n2, st, phase, ctypes.byref(bits),
+                                                 self._stream()))
+        return int(bits.value)
+
 
 def shard_layout(n: int, cutoff: int, world: int):
     """(c, q, bounds, nblk, local_rounds) of a world-way contiguous sharding."""
@@ -97,10 +132,17 @@ _GROUPS = {}
 
 
 def merge_shuffle_sharded(shard: torch.Tensor, n: int, cutoff: Optional[int], seed: int,
-                          engine=None) -> int:
+                          engine=None, exchange: str = "peer") -> int:
     """Shuffle the n-element array whose contiguous shard this rank holds
     (shard_range(n, cutoff, world, rank)); returns the total bit count
-    (ShuffleReport.bits of the whole shuffle) on every rank."""
+    (ShuffleReport.bits of the whole shuffle) on every rank.
+
+    exchange = "peer": the spanning rounds run as one fused kernel per rank
+    over peer memory (sk_merge_range_peers: each rank merges its share of the
+    pair's tiles, reading and writing the other ranks' shards directly over
+    NVLink; one rank applies the tail after a barrier).  exchange =
+    "allgather": the NCCL baseline (the pair all-gathered, merged redundantly
+    by every member, own slice kept)."""
     world, rank = dist.get_world_size(), dist.get_rank()
     cutoff = MERGE_CUTOFF_DEFAULT if cutoff is None else cutoff
     engine = engine or CudaEngine()
@@ -110,9 +152,57 @@ def merge_shuffle_sharded(shard: torch.Tensor, n: int, cutoff: Optional[int], se
     if shard.numel() != hi - lo:
         raise ValueError(f"rank {rank} shard has {shard.numel()} elements, expected {hi - lo}")
     bits = engine.shard(shard, n, cutoff, seed, blk0, nblk, local_rounds)
+    if world > 1 and exchange == "peer":
+        bits += _spanning_rounds_peer(shard, n, seed, engine, c, q, bounds, nblk, local_rounds)
+    elif world > 1:
+        bits += _spanning_rounds_allgather(shard, seed, engine, c, q, bounds, nblk, local_rounds)
     if world > 1:
-        groups = _GROUPS.setdefault(world, _Groups(world))
-        sizes = [bounds[(r + 1) * nblk] - bounds[r * nblk] for r in range(world)]
+        t = torch.tensor([bits], dtype=torch.float64, device=shard.device)
+        # bit counts fit 2^53 exactly for n < 2^47
+        dist.all_reduce(t)
+        bits = int(t.item())
+    return bits
+
+
+def _spanning_rounds_peer(shard, n, seed, engine, c, q, bounds, nblk, local_rounds) -> int:
+    world, rank = dist.get_world_size(), dist.get_rank()
+    groups = _GROUPS.setdefault(world, _Groups(world))
+    # every rank's shard buffer, mapped into this process (own: its pointer)
+    h = torch.tensor(list(engine.peer_handle(shard)), dtype=torch.uint8, device=shard.device)
+    hs = [torch.empty_like(h) for _ in range(world)]
+    dist.all_gather(hs, h)
+    ptr = [shard.data_ptr() if r == rank else engine.open_peer(bytes(hs[r].cpu().tolist())) for r in range(world)]
+    eb = shard.element_size()
+    bits = 0
+    try:
+        dist.barrier()  # every rank's local rounds are done before peers are touched
+        for r in range(local_rounds + 1, c + 1):
+            span = 1 << (r - local_rounds)
+            g0 = (rank // span) * span
+            p = 1 << (r - 1)
+            i = ((rank * nblk) // (2 * p)) * (2 * p)  # first block of the spanning pair
+            j, k, l = bounds[i], bounds[i + p], bounds[i + 2 * p]
+            starts = [bounds[(g0 + m) * nblk] - j for m in range(span)] + [l - j]
+            bases = [ptr[g0 + m] for m in range(span)]
+            sseed = substream_seed(seed, r * q + i)
+            grp = groups.get(span, g0)
+            engine.merge_peers(bases, starts, rank - g0, eb, k - j, l - k, sseed, 1)
+            dist.barrier(group=grp)
+            if rank == g0:
+                bits += engine.merge_peers(bases, starts, 0, eb, k - j, l - k, sseed, 2)
+            dist.barrier(group=grp)
+    finally:
+        engine.close_peers()
+    return bits
+
+
+def _spanning_rounds_allgather(shard, seed, engine, c, q, bounds, nblk, local_rounds) -> int:
+    world, rank = dist.get_world_size(), dist.get_rank()
+    blk0 = rank * nblk
+    lo, hi = bounds[blk0], bounds[blk0 + nblk]
+    bits = 0
+    groups = _GROUPS.setdefault(world, _Groups(world))
+    sizes = [bounds[(r + 1) * nblk] - bounds[r * nblk] for r in range(world)]
     for r in range(local_rounds + 1, c + 1):
         span = 1 << (r - local_rounds)
         g0 = (rank // span) * span
@@ -129,19 +219,16 @@ def merge_shuffle_sharded(shard: torch.Tensor, n: int, cutoff: Optional[int], se
         shard.copy_(pair[lo - j:hi - j])
         if rank == g0:
             bits += pb
-    if world > 1:
-        t = torch.tensor([bits], dtype=torch.float64, device=shard.device)
-        # bit counts fit 2^53 exactly for n < 2^47
-        dist.all_reduce(t)
-        bits = int(t.item())
     return bits
 
 
 def simulate_sharded(data: torch.Tensor, n: int, cutoff: Optional[int], seed: int, world: int,
-                     engine=None) -> int:
+                     engine=None, exchange: str = "allgather") -> int:
     """The sharded schedule of merge_shuffle_sharded executed by ONE process
     over all `world` shards in turn (no collectives): validates the per-shard
-    entry point and the cross-round logic on a single device."""
+    entry point and the cross-round logic on a single device.  exchange =
+    "peer" runs the spanning rounds through sk_merge_range_peers with every
+    part's phase 1 in turn (the parts are slices of `data`)."""
     cutoff = MERGE_CUTOFF_DEFAULT if cutoff is None else cutoff
     engine = engine or CudaEngine()
     c, q, bounds, nblk, local_rounds = shard_layout(n, cutoff, world)
@@ -154,7 +241,18 @@ def simulate_sharded(data: torch.Tensor, n: int, cutoff: Optional[int], seed: in
         p = 1 << (rr - 1)
         for i in range(0, q, 2 * p):
             j, k, l = bounds[i], bounds[i + p], bounds[i + 2 * p]
-            pair = data[j:l].clone()
-            bits += engine.merge(pair, 0, k - j, l - j, substream_seed(seed, rr * q + i))
-            data[j:l].copy_(pair)
+            sseed = substream_seed(seed, rr * q + i)
+            if exchange == "peer":
+                span = 1 << (rr - local_rounds)
+                r0 = i // nblk
+                starts = [bounds[(r0 + m) * nblk] - j for m in range(span)] + [l - j]
+                eb = data.element_size()
+                bases = [data.data_ptr() + eb * bounds[(r0 + m) * nblk] for m in range(span)]
+                for m in range(span):
+                    engine.merge_peers(bases, starts, m, eb, k - j, l - k, sseed, 1)
+                bits += engine.merge_peers(bases, starts, 0, eb, k - j, l - k, sseed, 2)
+            else:
+                pair = data[j:l].clone()
+                bits += engine.merge(pair, 0, k - j, l - j, sseed)
+                data[j:l].copy_(pair)
     return bits

@@ -8,6 +8,31 @@ from paper_1508_03167_b200.shufflers import merge_plan
 
 
 class OracleEngine:
+    """`whole` (optional): a shared-memory tensor holding every rank's shard
+    back to back, so the peer exchange can be emulated across CPU processes:
+    phase 1 is a no-op, phase 2 merges the whole pair in place."""
+
+    def __init__(self, whole=None):
+        self.whole = whole
+
+    def peer_handle(self, buf):
+        off = (buf.data_ptr() - self.whole.data_ptr()) // buf.element_size()
+        return bytes(64) + int(off).to_bytes(8, "little")
+
+    def open_peer(self, handle):
+        return self.whole.data_ptr() + self.whole.element_size() * int.from_bytes(handle[64:72], "little")
+
+    def close_peers(self):
+        pass
+
+    def merge_peers(self, bases, starts, part, elem_bytes, n1, n2, sseed, phase):
+        if phase == 1:
+            return 0
+        off = (bases[0] - self.whole.data_ptr()) // elem_bytes
+        st = O.state_vec(sseed, 0, 0, 0)
+        O.merge(self.whole.numpy(), off, off + n1, off + n1 + n2, st)
+        return int(st[3])
+
     def shard(self, buf, n, cutoff, seed, blk0, nblk, rounds):
         a = buf.numpy()
         assert a.dtype == np.int64

@@ -21,7 +21,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, n, cutoff, seed, out_dir):
+def _worker(rank, world, port, n, cutoff, seed, out_dir, exchange="allgather", whole=None):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -31,8 +31,12 @@ def _worker(rank, world, port, n, cutoff, seed, out_dir):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     lo, hi = D.shard_range(n, cutoff, world, rank)
-    shard = torch.arange(lo, hi, dtype=torch.int64)
-    bits = D.merge_shuffle_sharded(shard, n, cutoff, seed, engine=OracleEngine())
+    if whole is not None:  # peer exchange: shards are views of one shared-memory array
+        shard = whole[lo:hi]
+        shard.copy_(torch.arange(lo, hi, dtype=torch.int64))
+    else:
+        shard = torch.arange(lo, hi, dtype=torch.int64)
+    bits = D.merge_shuffle_sharded(shard, n, cutoff, seed, engine=OracleEngine(whole), exchange=exchange)
     np.save(os.path.join(out_dir, f"r{rank}.npy"), shard.numpy())
     np.save(os.path.join(out_dir, f"b{rank}.npy"), np.array([bits], dtype=np.int64))
     dist.barrier()
@@ -48,6 +52,20 @@ def test_sharded_equals_single(tmp_path, world, n, cutoff, seed):
     bits = [int(np.load(tmp_path / f"b{r}.npy")[0]) for r in range(world)]
     ref, rbits = O.merge_shuffle_perm(n, cutoff, seed)
     assert np.array_equal(got, ref)
+    assert all(b == rbits for b in bits)
+
+
+@pytest.mark.parametrize("world,n,cutoff,seed", [(2, 5000, 300, 5), (4, 10_003, 1000, 6)])
+def test_sharded_peer_exchange_orchestration(tmp_path, world, n, cutoff, seed):
+    # the peer-exchange driver (handle exchange, phase-1 parts, barrier,
+    # phase-2 tail by the span's first rank, bit accounting) over gloo; the
+    # "peer memory" is one shared-memory array
+    port = _free_port()
+    whole = torch.zeros(n, dtype=torch.int64).share_memory_()
+    mp.spawn(_worker, args=(world, port, n, cutoff, seed, str(tmp_path), "peer", whole), nprocs=world, join=True)
+    bits = [int(np.load(tmp_path / f"b{r}.npy")[0]) for r in range(world)]
+    ref, rbits = O.merge_shuffle_perm(n, cutoff, seed)
+    assert np.array_equal(whole.numpy(), ref)
     assert all(b == rbits for b in bits)
 
 

@@ -194,6 +194,52 @@ def test_determinism_and_seed_sensitivity():
     assert torch.equal(a, b) and not torch.equal(a, c)
 
 
+@pytest.mark.parametrize("n", [1 << 20, (1 << 20) + 12345])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_peer_exchange_on_one_gpu(world, n):
+    # the fused peer-memory merge of the spanning rounds (sk_merge_range_peers,
+    # every part's phase 1 in turn, then the tail), parts = slices of one
+    # buffer: 16-byte aligned part boundaries (TMA path) and ragged ones
+    from paper_1508_03167_b200 import distributed as D
+    cutoff, seed = 32768, 23
+    data = torch.arange(n, dtype=torch.int32, device="cuda")
+    bits = D.simulate_sharded(data, n, cutoff, seed, world, exchange="peer")
+    ref, rbits = O.merge_shuffle_perm(n, cutoff, seed)
+    assert bits == rbits
+    assert np.array_equal(data.cpu().numpy(), ref.astype(np.int32))
+
+
+def test_merge_range_peers_random_splits():
+    from paper_1508_03167_b200 import distributed as D
+    eng = D.CudaEngine()
+    rng = np.random.default_rng(31)
+    for trial in range(12):
+        n1, n2 = int(rng.integers(1, 200_000)), int(rng.integers(1, 200_000))
+        N = n1 + n2
+        nparts = int(rng.integers(1, 9))
+        cuts = sorted(int(x) for x in rng.integers(0, N, nparts - 1))
+        starts = [0] + cuts + [N]
+        dt = torch.int64 if trial % 2 else torch.int32
+        # each part in its own buffer, at an odd element offset for some
+        bufs, bases = [], []
+        for k in range(nparts):
+            pad = int(rng.integers(0, 3))
+            b = torch.empty(starts[k + 1] - starts[k] + pad, dtype=dt, device="cuda")
+            b[pad:] = torch.arange(starts[k], starts[k + 1], dtype=dt, device="cuda")
+            bufs.append((b, pad))
+            bases.append(b.data_ptr() + pad * b.element_size())
+        seed = int(rng.integers(0, 2 ** 63))
+        for k in range(nparts):
+            eng.merge_peers(bases, starts, k, bufs[0][0].element_size(), n1, n2, seed, 1)
+        bits = eng.merge_peers(bases, starts, 0, bufs[0][0].element_size(), n1, n2, seed, 2)
+        got = torch.cat([b[pad:] for b, pad in bufs]).cpu().numpy().astype(np.int64)
+        ref = np.arange(N, dtype=np.int64)
+        st = O.state_vec(seed, 0, 0, 0)
+        O.merge(ref, 0, n1, N, st)
+        assert bits == int(st[3])
+        assert np.array_equal(got, ref)
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_sharded_schedule_on_one_gpu(world):
     # the multi-GPU schedule (per-shard C-ABI calls + spanning-round merges),
