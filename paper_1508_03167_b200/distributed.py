@@ -69,16 +69,19 @@ class CudaEngine:
         return bytes(h) + int(off.value).to_bytes(8, "little")
 
     def open_peer(self, handle: bytes) -> int:
-        base = ctypes.c_void_p(0)
-        h = (ctypes.c_ubyte * 64).from_buffer_copy(handle[:64])
-        _lib.check(self.lib.sk_ipc_open(h, ctypes.byref(base)))
-        self._opened = getattr(self, "_opened", []) + [base.value]
-        return int(base.value) + int.from_bytes(handle[64:72], "little")
+        # mappings are cached per process (an allocation is mapped once; the
+        # caching allocator keeps shard buffers alive across calls)
+        key = bytes(handle[:64])
+        base = _PEER_MAPS.get(key)
+        if base is None:
+            b = ctypes.c_void_p(0)
+            h = (ctypes.c_ubyte * 64).from_buffer_copy(key)
+            _lib.check(self.lib.sk_ipc_open(h, ctypes.byref(b)))
+            base = _PEER_MAPS[key] = int(b.value)
+        return base + int.from_bytes(handle[64:72], "little")
 
     def close_peers(self) -> None:
-        for b in getattr(self, "_opened", []):
-            self.lib.sk_ipc_close(ctypes.c_void_p(b))
-        self._opened = []
+        pass  # see release_peer_maps()
 
     def merge_peers(self, bases: List[int], starts: List[int], part: int, elem_bytes: int, n1: int, n2: int,
                     sseed: int, phase: int) -> int:
@@ -90,6 +93,17 @@ class CudaEngine:
         _lib.check(self.lib.sk_merge_range_peers(pb, ps, n, part, elem_bytes, n1, n2, st, phase, ctypes.byref(bits),
                                                  self._stream()))
         return int(bits.value)
+
+
+_PEER_MAPS = {}
+
+
+def release_peer_maps() -> None:
+    """Unmap every peer allocation mapped by this process."""
+    lib = _lib.load()
+    for base in _PEER_MAPS.values():
+        lib.sk_ipc_close(ctypes.c_void_p(base))
+    _PEER_MAPS.clear()
 
 
 def shard_layout(n: int, cutoff: int, world: int):
