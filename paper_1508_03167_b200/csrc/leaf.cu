@@ -210,7 +210,6 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
     }
     const uint16_t* __restrict__ dr = draws + L.lo;
     if (tid == 0) {  // pull this leaf's data and the next leaf's draws into L2
-      l2_prefetch(src_in, (size_t)m * sizeof(V));
       if (g == blockIdx.x) l2_prefetch(dr, (size_t)m * 2);
       if (g + gridDim.x < nleaves) {
         const LeafDesc Ln = leaf_desc(J, E, g + gridDim.x);
@@ -219,6 +218,9 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
     }
     for (uint32_t T0 = 0; T0 < m; T0 += kLeafHalf) {
       const uint32_t nt = min(kLeafHalf, m - T0);  // targets [T0, T0+nt)
+      // the leaf's data is gathered only at the end: pull it into L2 during
+      // the last target half (earlier it would be evicted before use)
+      if (tid == 0 && T0 + kLeafHalf >= m) l2_prefetch(src_in, (size_t)m * sizeof(V));
       for (uint32_t w = tid; w < ((nt + 1) >> 1); w += BLOCK) sh[w] = 0;
       __syncthreads();
       // 1. histogram of this half's targets (steps s = 1 .. m-1)
