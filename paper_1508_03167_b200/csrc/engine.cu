@@ -577,6 +577,7 @@ int sk_version(void) { return 1; }
 int sk_debug_set(int key, int value) {
   if (key == 1) { debug_set_leaf_stop(value); return 0; }
   if (key == 2) { debug_set_seg_variant(value); return 0; }
+  if (key == 4) { debug_set_tree_force_direct(value); return 0; }
   return -1;
 }
 const char* sk_last_error(void) { return g_err.c_str(); }

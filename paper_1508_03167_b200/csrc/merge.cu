@@ -528,6 +528,10 @@ void launch_tree_chains(int eb, const PairPlan* plans, uint64_t npairs, const ui
   count_launch();
 }
 
+// debug: 1 = every tile takes the direct (window-by-window) path
+__device__ int g_tree_force_direct = 0;
+void debug_set_tree_force_direct(int v) { cudaMemcpyToSymbol(g_tree_force_direct, &v, sizeof(int)); }
+
 // Element access of one pair for the tree kernels: FlatAcc = the pair in one
 // buffer (in/out may differ); PeerAcc = the pair split into up to kMaxParts
 // contiguous parts living in different buffers (other GPUs' memory mapped
@@ -824,7 +828,8 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
     }
     const uint32_t treg = __shfl_sync(0xffffffffu, sreg, 31), tgc = __shfl_sync(0xffffffffu, sgc, 31);
     const uint32_t tby = __shfl_sync(0xffffffffu, sby, 31);
-    const bool ok = nw < (uint32_t)kTreeD && !__any_sync(0xffffffffu, big) && treg <= C::SCAP && tgc <= C::GCAP;
+    const bool ok = nw < (uint32_t)kTreeD && !__any_sync(0xffffffffu, big) && treg <= C::SCAP && tgc <= C::GCAP &&
+                    !g_tree_force_direct;
     if (act) {
       stoff[lane] = sreg - reg + mis;
       goff[lane] = sgc - gc;

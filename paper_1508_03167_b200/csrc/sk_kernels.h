@@ -21,6 +21,7 @@ void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64
 void debug_set_leaf_stop(int v);
 void debug_set_seg_variant(int v);
 bool merge_tree_active();
+void debug_set_tree_force_direct(int v);
 
 // merge.cu
 struct PeerSpan {             // a pair split into contiguous parts in different (peer) buffers

@@ -261,3 +261,32 @@ def test_config4_sharded_2p24_uint64_golden():
     bits = D.simulate_sharded(data, 1 << 24, None, case["seed"], 8)
     assert bits == case["bits"]
     assert sha(data.cpu().numpy().astype("<u8")) == case["sha_u64"]
+
+
+@pytest.mark.parametrize("mode", ["direct", "segment"])
+def test_merge_fallback_paths(mode):
+    # the tree merge's window-by-window path (taken when a tile's windows do
+    # not fit shared memory or its chain is deeper than the stored starts) and
+    # the segment-pass kernels, forced for every tile: same results
+    import ctypes
+    from paper_1508_03167_b200 import _lib
+    lib = _lib.load()
+    lib.sk_debug_set.argtypes = [ctypes.c_int, ctypes.c_int]
+    key, on, off = (4, 1, 0) if mode == "direct" else (2, 100, 0)
+    lib.sk_debug_set(key, on)
+    try:
+        for n, cutoff, seed in [(1 << 20, 65536, 0), (300_007, 4096, 1234), (100_000, 1000, 9), (5000, 7, 3)]:
+            x, rep = gpu_perm(n, cutoff, seed, torch.int32)
+            ref, rbits = O.merge_shuffle_perm(n, cutoff, seed)
+            assert rep.bits == rbits
+            assert np.array_equal(x.cpu().numpy(), ref.astype(np.int32))
+        for dt in (torch.int32, torch.int64):
+            src = sk.BitSource(77)
+            x = torch.arange(70_001, dtype=dt, device="cuda")
+            sk.merge(x, sk.MergeRange(1, 40_000, 30_000), src)
+            a = np.arange(70_001, dtype=np.int64)
+            st = O.state_vec(77, 0, 0, 0)
+            O.merge(a, 1, 40_001, 70_001, st)
+            assert np.array_equal(x.cpu().numpy().astype(np.int64), a)
+    finally:
+        lib.sk_debug_set(key, off)
