@@ -18,3 +18,5 @@ def sha(a) -> str:
 
 def cutoff_of(case):
     return 65536 if case["cutoff"] is None else case["cutoff"]
+
+CLI = json.load(open(os.path.join(HERE, "cli.json")))
