@@ -47,6 +47,9 @@ def lib():
         L.ora_merge_shuffle_seq.argtypes = [ip, u64, u64, ip]
         L.ora_fy_range.restype = None
         L.ora_fy_range.argtypes = [ip, i64, i64, ip]
+        L.ora_rs_range.argtypes = [ip, i64, i64, u64, ip]
+        L.ora_rs_parallel.argtypes = [ip, u64, u64, u64]
+        L.ora_rs_parallel.restype = u64
         L.ora_merge.restype = None
         L.ora_merge.argtypes = [ip, i64, i64, i64, ip]
         L.ora_take.restype = u64
@@ -127,3 +130,14 @@ def chi_counts(algo: str, n: int, trials: int, seed: int, cutoff: int,
     lib().ora_chi_counts(_CHI_ALGO[algo], n, trials, seed & MASK64, cutoff,
                          _ptr(counts), threads)
     return counts
+
+
+def rs_range(arr: np.ndarray, lo: int, hi: int, cutoff: int, st: np.ndarray) -> None:
+    """rs_range_inplace (_kernels.py:449-457): sequential splitting shuffle, state in/out."""
+    lib().ora_rs_range(_ptr(arr), lo, hi, cutoff, _ptr(st))
+
+
+def rs_parallel(arr: np.ndarray, cutoff: int, seed: int) -> int:
+    """rs_shuffle_parallel (splitshuffle.py:92-133); returns ShuffleReport.bits."""
+    assert arr.dtype == np.int64 and arr.flags.c_contiguous
+    return int(lib().ora_rs_parallel(_ptr(arr), arr.shape[0], cutoff, seed & MASK64))

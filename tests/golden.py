@@ -20,3 +20,4 @@ def cutoff_of(case):
     return 65536 if case["cutoff"] is None else case["cutoff"]
 
 CLI = json.load(open(os.path.join(HERE, "cli.json")))
+RS = json.load(open(os.path.join(HERE, "rs.json")))
