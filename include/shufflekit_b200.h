@@ -75,6 +75,22 @@ int sk_fy_range(void *data, int elem_bytes, uint64_t lo, uint64_t hi, uint64_t s
 int sk_merge_range(void *data, int elem_bytes, uint64_t j, uint64_t k, uint64_t l, uint64_t state_io[4],
                    void *stream);
 
+/* Rao-Sandelius splitting shuffle (the paper's baseline).
+ * Replaces splitshuffle.rs_shuffle_parallel (splitshuffle.py:92-133): ranges
+ * larger than 2^14 flip one coin per element from substream depth*(n+1)+lo and
+ * are stably partitioned, smaller ones run the sequential splitting shuffle
+ * (Fisher-Yates at <= cutoff) on their own substream.  cutoff = 0 selects
+ * RS_CUTOFF_DEFAULT (4096, splitshuffle.py:27).  *bits_out = ShuffleReport.bits
+ * (synchronizes). */
+int sk_rs_shuffle_parallel(void *data, int elem_bytes, uint64_t n, uint64_t cutoff, uint64_t seed,
+                           uint64_t *bits_out, void *stream);
+
+/* Replaces _kernels.rs_range_inplace (_kernels.py:449-457) / rs_shuffle
+ * (splitshuffle.py:66-79): the sequential splitting shuffle of [lo, hi) from a
+ * mid-stream state (cutoff 0 = 4096). */
+int sk_rs_range(void *data, int elem_bytes, uint64_t lo, uint64_t hi, uint64_t cutoff, uint64_t state_io[4],
+                void *stream);
+
 /* Multi-GPU exchange step (SURVEY.md §8 e): the merge of one pair [0, n1+n2)
  * whose elements are split into `nparts` contiguous parts held by different
  * GPUs; part k = positions [part_starts[k], part_starts[k+1]) at device

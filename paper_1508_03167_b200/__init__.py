@@ -9,6 +9,7 @@ from .bitstream import (BitSource, DrawTape, TapeExhausted, advance_state, mix64
 from .shufflers import (MERGE_CUTOFF_DEFAULT, MergeRange, ShuffleConfig, ShuffleReport, batched_shuffle,
                         fisher_yates, merge, merge_plan, merge_rounds, merge_shuffle, merge_shuffle_parallel,
                         merge_task_indices)
+from .splitshuffle import RS_CUTOFF_DEFAULT, rs_shuffle, rs_shuffle_parallel
 from .verify import ChiSquareResult, chi_counts, chi_square_threshold, chi_square_uniformity, permutation_rank
 
 __version__ = "0.1.0"
@@ -18,5 +19,5 @@ __all__ = [
     "advance_state", "MergeRange", "ShuffleConfig", "ShuffleReport", "MERGE_CUTOFF_DEFAULT", "fisher_yates",
     "merge", "merge_plan", "merge_rounds", "merge_task_indices", "merge_shuffle", "merge_shuffle_parallel",
     "batched_shuffle", "ChiSquareResult", "chi_counts", "chi_square_threshold", "chi_square_uniformity",
-    "permutation_rank",
+    "permutation_rank", "RS_CUTOFF_DEFAULT", "rs_shuffle", "rs_shuffle_parallel",
 ]

@@ -23,6 +23,8 @@ SIGNATURES = {
     "sk_merge_shuffle_parallel_host": (_int, [_vp, _int, _u64, _u64, _u64, _u64p, _vp]),
     "sk_merge_shuffle_shard": (_int, [_vp, _int, _u64, _u64, _u64, _u64, _u64, _int, _u64p, _vp]),
     "sk_batched_shuffle": (_int, [_vp, _int, _u64, _u64, _u64, _u64, _u64p, _vp]),
+    "sk_rs_shuffle_parallel": (_int, [_vp, _int, _u64, _u64, _u64, _u64p, _vp]),
+    "sk_rs_range": (_int, [_vp, _int, _u64, _u64, _u64, _u64p, _vp]),
     "sk_merge_range_peers": (_int, [ctypes.POINTER(_vp), _u64p, _int, _int, _int, _u64, _u64, _u64p, _int, _u64p,
                                     _vp]),
     "sk_ipc_get_handle": (_int, [_vp, _vp, _u64p]),

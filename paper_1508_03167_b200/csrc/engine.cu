@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -508,6 +509,189 @@ static void run_pair_peers(int eb, const PeerSpan& span, uint64_t n1, uint64_t n
   A.release(st);
 }
 
+// ---------------------------------------------------------------- Rao-Sandelius
+// Small tasks of the splitting shuffle (rs.cu): plan on the device (one lane
+// per task), then the split nodes level by level, then the Fisher-Yates
+// leaves; every leaf's result is left in buf0 (the caller's buffer).
+// buf0/buf1/draws are indexed by global position.  Returns the tasks' bits.
+static uint64_t run_rs_tasks(int eb, void* buf0, void* buf1, const std::vector<RsTask>& tasks, uint64_t span_lo,
+                             uint64_t span_hi, uint64_t cutoff, Arena& A, cudaStream_t st) {
+  if (tasks.empty()) return 0;
+  const uint32_t nt = (uint32_t)tasks.size();
+  const uint64_t span = span_hi - span_lo;
+  RsTask* dT = A.alloc<RsTask>(nt, st);
+  CK(cudaMemcpyAsync(dT, tasks.data(), nt * sizeof(RsTask), cudaMemcpyHostToDevice, st));
+  uint16_t* draws = A.alloc<uint16_t>(span, st) - span_lo;
+  unsigned long long* counts = A.alloc<unsigned long long>(3, st);
+  unsigned long long* tbits = A.alloc<unsigned long long>(nt, st);
+  uint64_t cap = std::min<uint64_t>(span + 1, 4 * span / std::max<uint64_t>(cutoff, 1) + 4ull * nt + 1024);
+  uint64_t ncap = cap, lcap = cap;
+  std::vector<RsNode> nodes;
+  std::vector<RsLeaf> leaves;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    RsNode* dN = A.alloc<RsNode>(ncap, st);
+    RsLeaf* dL = A.alloc<RsLeaf>(lcap, st);
+    CK(cudaMemsetAsync(counts, 0, 3 * 8, st));
+    CK(cudaMemsetAsync(tbits, 0, nt * 8, st));
+    // per-task bit counts: RsTask.array indexes tbits
+    launch_rs_plan(dT, nt, cutoff, draws, dN, counts, ncap, dL, lcap, tbits, st);
+    unsigned long long hc[3];
+    CK(cudaMemcpyAsync(hc, counts, 24, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hc[2]) throw std::runtime_error("splitting-shuffle stack overflow (more than 256 pending ranges)");
+    if (hc[0] > ncap || hc[1] > lcap) {
+      ncap = hc[0];
+      lcap = hc[1];
+      continue;
+    }
+    nodes.resize(hc[0]);
+    leaves.resize(hc[1]);
+    if (hc[0]) CK(cudaMemcpyAsync(nodes.data(), dN, hc[0] * sizeof(RsNode), cudaMemcpyDeviceToHost, st));
+    if (hc[1]) CK(cudaMemcpyAsync(leaves.data(), dL, hc[1] * sizeof(RsLeaf), cudaMemcpyDeviceToHost, st));
+    break;
+  }
+  std::vector<unsigned long long> hb(nt);
+  CK(cudaMemcpyAsync(hb.data(), tbits, nt * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  uint64_t bits = 0;
+  for (auto b : hb) bits += b;
+  // split nodes, level by level (a node's input is its parent's output)
+  std::stable_sort(nodes.begin(), nodes.end(), [](const RsNode& a, const RsNode& b) { return a.level < b.level; });
+  if (!nodes.empty()) {
+    RsNode* dN = A.alloc<RsNode>(nodes.size(), st);
+    CK(cudaMemcpyAsync(dN, nodes.data(), nodes.size() * sizeof(RsNode), cudaMemcpyHostToDevice, st));
+    size_t i = 0;
+    while (i < nodes.size()) {
+      size_t j = i;
+      while (j < nodes.size() && nodes[j].level == nodes[i].level) ++j;
+      launch_rs_nodes(eb, dN + i, (uint32_t)(j - i), dT, buf0, buf1, st);
+      i = j;
+    }
+  }
+  // leaves: their data is in buf[parity ^ depth]
+  std::vector<uint64_t> lst[2], back, serial_back;
+  std::vector<RsLeaf> serial;
+  uint32_t mmax[2] = {0, 0};
+  for (const RsLeaf& lf : leaves) {
+    const uint32_t par = (tasks[lf.task].parity ^ lf.depth) & 1u;
+    const uint64_t m = lf.hi - lf.lo;
+    if (m <= 1) {
+      if (m == 1 && par == 1) { back.push_back(lf.lo); back.push_back(lf.hi); }
+      continue;
+    }
+    if (m > 65536) {
+      serial.push_back(lf);
+      if (par == 0) { back.push_back(lf.lo); back.push_back(lf.hi); }
+      continue;
+    }
+    lst[par].push_back(lf.lo);
+    lst[par].push_back(lf.hi);
+    mmax[par] = std::max(mmax[par], (uint32_t)m);
+    if (par == 0) { back.push_back(lf.lo); back.push_back(lf.hi); }  // the result lands in buf1
+  }
+  ArrayJob J0 = make_job(1, 1, 0, 0, 0);
+  ExplicitTask E0{};
+  for (int par = 0; par < 2; ++par) {
+    const uint64_t cnt = lst[par].size() / 2;
+    if (!cnt) continue;
+    uint64_t* dl = A.alloc<uint64_t>(lst[par].size(), st);
+    CK(cudaMemcpyAsync(dl, lst[par].data(), lst[par].size() * 8, cudaMemcpyHostToDevice, st));
+    const uint32_t grid = leaf_apply_grid(cnt, mmax[par], num_sms());
+    uint16_t* lscr = A.alloc<uint16_t>((uint64_t)grid * 2 * ((mmax[par] + 1) & ~1u) + 8, st);
+    launch_leaf_apply(eb, J0, E0, cnt, par ? buf1 : buf0, par ? buf0 : buf1, draws, lscr, mmax[par], grid, st, dl);
+  }
+  if (!serial.empty()) {
+    RsLeaf* dS = A.alloc<RsLeaf>(serial.size(), st);
+    CK(cudaMemcpyAsync(dS, serial.data(), serial.size() * sizeof(RsLeaf), cudaMemcpyHostToDevice, st));
+    launch_rs_leaf_serial(eb, dS, (uint32_t)serial.size(), dT, buf0, buf1, st);
+  }
+  if (!back.empty()) {
+    uint64_t* db = A.alloc<uint64_t>(back.size(), st);
+    CK(cudaMemcpyAsync(db, back.data(), back.size() * 8, cudaMemcpyHostToDevice, st));
+    launch_rs_copy_ranges(eb, db, (uint32_t)(back.size() / 2), buf1, buf0, st);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));  // host vectors above are the copies' sources
+  return bits;
+}
+
+// rs_shuffle_parallel (splitshuffle.py:92-133): big ranges level by level,
+// then the small tasks.  Returns ShuffleReport.bits.
+static uint64_t run_rs_parallel(int eb, void* data, uint64_t n, uint64_t cutoff, uint64_t seed, cudaStream_t st) {
+  setup_pool_once();
+  Arena A;
+  uint64_t bits = 0;
+  try {
+    void* scratch = A.alloc<unsigned char>(n * eb, st);
+    void* buf[2] = {data, scratch};
+    struct F { uint64_t lo, hi, depth; };
+    std::vector<F> frontier{{0, n, 0}};
+    std::vector<RsTask> tasks;
+    const uint64_t kSpawnMin = 1ull << 14;  // shufflers.py:32
+    while (!frontier.empty()) {
+      std::vector<RsRange> big;
+      uint64_t nch = 0, depth = frontier[0].depth;
+      for (const F& f : frontier) {
+        const uint64_t size = f.hi - f.lo;
+        const StreamDesc sd = fresh_stream(substream_seed(seed, f.depth * (n + 1) + f.lo));
+        if (size > kSpawnMin) {
+          big.push_back(RsRange{f.lo, f.hi, sd, nch});
+          nch += (size + 2047) / 2048;
+        } else {
+          tasks.push_back(RsTask{f.lo, f.hi, sd, (uint32_t)(f.depth & 1), (uint32_t)tasks.size()});
+        }
+      }
+      if (big.empty()) break;
+      const uint32_t nr = (uint32_t)big.size();
+      RsRange* dR = A.alloc<RsRange>(nr, st);
+      CK(cudaMemcpyAsync(dR, big.data(), nr * sizeof(RsRange), cudaMemcpyHostToDevice, st));
+      uint32_t* cz = A.alloc<uint32_t>(nch, st);
+      uint64_t* dnz = A.alloc<uint64_t>(nr, st);
+      launch_rs_level(eb, dR, nr, nch, cz, dnz, st);
+      const uint32_t par = (uint32_t)(depth & 1);
+      launch_rs_split(eb, dR, nr, nch, cz, dnz, buf[par], buf[par ^ 1], st);
+      std::vector<uint64_t> hnz(nr);
+      CK(cudaMemcpyAsync(hnz.data(), dnz, nr * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::vector<F> next;
+      for (uint32_t r = 0; r < nr; ++r) {
+        const uint64_t lo = big[r].lo, hi = big[r].hi, nz = hnz[r];
+        bits += hi - lo;
+        if (nz) next.push_back(F{lo, lo + nz, depth + 1});
+        if (hi - lo - nz) next.push_back(F{lo + nz, hi, depth + 1});
+      }
+      frontier.swap(next);
+    }
+    bits += run_rs_tasks(eb, buf[0], buf[1], tasks, 0, n, cutoff, A, st);
+  } catch (...) {
+    cudaStreamSynchronize(st);
+    A.release(st);
+    throw;
+  }
+  A.release(st);
+  return bits;
+}
+
+// rs_range_inplace (_kernels.py:449-457): the sequential splitting shuffle of
+// [lo, hi) from a mid-stream state.  Returns the bits consumed.
+static uint64_t run_rs_range(int eb, void* data, uint64_t lo, uint64_t hi, uint64_t cutoff, const StreamDesc& sd,
+                             cudaStream_t st) {
+  setup_pool_once();
+  Arena A;
+  uint64_t bits = 0;
+  try {
+    unsigned char* scratch = A.alloc<unsigned char>((hi - lo) * eb, st);
+    std::vector<RsTask> tasks{RsTask{lo, hi, sd, 0u, 0u}};
+    bits = run_rs_tasks(eb, data, (void*)(scratch - lo * eb), tasks, lo, hi, cutoff, A, st);
+  } catch (...) {
+    cudaStreamSynchronize(st);
+    A.release(st);
+    throw;
+  }
+  A.release(st);
+  return bits;
+}
+
 static void run_single_leaf(int eb, void* data, uint64_t lo, uint64_t hi, const StreamDesc& sd,
                             unsigned long long* d_bits, cudaStream_t st) {
   setup_pool_once();
@@ -850,6 +1034,30 @@ int sk_ipc_open(const void* handle, void** base_out) {
 int sk_ipc_close(void* base) {
   SK_TRY
   CK(cudaIpcCloseMemHandle(base));
+  SK_CATCH
+}
+
+int sk_rs_shuffle_parallel(void* data, int elem_bytes, uint64_t n, uint64_t cutoff, uint64_t seed, uint64_t* bits_out,
+                           void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (cutoff == 0) cutoff = 1ull << 12;  // RS_CUTOFF_DEFAULT (splitshuffle.py:27)
+  if (bits_out) *bits_out = 0;
+  if (n < 2) return SK_OK;
+  SK_TRY
+  const uint64_t bits = run_rs_parallel(elem_bytes, data, n, cutoff, seed, (cudaStream_t)stream);
+  if (bits_out) *bits_out = bits;
+  SK_CATCH
+}
+
+int sk_rs_range(void* data, int elem_bytes, uint64_t lo, uint64_t hi, uint64_t cutoff, uint64_t state_io[4],
+                void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (!state_io || hi < lo) { set_err("bad range or state"); return SK_EINVAL; }
+  if (state_io[2] > 63) { set_err("buffered_bits must be < 64"); return SK_EINVAL; }
+  if (cutoff == 0) cutoff = 1ull << 12;
+  SK_TRY
+  const uint64_t bits = run_rs_range(elem_bytes, data, lo, hi, cutoff, desc_from_state(state_io), (cudaStream_t)stream);
+  advance_state(state_io, bits);
   SK_CATCH
 }
 

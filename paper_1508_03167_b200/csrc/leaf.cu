@@ -182,11 +182,14 @@ __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
 // table is staged in global and reloaded into shared memory for the chase.
 constexpr uint32_t kLeafHalf = 32768;
 
+// list (optional): leaf g = [list[2g], list[2g+1]) instead of the schedule's
+// leaf g (the Rao-Sandelius leaves).
 template <typename V, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
                                                            const V* __restrict__ in, V* __restrict__ out,
                                                            const uint16_t* __restrict__ draws,
-                                                           uint16_t* __restrict__ scratch, uint32_t mmax) {
+                                                           uint16_t* __restrict__ scratch, uint32_t mmax,
+                                                           const uint64_t* __restrict__ list) {
   extern __shared__ uint32_t sh[];
   __shared__ uint32_t warp_tot[BLOCK / 32];
   const uint32_t half = mmax < kLeafHalf ? mmax : kLeafHalf;
@@ -200,7 +203,13 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
   constexpr uint32_t NW = BLOCK / 32;
 
   for (uint64_t g = blockIdx.x; g < nleaves; g += gridDim.x) {
-    const LeafDesc L = leaf_desc(J, E, g);
+    LeafDesc L;
+    if (list) {
+      L.lo = list[2 * g];
+      L.hi = list[2 * g + 1];
+    } else {
+      L = leaf_desc(J, E, g);
+    }
     const uint32_t m = (uint32_t)(L.hi - L.lo);
     const V* __restrict__ src_in = in + L.lo;
     V* __restrict__ dst = out + L.lo;
@@ -212,8 +221,16 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
     if (tid == 0) {  // pull this leaf's data and the next leaf's draws into L2
       if (g == blockIdx.x) l2_prefetch(dr, (size_t)m * 2);
       if (g + gridDim.x < nleaves) {
-        const LeafDesc Ln = leaf_desc(J, E, g + gridDim.x);
-        l2_prefetch(draws + Ln.lo, (size_t)(Ln.hi - Ln.lo) * 2);
+        uint64_t nlo, nhi;
+        if (list) {
+          nlo = list[2 * (g + gridDim.x)];
+          nhi = list[2 * (g + gridDim.x) + 1];
+        } else {
+          const LeafDesc Ln = leaf_desc(J, E, g + gridDim.x);
+          nlo = Ln.lo;
+          nhi = Ln.hi;
+        }
+        l2_prefetch(draws + nlo, (size_t)(nhi - nlo) * 2);
       }
     }
     for (uint32_t T0 = 0; T0 < m; T0 += kLeafHalf) {
@@ -364,16 +381,16 @@ static size_t leaf_apply_smem(uint32_t mmax) {
 template <typename V>
 static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, const void* in, void* out,
                          const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid,
-                         cudaStream_t st) {
+                         const uint64_t* list, cudaStream_t st) {
   size_t smem = leaf_apply_smem(mmax);
   if (mmax > 8192) {
     auto k = leaf_apply_kernel<V, 1024>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, 1024, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax);
+    k<<<grid, 1024, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
   } else {
     auto k = leaf_apply_kernel<V, 256>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, 256, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax);
+    k<<<grid, 256, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
   }
   count_launch();
 }
@@ -390,10 +407,11 @@ uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms) {
 }
 
 void launch_leaf_apply(int eb, const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, const void* in, void* out,
-                       const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid, cudaStream_t st) {
+                       const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid, cudaStream_t st,
+                       const uint64_t* list) {
   if (!nleaves) return;
-  if (eb == 4) leaf_apply_t<uint32_t>(J, E, nleaves, in, out, draws, scratch, mmax, grid, st);
-  else leaf_apply_t<unsigned long long>(J, E, nleaves, in, out, draws, scratch, mmax, grid, st);
+  if (eb == 4) leaf_apply_t<uint32_t>(J, E, nleaves, in, out, draws, scratch, mmax, grid, list, st);
+  else leaf_apply_t<unsigned long long>(J, E, nleaves, in, out, draws, scratch, mmax, grid, list, st);
 }
 
 void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, void* out,

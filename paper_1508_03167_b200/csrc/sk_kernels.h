@@ -14,7 +14,8 @@ void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nle
                           unsigned long long* bits, cudaStream_t st);
 uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms);
 void launch_leaf_apply(int eb, const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, const void* in, void* out,
-                       const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid, cudaStream_t st);
+                       const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid, cudaStream_t st,
+                       const uint64_t* list = nullptr);
 void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, void* out,
                         unsigned long long* bits, cudaStream_t st);
 
@@ -68,6 +69,34 @@ void launch_tail_apply_peer(int eb, const PeerSpan& ps, const uint64_t* dst, con
                             uint64_t nslots, cudaStream_t st);
 void launch_tail_apply(int eb, void* buf, const uint64_t* dst, const uint64_t* src, void* tmp, uint64_t nslots,
                        cudaStream_t st);
+
+// rs.cu (Rao-Sandelius, §8 row F2)
+struct RsRange {              // a big range of one frontier level
+  uint64_t lo, hi;
+  StreamDesc sd;              // its substream (flip i <-> element lo + i)
+  uint64_t chunk0;            // its first 2048-position chunk in the level's chunk list
+};
+struct RsTask {               // a small task: the sequential splitting shuffle of [lo, hi)
+  uint64_t lo, hi;
+  StreamDesc sd;
+  uint32_t parity;            // its data is in buf[parity] (0: the caller's buffer)
+  uint32_t array;
+};
+struct RsNode { uint64_t lo, hi, off; uint32_t task, level; };   // a split of a task at stream offset off
+struct RsLeaf { uint64_t lo, hi, off; uint32_t task, depth; };   // a Fisher-Yates leaf of a task
+void launch_rs_level(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, uint32_t* cz, uint64_t* nz,
+                     cudaStream_t st);
+void launch_rs_split(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, const uint32_t* czp,
+                     const uint64_t* nz, const void* in, void* out, cudaStream_t st);
+void launch_rs_plan(const RsTask* T, uint32_t ntasks, uint64_t cutoff, uint16_t* draws, RsNode* nodes,
+                    unsigned long long* counts, uint64_t node_cap, RsLeaf* leaves, uint64_t leaf_cap,
+                    unsigned long long* bits, cudaStream_t st);
+void launch_rs_nodes(int eb, const RsNode* nodes, uint32_t count, const RsTask* T, void* buf0, void* buf1,
+                     cudaStream_t st);
+void launch_rs_leaf_serial(int eb, const RsLeaf* L, uint32_t count, const RsTask* T, void* buf0, void* buf1,
+                           cudaStream_t st);
+void launch_rs_copy_ranges(int eb, const uint64_t* list, uint32_t count, const void* from, void* to,
+                           cudaStream_t st);
 
 // misc.cu
 void launch_chi(int algo, int n, uint64_t trials, uint64_t seed, uint64_t cutoff, unsigned long long* counts,

@@ -7,8 +7,8 @@ Run in the build container only (the reference is not on the GPU box):
 
 Writes tests/golden/cli.json: for each command line, the reference's exit
 code, stdout and stderr (wall-clock columns of `bench` are blanked).  The
-commands only use algorithms the B200 backend serves (fy, merge; chisq for
-fy / merge / merge_parallel).
+commands only use algorithms the B200 backend serves (fy, merge, rs; chisq
+for fy / merge / merge_parallel).
 """
 from __future__ import annotations
 
@@ -32,6 +32,10 @@ CASES = [
               "--threads", "2"]},
     {"argv": ["bench", "--algos", "merge", "--sizes", "0,1,2,5000", "--trials", "3", "--seed", "2",
               "--threads", "8", "--cutoff", "64"]},
+    {"argv": ["shuffle", "--algo", "rs", "--n", "40000", "--seed", "21", "--threads", "4", "--report"]},
+    {"argv": ["shuffle", "--algo", "rs", "--n", "500", "--seed", "22", "--cutoff", "8", "--report"]},
+    {"argv": ["bench", "--algos", "rs,merge", "--sizes", "1000,50000", "--trials", "3", "--seed", "5",
+              "--threads", "2"]},
     {"argv": ["verify", "--mode", "chisq", "--algo", "merge_parallel", "--n", "5", "--trials", "20000", "--seed",
               "2", "--cutoff", "1"]},
     {"argv": ["verify", "--mode", "chisq", "--algo", "fy", "--n", "4", "--trials", "5000", "--seed", "3"]},
