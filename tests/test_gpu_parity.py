@@ -290,3 +290,16 @@ def test_merge_fallback_paths(mode):
             assert np.array_equal(x.cpu().numpy().astype(np.int64), a)
     finally:
         lib.sk_debug_set(key, off)
+
+
+@pytest.mark.parametrize("n,cutoff,seed,dt", [((1 << 25) + 17, 65536, 3, np.uint32), (1 << 24, 4096, 4, np.int64),
+                                              (50_000_001, 65536, 5, np.float32)])
+def test_host_entry_pipelined(n, cutoff, seed, dt):
+    # numpy arrays go through the C-ABI host entry, which pipelines the H2D
+    # copy with the leaf stage and the chunk-local rounds for n >= 2^24
+    idx, bits = O.merge_shuffle_perm(n, cutoff, seed, threads=8)
+    payload = (np.arange(n, dtype=np.int64) * 7 + 3).astype(dt)
+    a = payload.copy()
+    rep = sk.merge_shuffle_parallel(a, sk.ShuffleConfig(cutoff=cutoff), sk.BitSource(seed))
+    assert rep.bits == bits
+    assert np.array_equal(a, payload[idx])
