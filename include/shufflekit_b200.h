@@ -107,6 +107,15 @@ int sk_merge_range_peers(void *const *part_bases, const uint64_t *part_starts, i
                          uint64_t n1, uint64_t n2, const uint64_t state[4], int phase, uint64_t *bits_out,
                          void *stream);
 
+/* Single-process multi-GPU merge_shuffle_parallel: shards[r] (device pointer on
+ * devices[r]) holds elements [(n*r*q/G)>>c, (n*(r+1)*q/G)>>c) of the array,
+ * G = ngpu (a power of two <= 8 and <= q = 2^c).  Leaves and local rounds run
+ * per shard (a host thread per device), the spanning rounds as the fused
+ * peer-memory merge (peer access is enabled between the devices).  Devices may
+ * repeat.  *bits_out = ShuffleReport.bits.  Synchronizes. */
+int sk_merge_shuffle_multi(void *const *shards, const int *devices, int ngpu, int elem_bytes, uint64_t n,
+                           uint64_t cutoff, uint64_t seed, uint64_t *bits_out);
+
 /* CUDA IPC plumbing for sk_merge_range_peers: the 64-byte handle and byte
  * offset of the allocation holding `ptr`; map a peer's allocation (returns its
  * base; add the offset); unmap. */

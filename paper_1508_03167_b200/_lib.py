@@ -27,6 +27,8 @@ SIGNATURES = {
     "sk_rs_range": (_int, [_vp, _int, _u64, _u64, _u64, _u64p, _vp]),
     "sk_merge_range_peers": (_int, [ctypes.POINTER(_vp), _u64p, _int, _int, _int, _u64, _u64, _u64p, _int, _u64p,
                                     _vp]),
+    "sk_merge_shuffle_multi": (_int, [ctypes.POINTER(_vp), ctypes.POINTER(_int), _int, _int, _u64, _u64, _u64,
+                                      _u64p]),
     "sk_ipc_get_handle": (_int, [_vp, _vp, _u64p]),
     "sk_ipc_open": (_int, [_vp, ctypes.POINTER(_vp)]),
     "sk_ipc_close": (_int, [_vp]),

@@ -12,9 +12,11 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -85,17 +87,21 @@ struct StageTimer {
 };
 
 // ------------------------------------------------------------ device memory
+// Keep freed stream-ordered memory in the current device's pool (repeated
+// calls reuse it instead of returning it to the driver); once per device.
 static void setup_pool_once() {
-  static std::once_flag f;
-  std::call_once(f, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ULL;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
+  static std::mutex mu;
+  static uint64_t done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && (done >> dev & 1)) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (dev < 64) done |= 1ull << dev;
 }
 
 // All allocations of one call; freed stream-ordered on the data stream.
@@ -839,6 +845,139 @@ int sk_merge_shuffle_parallel_host(void* host_data, int elem_bytes, uint64_t n, 
   if (rc) return rc;
   if (bits_out) *bits_out = bits;
   SK_CATCH
+}
+
+// Single-process multi-GPU merge_shuffle_parallel (SURVEY.md §8 b/e): shard r
+// (elements [(n*r*q/G)>>c, (n*(r+1)*q/G)>>c)) lives on devices[r]; a host
+// thread per shard runs its leaves and local rounds, then every spanning round
+// runs as the fused peer-memory merge (phase 1 on every part's device in
+// parallel, phase 2 once per pair).  Devices may repeat.
+int sk_merge_shuffle_multi(void* const* shards, const int* devices, int ngpu, int elem_bytes, uint64_t n,
+                           uint64_t cutoff, uint64_t seed, uint64_t* bits_out) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (!shards || !devices || ngpu < 1 || ngpu > 8 || (ngpu & (ngpu - 1))) {
+    set_err("multi: 1..8 shards, a power of two");
+    return SK_EINVAL;
+  }
+  if (cutoff == 0) cutoff = 65536;
+  const int c = plan_c(n, cutoff);
+  const uint64_t q = 1ull << c;
+  int lg = 0;
+  while ((1 << lg) < ngpu) ++lg;
+  if ((uint64_t)ngpu > q) {
+    set_err("multi: more shards than leaf blocks (lower the cutoff)");
+    return SK_EINVAL;
+  }
+  const uint64_t nblk = q >> lg;
+  const int local = c - lg;
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  // peer access between distinct devices
+  for (int a = 0; a < ngpu; ++a)
+    for (int b = 0; b < ngpu; ++b) {
+      if (devices[a] == devices[b]) continue;
+      cudaSetDevice(devices[a]);
+      cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        cudaSetDevice(cur_dev);
+        set_err(std::string("peer access: ") + cudaGetErrorString(e));
+        return SK_ECUDA;
+      }
+      cudaGetLastError();
+    }
+  cudaSetDevice(cur_dev);
+  std::vector<std::string> errs;
+  std::mutex emu;
+  auto run_all = [&](int count, const std::function<int(int)>& fn) {
+    std::vector<std::thread> th;
+    for (int w = 0; w < count; ++w)
+      th.emplace_back([&, w] {
+        if (fn(w) != SK_OK) {
+          std::lock_guard<std::mutex> lk(emu);
+          errs.push_back(sk_last_error());
+        }
+      });
+    for (auto& t : th) t.join();
+    return errs.empty();
+  };
+  auto on_device = [&](int dev, const std::function<int(cudaStream_t)>& fn) -> int {
+    cudaSetDevice(dev);
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+      set_err("stream creation failed");
+      return SK_ECUDA;
+    }
+    int rc = fn(s);
+    if (rc == SK_OK && cudaStreamSynchronize(s) != cudaSuccess) {
+      set_err("stream synchronize failed");
+      rc = SK_ECUDA;
+    }
+    cudaStreamDestroy(s);
+    return rc;
+  };
+  std::vector<uint64_t> b(ngpu, 0);
+  std::mutex bmu;
+  uint64_t total = 0;
+  bool ok = run_all(ngpu, [&](int r) {
+    return on_device(devices[r], [&](cudaStream_t s) {
+      return sk_merge_shuffle_shard(shards[r], elem_bytes, n, cutoff, seed, r * nblk, nblk, local, &b[r], s);
+    });
+  });
+  for (int r = 0; r < ngpu; ++r) total += b[r];
+  auto bound = [&](uint64_t i) { return bound_at(n, i, c); };
+  for (int rr = local + 1; ok && rr <= c; ++rr) {
+    const int span = 1 << (rr - local);
+    const int groups = ngpu / span;
+    const uint64_t p = 1ull << (rr - 1);
+    auto pair_args = [&](int gi, std::vector<void*>& bases, std::vector<uint64_t>& starts, uint64_t& n1,
+                         uint64_t& n2, uint64_t st[4]) {
+      const int g0 = gi * span;
+      const uint64_t i = (uint64_t)g0 * nblk;
+      const uint64_t j = bound(i), k = bound(i + p), l = bound(i + 2 * p);
+      bases.resize(span);
+      starts.resize(span + 1);
+      for (int m = 0; m < span; ++m) {
+        bases[m] = shards[g0 + m];
+        starts[m] = bound((uint64_t)(g0 + m) * nblk) - j;
+      }
+      starts[span] = l - j;
+      n1 = k - j;
+      n2 = l - k;
+      st[0] = substream_seed(seed, (uint64_t)rr * q + i);
+      st[1] = st[2] = st[3] = 0;
+    };
+    ok = run_all(ngpu, [&](int w) {  // phase 1: every part of every spanning pair
+      const int gi = w / span, m = w % span;
+      std::vector<void*> bases;
+      std::vector<uint64_t> starts;
+      uint64_t n1, n2, st[4];
+      pair_args(gi, bases, starts, n1, n2, st);
+      return on_device(devices[w], [&](cudaStream_t s) {
+        return sk_merge_range_peers(bases.data(), starts.data(), span, m, elem_bytes, n1, n2, st, 1, nullptr, s);
+      });
+    });
+    if (!ok) break;
+    ok = run_all(groups, [&](int gi) {  // phase 2: the tail, once per pair
+      std::vector<void*> bases;
+      std::vector<uint64_t> starts;
+      uint64_t n1, n2, st[4], pb = 0;
+      pair_args(gi, bases, starts, n1, n2, st);
+      const int rc = on_device(devices[gi * span], [&](cudaStream_t s) {
+        return sk_merge_range_peers(bases.data(), starts.data(), span, 0, elem_bytes, n1, n2, st, 2, &pb, s);
+      });
+      std::lock_guard<std::mutex> lk(bmu);
+      total += pb;
+      return rc;
+    });
+  }
+  cudaSetDevice(cur_dev);
+  if (!ok) {
+    set_err(errs.empty() ? std::string("multi: failed") : errs[0]);
+    return SK_ECUDA;
+  }
+  if (bits_out) *bits_out = total;
+  return SK_OK;
 }
 
 int sk_merge_shuffle_shard(void* data, int elem_bytes, uint64_t n_total, uint64_t cutoff, uint64_t seed,

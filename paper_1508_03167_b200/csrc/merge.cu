@@ -1009,12 +1009,8 @@ static void merge_tree_peer_t(const PeerSpan& ps, const PairPlan* plans, const u
   }
   P.start[ps.n] = ps.start[ps.n];
   P.tma = tma ? 1 : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(merge_tree_peer_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TreeCfg<V>::SMEM);
-    attr = true;
-  }
+  // (per device: function attributes belong to the current device's context)
+  cudaFuncSetAttribute(merge_tree_peer_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TreeCfg<V>::SMEM);
   const uint32_t nparts = (uint32_t)ps.n;
   const uint32_t grid = (tpp + nparts - 1 - part) / nparts;
   if (!grid) return;
@@ -1032,11 +1028,7 @@ template <typename V>
 static void merge_tree_t(void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
                          const uint64_t* chains, uint32_t tpp, cudaStream_t st) {
   const size_t smem = TreeCfg<V>::SMEM;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(merge_tree_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  cudaFuncSetAttribute(merge_tree_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   merge_tree_kernel<V><<<(unsigned)(npairs * tpp), kTreeBlock, smem, st>>>((const V*)in, (V*)out, plans, rank,
                                                                              chains, tpp);
   count_launch();

@@ -236,6 +236,26 @@ def _spanning_rounds_allgather(shard, seed, engine, c, q, bounds, nblk, local_ro
     return bits
 
 
+def merge_shuffle_multi(shards: List[torch.Tensor], n: int, cutoff: Optional[int], seed: int) -> int:
+    """Single-process multi-GPU form (sk_merge_shuffle_multi): shards[r] is a
+    CUDA tensor (any device) holding shard_range(n, cutoff, len(shards), r);
+    returns ShuffleReport.bits.  The devices may repeat (e.g. all cuda:0)."""
+    cutoff = MERGE_CUTOFF_DEFAULT if cutoff is None else cutoff
+    G = len(shards)
+    for r, t in enumerate(shards):
+        lo, hi = shard_range(n, cutoff, G, r)
+        if not t.is_cuda or not t.is_contiguous() or t.numel() != hi - lo:
+            raise ValueError(f"shard {r} must be a contiguous CUDA tensor of {hi - lo} elements")
+    eb = shards[0].element_size()
+    torch.cuda.synchronize()
+    ptrs = (ctypes.c_void_p * G)(*[t.data_ptr() for t in shards])
+    devs = (ctypes.c_int * G)(*[t.device.index for t in shards])
+    bits = ctypes.c_uint64(0)
+    _lib.check(_lib.load().sk_merge_shuffle_multi(ptrs, devs, G, eb, n, cutoff, seed & ((1 << 64) - 1),
+                                                  ctypes.byref(bits)))
+    return int(bits.value)
+
+
 def simulate_sharded(data: torch.Tensor, n: int, cutoff: Optional[int], seed: int, world: int,
                      engine=None, exchange: str = "allgather") -> int:
     """The sharded schedule of merge_shuffle_sharded executed by ONE process

@@ -303,3 +303,21 @@ def test_host_entry_pipelined(n, cutoff, seed, dt):
     rep = sk.merge_shuffle_parallel(a, sk.ShuffleConfig(cutoff=cutoff), sk.BitSource(seed))
     assert rep.bits == bits
     assert np.array_equal(a, payload[idx])
+
+
+@pytest.mark.parametrize("world,n,dt", [(2, (1 << 20) + 12345, torch.int32), (4, 1 << 21, torch.int64),
+                                        (8, 3_000_001, torch.int32)])
+def test_merge_shuffle_multi_single_process(world, n, dt):
+    # the single-process multi-GPU entry (sk_merge_shuffle_multi), shards as
+    # separate buffers (all on this device): host thread per shard, fused
+    # peer-memory merge for the spanning rounds
+    from paper_1508_03167_b200 import distributed as D
+    cutoff, seed = 32768, 29
+    shards = []
+    for r in range(world):
+        lo, hi = D.shard_range(n, cutoff, world, r)
+        shards.append(torch.arange(lo, hi, dtype=dt, device="cuda"))
+    bits = D.merge_shuffle_multi(shards, n, cutoff, seed)
+    ref, rbits = O.merge_shuffle_perm(n, cutoff, seed)
+    assert bits == rbits
+    assert np.array_equal(torch.cat(shards).cpu().numpy().astype(np.int64), ref)
