@@ -212,11 +212,27 @@ def main():
     sp = ctypes.c_void_p(stream.cuda_stream)
     bits = ctypes.c_uint64(0)
 
+    # N > 1: contiguous shards of one n_total array; the spanning rounds run as
+    # the fused peer-memory merge (CUDA IPC over NVLink).  If the peer mapping
+    # fails on this box, every rank falls back to the NCCL all-gather exchange.
+    exchange = os.environ.get("SK_EXCHANGE", "peer")
+    if world > 1 and exchange == "peer":
+        ok = torch.tensor([1], device="cuda")
+        try:
+            D.merge_shuffle_sharded(x, n_total, 65536, 0, exchange="peer")
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] peer exchange unavailable on rank {rank}: {exc}", file=sys.stderr)
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            exchange = "allgather"
+        x.copy_(torch.randint(-2 ** 31, 2 ** 31 - 1, (n,), dtype=torch.int32, device="cuda", generator=g))
+
     def step():
         if world == 1:
             _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), 4, n, 65536, 0, None, sp))
-        else:  # contiguous shards of one n_total array; spanning rounds exchange over NCCL
-            D.merge_shuffle_sharded(x, n_total, 65536, 0)
+        else:
+            D.merge_shuffle_sharded(x, n_total, 65536, 0, exchange=exchange)
 
     for _ in range(args.warmup):
         step()
@@ -226,7 +242,7 @@ def main():
         _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), 4, n, 65536, 0, ctypes.byref(bits),
                                                  sp))
     else:
-        bits.value = D.merge_shuffle_sharded(x, n_total, 65536, 0)
+        bits.value = D.merge_shuffle_sharded(x, n_total, 65536, 0, exchange=exchange)
 
     lib.sk_profile_enable(1)
     l0 = lib.sk_launch_count()
@@ -293,7 +309,7 @@ def main():
                 _lib.check(lib.sk_merge_shuffle_parallel_host(hp, 4, n, 65536, 0, ctypes.byref(bits), sp))
             else:
                 x.copy_(host, non_blocking=True)
-                bits.value = D.merge_shuffle_sharded(x, n_total, 65536, 0)
+                bits.value = D.merge_shuffle_sharded(x, n_total, 65536, 0, exchange=exchange)
                 host.copy_(x, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
 
@@ -328,7 +344,8 @@ def main():
                            "n_per_gpu": n, "elem_bytes": 4, "cutoff": 65536, "seed": 0,
                            "n_total": n_total,
                            "parallelism": (f"{world} contiguous shards; top {world.bit_length() - 1} rounds "
-                                           "exchange over NCCL all-gather") if world > 1 else "1 GPU",
+                                           + ("fused peer-memory merge over NVLink (CUDA IPC)" if exchange == "peer"
+                                              else "exchange over NCCL all-gather")) if world > 1 else "1 GPU",
                            "l2": f"input {4 * n >> 20} MiB per GPU >> 126 MB L2; no flush needed",
                            "bits_per_shuffle": int(bits.value)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

@@ -185,7 +185,18 @@ def _spanning_rounds_peer(shard, n, seed, engine, c, q, bounds, nblk, local_roun
     h = torch.tensor(list(engine.peer_handle(shard)), dtype=torch.uint8, device=shard.device)
     hs = [torch.empty_like(h) for _ in range(world)]
     dist.all_gather(hs, h)
-    ptr = [shard.data_ptr() if r == rank else engine.open_peer(bytes(hs[r].cpu().tolist())) for r in range(world)]
+    ok = torch.ones(1, dtype=torch.int32, device=shard.device)
+    ptr = [0] * world
+    err = None
+    try:
+        for r in range(world):
+            ptr[r] = shard.data_ptr() if r == rank else engine.open_peer(bytes(hs[r].cpu().tolist()))
+    except Exception as exc:  # noqa: BLE001 - every rank must learn about it before any barrier
+        ok.zero_()
+        err = exc
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if int(ok.item()) == 0:
+        raise RuntimeError(f"peer mapping unavailable on at least one rank ({err})")
     eb = shard.element_size()
     bits = 0
     try:
