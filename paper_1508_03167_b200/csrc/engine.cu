@@ -356,16 +356,20 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
       StageTimer tm(0, st);
       if (fast_leaf) launch_leaf_decode16(J, E0, nleaves, draws, d_bits, st);
     }
-    void* cur;
+    void* cur = nullptr;
     {
       StageTimer tm(1, st);
-      if (fast_leaf) {
+      if (fast_leaf && lv.empty() && mmax <= 8192) {
+        // no merge rounds and small leaves: staged in shared memory, in place
+        launch_leaf_apply(eb, J, E0, nleaves, data, data, draws, lscr, (uint32_t)mmax, grid, st);
+        cur = data;
+      } else if (fast_leaf) {
         launch_leaf_apply(eb, J, E0, nleaves, data, scratch, draws, lscr, (uint32_t)mmax, grid, st);
       } else {
         CK(cudaMemcpyAsync(scratch, data, ntot * eb, cudaMemcpyDeviceToDevice, st));
         launch_leaf_serial(eb, J, E0, nleaves, scratch, d_bits, st);
       }
-      cur = scratch;
+      if (cur != data) cur = scratch;
     }
     CK(cudaGetLastError());
     // plans run on the side stream while the leaf stage runs

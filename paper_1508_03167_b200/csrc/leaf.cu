@@ -186,7 +186,7 @@ constexpr uint32_t kLeafHalf = 32768;
 // leaf g (the Rao-Sandelius leaves).
 template <typename V, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
-                                                           const V* __restrict__ in, V* __restrict__ out,
+                                                           const V* in, V* out,
                                                            const uint16_t* __restrict__ draws,
                                                            uint16_t* __restrict__ scratch, uint32_t mmax,
                                                            const uint64_t* __restrict__ list) {
@@ -197,6 +197,8 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
   uint16_t* cur = reinterpret_cast<uint16_t*>(sh);               // [half]
   uint16_t* bkt = reinterpret_cast<uint16_t*>(sh + cw);          // [mmax] buckets; later H
   const uint32_t ms = (mmax + 1) & ~1u;
+  constexpr bool kStage = BLOCK == 256;
+  V* sdata = reinterpret_cast<V*>(sh + ((cw + ((mmax + 1) >> 1) + 1) & ~1u));  // after the buckets, 8-byte aligned
   uint16_t* Nn = scratch + (uint64_t)blockIdx.x * 2 * ms;
   uint16_t* Hg = Nn + ms;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -211,11 +213,16 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
       L = leaf_desc(J, E, g);
     }
     const uint32_t m = (uint32_t)(L.hi - L.lo);
-    const V* __restrict__ src_in = in + L.lo;
-    V* __restrict__ dst = out + L.lo;
+    const V* src_in = in + L.lo;
+    V* dst = out + L.lo;
     if (m < 2) {
       if (m == 1 && tid == 0) dst[0] = src_in[0];
       continue;
+    }
+    // small leaves (BLOCK 256 configuration): the data is staged in shared
+    // memory, gathered from there, and may be written back in place
+    if (kStage) {
+      for (uint32_t k = tid; k < m; k += BLOCK) sdata[k] = src_in[k];
     }
     const uint16_t* __restrict__ dr = draws + L.lo;
     if (tid == 0) {  // pull this leaf's data and the next leaf's draws into L2
@@ -325,7 +332,7 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
           while ((h = Hs[y]) != 0) y = h;
           src = y;
         }
-        if (i < m) v[k] = src_in[src];
+        if (i < m) v[k] = kStage ? sdata[src] : src_in[src];
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -373,16 +380,18 @@ void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nle
   count_launch();
 }
 
-static size_t leaf_apply_smem(uint32_t mmax) {
+static size_t leaf_apply_smem(uint32_t mmax, int eb = 0) {
   const uint32_t half = mmax < kLeafHalf ? mmax : kLeafHalf;
-  return (size_t)((half + 1) / 2) * 4 + (size_t)((mmax + 1) / 2) * 4;
+  const size_t words = (size_t)((half + 1) / 2) + (size_t)((mmax + 1) / 2);
+  if (mmax <= 8192) return ((words + 1) & ~(size_t)1) * 4 + (size_t)mmax * (eb ? eb : 8);  // + staged data
+  return words * 4;
 }
 
 template <typename V>
 static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, const void* in, void* out,
                          const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid,
                          const uint64_t* list, cudaStream_t st) {
-  size_t smem = leaf_apply_smem(mmax);
+  size_t smem = leaf_apply_smem(mmax, (int)sizeof(V));
   if (mmax > 8192) {
     auto k = leaf_apply_kernel<V, 1024>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
