@@ -1,0 +1,71 @@
+"""Edge cases on the GPU against the oracle: sizes around powers of two,
+extreme cutoffs (leaves above 65536 take the serial leaf path), odd batch
+shapes, long single-stream Fisher-Yates, and the splitting shuffle with a
+huge cutoff."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1508_03167_b200 as sk  # noqa: E402
+from paper_1508_03167_b200 import splitshuffle as S  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def run(n, cutoff, seed, dt):
+    x = torch.arange(n, dtype=dt, device="cuda")
+    rep = sk.merge_shuffle_parallel(x, sk.ShuffleConfig(cutoff=cutoff), sk.BitSource(seed))
+    ref, bits = O.merge_shuffle_perm(n, cutoff if cutoff else 65536, seed)
+    assert rep.bits == bits
+    assert np.array_equal(x.cpu().numpy().astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("k", [16, 17, 20])
+@pytest.mark.parametrize("d", [-1, 0, 1])
+@pytest.mark.parametrize("dt", [torch.int32, torch.int64])
+def test_sizes_around_powers_of_two(k, d, dt):
+    run((1 << k) + d, None, 1000 + k + d, dt)
+
+
+@pytest.mark.parametrize("cutoff", [2, 3, 5, 65535, 65537, 100_000, 1 << 20])
+def test_extreme_cutoffs(cutoff):
+    run(300_001, cutoff, cutoff, torch.int32)
+
+
+def test_batched_odd_shapes():
+    for B, L, cutoff in [(3, 100_003, 1000), (7, 65_537, None), (1000, 1, None), (5, 2, 1)]:
+        x = torch.arange(L, dtype=torch.int64, device="cuda").repeat(B, 1).contiguous()
+        bits = sk.batched_shuffle(x, sk.ShuffleConfig(cutoff=cutoff), 77)
+        ref, rbits = O.batched(B, L, cutoff if cutoff else 65536, 77)
+        assert np.array_equal(bits.astype(np.int64), rbits.astype(np.int64))
+        assert np.array_equal(x.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("m", [65_535, 65_536, 65_537, 300_000])
+def test_long_fisher_yates(m):
+    x = torch.arange(m, dtype=torch.int32, device="cuda")
+    src = sk.BitSource(5)
+    src.take(13)
+    st = np.array(src.state_tuple(), dtype=np.uint64)
+    sk.fisher_yates(x, src)
+    a = np.arange(m, dtype=np.int64)
+    O.fy_range(a, 0, m, st)
+    assert np.array_equal(x.cpu().numpy(), a)
+    assert list(src.state_tuple()) == [int(v) for v in st]
+
+
+def test_rs_sequential_huge_cutoff():
+    # leaves above 65536 elements take the serial leaf kernel
+    n = 200_000
+    x = torch.arange(n, dtype=torch.int64, device="cuda")
+    src = sk.BitSource(9)
+    S.rs_shuffle(x, sk.ShuffleConfig(cutoff=150_000), src)
+    a = np.arange(n, dtype=np.int64)
+    st = O.state_vec(9, 0, 0, 0)
+    O.rs_range(a, 0, n, 150_000, st)
+    assert np.array_equal(x.cpu().numpy(), a)
+    assert list(src.state_tuple()) == [int(v) for v in st]
