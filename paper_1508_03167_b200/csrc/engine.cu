@@ -397,6 +397,88 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
   A.release(st);
 }
 
+static cudaStream_t copy_stream() {
+  static thread_local SideStream cs;
+  return cs.s;
+}
+
+// The host entry for big arrays: the H2D copy runs in 2^k chunks on a copy
+// stream; the leaf draws (no data needed) and the merge plans are prepared
+// meanwhile, and chunk j's leaves are applied as soon as chunk j has landed,
+// so the leaf stage hides under the transfer.  Then the merge rounds, then
+// the D2H copy.  Same result as copy + sk_merge_shuffle_parallel + copy.
+static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned long long* d_bits, cudaStream_t st) {
+  const uint64_t n = J.len;
+  const int c = J.c;
+  setup_pool_once();
+  Arena A;
+  cudaStream_t ps = side_stream(), cs = copy_stream();
+  std::vector<LevelBufs> lv = make_levels(J, eb);
+  unsigned char* dev = A.alloc<unsigned char>(n * eb, st);
+  unsigned char* scr = A.alloc<unsigned char>(n * eb, st);
+  uint16_t* draws = A.alloc<uint16_t>(n, st);
+  const uint64_t nleaves = J.q, K = 1ull << k, B = nleaves >> k;
+  const uint32_t mmax = (uint32_t)((n + J.q - 1) >> c);
+  const uint32_t grid = leaf_apply_grid(B, mmax, num_sms());
+  uint16_t* lscr = A.alloc<uint16_t>((uint64_t)grid * 2 * ((mmax + 1) & ~1u) + 8, st);
+  std::vector<cudaEvent_t> ev(K + 1, nullptr);
+  ExplicitTask E0{};
+  try {
+    fork_side(st, ps);
+    fork_side(st, cs);
+    for (uint64_t j = 0; j < K; ++j) {
+      const uint64_t lo = bound_at(n, j * B, c), hi = bound_at(n, (j + 1) * B, c);
+      CK(cudaMemcpyAsync(dev + lo * eb, (unsigned char*)host + lo * eb, (hi - lo) * eb, cudaMemcpyHostToDevice, cs));
+      CK(cudaEventCreateWithFlags(&ev[j], cudaEventDisableTiming));
+      CK(cudaEventRecord(ev[j], cs));
+    }
+    {
+      StageTimer tm(0, st);
+      launch_leaf_decode16(J, E0, nleaves, draws, d_bits, st);  // needs no data
+    }
+    for (uint64_t j = 0; j < K; ++j) {
+      const uint64_t lo = bound_at(n, j * B, c);
+      CK(cudaStreamWaitEvent(st, ev[j], 0));
+      ArrayJob Jj = J;
+      Jj.blk0 = j * B;
+      Jj.lognblk = c - k;
+      Jj.elem0 = lo;
+      StageTimer tm(1, st);
+      launch_leaf_apply(eb, Jj, E0, B, dev + lo * eb, scr + lo * eb, draws + lo, lscr, mmax, grid, st);
+    }
+    build_plans(lv, eb, d_bits, A, ps, st);
+    void* res = run_rounds(lv, eb, scr, dev, st);
+    if (res != dev) CK(cudaMemcpyAsync(dev, res, n * eb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaEventCreateWithFlags(&ev[K], cudaEventDisableTiming));
+    CK(cudaEventRecord(ev[K], st));
+    CK(cudaStreamWaitEvent(cs, ev[K], 0));
+    CK(cudaMemcpyAsync(host, dev, n * eb, cudaMemcpyDeviceToHost, cs));
+    CK(cudaEventRecord(ev[K], cs));
+    CK(cudaStreamWaitEvent(st, ev[K], 0));
+    CK(cudaGetLastError());
+  } catch (...) {
+    cudaStreamSynchronize(ps);
+    cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(st);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& L : lv)
+      if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+    A.release(st);
+    throw;
+  }
+  cudaEvent_t done;
+  CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  CK(cudaEventRecord(done, ps));
+  CK(cudaStreamWaitEvent(st, done, 0));
+  cudaEventDestroy(done);
+  for (auto e : ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& L : lv)
+    if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+  A.release(st);
+}
+
 // ---------------------------------------------------- bit-source state maths
 // State after consuming T more bits (SURVEY A2 closed form of bitstream.py:152-176).
 static void advance_state(uint64_t s[4], uint64_t T) {
@@ -836,6 +918,27 @@ int sk_merge_shuffle_parallel_host(void* host_data, int elem_bytes, uint64_t n, 
   SK_TRY
   cudaStream_t st = (cudaStream_t)stream;
   setup_pool_once();
+  {
+    const uint64_t cut = cutoff ? cutoff : 65536;
+    const int c = plan_c(n, cut);
+    if (n >= (1ull << 24) && c >= 3 && ((n + (1ull << c) - 1) >> c) <= 65536 && merge_tree_active()) {
+      unsigned long long* d_bits;
+      CK(cudaMallocAsync((void**)&d_bits, 8, st));
+      CK(cudaMemsetAsync(d_bits, 0, 8, st));
+      uint64_t bits = 0;
+      try {
+        run_job_host(elem_bytes, host_data, make_job(1, n, c, 0, seed), 3, d_bits, st);
+        fetch_bits(d_bits, &bits, 1, st);
+      } catch (...) {
+        cudaFreeAsync(d_bits, st);
+        throw;
+      }
+      CK(cudaFreeAsync(d_bits, st));
+      CK(cudaStreamSynchronize(st));
+      if (bits_out) *bits_out = bits;
+      return SK_OK;
+    }
+  }
   void* d = nullptr;
   CK(cudaMallocAsync(&d, n ? n * elem_bytes : 1, st));
   CK(cudaMemcpyAsync(d, host_data, n * elem_bytes, cudaMemcpyHostToDevice, st));
