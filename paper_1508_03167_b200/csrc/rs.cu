@@ -33,7 +33,7 @@ __device__ __forceinline__ uint32_t rs_range_of_chunk(const RsRange* R, uint32_t
 }
 
 // zeros among the chunk's coin flips (one word per lane of warp 0)
-__global__ void rs_chunk_zeros_kernel(const RsRange* __restrict__ R, uint32_t nr, uint32_t* __restrict__ cz) {
+__global__ void rs_chunk_zeros_kernel(const RsRange* __restrict__ R, uint32_t nr, uint64_t* __restrict__ cz) {
   const uint64_t c = blockIdx.x;
   const uint32_t r = rs_range_of_chunk(R, nr, c);
   const RsRange rg = R[r];
@@ -54,7 +54,7 @@ __global__ void rs_chunk_zeros_kernel(const RsRange* __restrict__ R, uint32_t nr
 }
 
 // per range: exclusive scan of its chunks' zero counts, and the range's total
-__global__ void rs_range_scan_kernel(const RsRange* __restrict__ R, uint32_t* __restrict__ cz,
+__global__ void rs_range_scan_kernel(const RsRange* __restrict__ R, uint64_t* __restrict__ cz,
                                      uint64_t* __restrict__ nz) {
   __shared__ uint32_t wsum[8];
   __shared__ uint64_t carry_s;
@@ -65,7 +65,7 @@ __global__ void rs_range_scan_kernel(const RsRange* __restrict__ R, uint32_t* __
   __syncthreads();
   for (uint64_t b = 0; b < nch; b += 256) {
     const uint64_t c = b + tid;
-    const uint32_t v = c < nch ? cz[rg.chunk0 + c] : 0u;
+    const uint32_t v = c < nch ? (uint32_t)cz[rg.chunk0 + c] : 0u;
     uint32_t x = v;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -79,7 +79,7 @@ __global__ void rs_range_scan_kernel(const RsRange* __restrict__ R, uint32_t* __
       tot += wsum[w];
     }
     const uint64_t carry = carry_s;
-    if (c < nch) cz[rg.chunk0 + c] = (uint32_t)(carry + before + x - v);  // exclusive, < 2^32 (sizes < 2^32)
+    if (c < nch) cz[rg.chunk0 + c] = carry + before + x - v;  // exclusive
     __syncthreads();
     if (tid == 0) carry_s = carry + tot;
     __syncthreads();
@@ -142,7 +142,7 @@ __device__ __forceinline__ uint32_t rs_partition_chunk(const V* __restrict__ in,
 
 template <typename V>
 __global__ void __launch_bounds__(256) rs_split_kernel(const RsRange* __restrict__ R, uint32_t nr,
-                                                       const uint32_t* __restrict__ czp,
+                                                       const uint64_t* __restrict__ czp,
                                                        const uint64_t* __restrict__ nz, const V* __restrict__ in,
                                                        V* __restrict__ out) {
   __shared__ uint32_t wsum[8];
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(256) rs_split_kernel(const RsRange* __restrict
   rs_partition_chunk<V>(in, out, rg.sd, 0, rg.lo, cs, len, czp[c], nz[r], wsum);
 }
 
-void launch_rs_level(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, uint32_t* cz, uint64_t* nz,
+void launch_rs_level(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, uint64_t* cz, uint64_t* nz,
                      cudaStream_t st) {
   rs_chunk_zeros_kernel<<<(unsigned)nchunks, 32, 0, st>>>(d_ranges, nr, cz);
   rs_range_scan_kernel<<<nr, 256, 0, st>>>(d_ranges, cz, nz);
@@ -164,7 +164,7 @@ void launch_rs_level(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchu
   (void)eb;
 }
 
-void launch_rs_split(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, const uint32_t* czp,
+void launch_rs_split(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, const uint64_t* czp,
                      const uint64_t* nz, const void* in, void* out, cudaStream_t st) {
   if (eb == 4)
     rs_split_kernel<uint32_t><<<(unsigned)nchunks, 256, 0, st>>>(d_ranges, nr, czp, nz, (const uint32_t*)in,

@@ -84,9 +84,9 @@ struct RsTask {               // a small task: the sequential splitting shuffle 
 };
 struct RsNode { uint64_t lo, hi, off; uint32_t task, level; };   // a split of a task at stream offset off
 struct RsLeaf { uint64_t lo, hi, off; uint32_t task, depth; };   // a Fisher-Yates leaf of a task
-void launch_rs_level(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, uint32_t* cz, uint64_t* nz,
+void launch_rs_level(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, uint64_t* cz, uint64_t* nz,
                      cudaStream_t st);
-void launch_rs_split(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, const uint32_t* czp,
+void launch_rs_split(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, const uint64_t* czp,
                      const uint64_t* nz, const void* in, void* out, cudaStream_t st);
 void launch_rs_plan(const RsTask* T, uint32_t ntasks, uint64_t cutoff, uint16_t* draws, RsNode* nodes,
                     unsigned long long* counts, uint64_t node_cap, RsLeaf* leaves, uint64_t leaf_cap,
