@@ -166,8 +166,10 @@ def run_reference(args, rank, world):
         return
     steps = []
     base = None
+    sample_log2 = min(26, args.log2n)
+    scale = float(os.environ.get("SK_REF_SECONDS", "1"))  # (tests shorten the bounded samples)
     for i in range(args.warmup + args.steps):
-        b = oracle_sample(seconds_target=4.0 if i < args.warmup else 8.0)
+        b = oracle_sample(seconds_target=(4.0 if i < args.warmup else 8.0) * scale, log2n=sample_log2)
         if i >= args.warmup:
             steps.append(b)
         base = b
