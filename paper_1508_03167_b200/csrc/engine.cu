@@ -349,7 +349,7 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
     if (fast_leaf) {
       draws = A.alloc<uint16_t>(ntot, st);
       grid = leaf_apply_grid(nleaves, (uint32_t)mmax, num_sms());
-      lscr = A.alloc<uint16_t>((uint64_t)grid * 2 * ((mmax + 1) & ~1ULL) + 8, st);
+      lscr = A.alloc<uint16_t>((uint64_t)grid * leaf_scratch_stride(mmax) + 8, st);
     }
     fork_side(st, ps);
     {
@@ -420,7 +420,7 @@ static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned 
   const uint64_t nleaves = J.q, K = 1ull << k, B = nleaves >> k;
   const uint32_t mmax = (uint32_t)((n + J.q - 1) >> c);
   const uint32_t grid = leaf_apply_grid(B, mmax, num_sms());
-  uint16_t* lscr = A.alloc<uint16_t>((uint64_t)grid * 2 * ((mmax + 1) & ~1u) + 8, st);
+  uint16_t* lscr = A.alloc<uint16_t>((uint64_t)grid * leaf_scratch_stride(mmax) + 8, st);
   std::vector<cudaEvent_t> ev(K + 1, nullptr);
   ExplicitTask E0{};
   try {
@@ -689,7 +689,7 @@ static uint64_t run_rs_tasks(int eb, void* buf0, void* buf1, const std::vector<R
     uint64_t* dl = A.alloc<uint64_t>(lst[par].size(), st);
     CK(cudaMemcpyAsync(dl, lst[par].data(), lst[par].size() * 8, cudaMemcpyHostToDevice, st));
     const uint32_t grid = leaf_apply_grid(cnt, mmax[par], num_sms());
-    uint16_t* lscr = A.alloc<uint16_t>((uint64_t)grid * 2 * ((mmax[par] + 1) & ~1u) + 8, st);
+    uint16_t* lscr = A.alloc<uint16_t>((uint64_t)grid * leaf_scratch_stride(mmax[par]) + 8, st);
     launch_leaf_apply(eb, J0, E0, cnt, par ? buf1 : buf0, par ? buf0 : buf1, draws, lscr, mmax[par], grid, st, dl);
   }
   if (!serial.empty()) {
@@ -795,7 +795,7 @@ static void run_single_leaf(int eb, void* data, uint64_t lo, uint64_t hi, const 
     if (m <= 65536) {
       uint16_t* draws = A.alloc<uint16_t>(m, st);
       unsigned char* scratch = A.alloc<unsigned char>(m * eb, st);
-      uint16_t* lscr = A.alloc<uint16_t>(2 * ((m + 1) & ~1ULL) + 8, st);
+      uint16_t* lscr = A.alloc<uint16_t>(leaf_scratch_stride(m) + 8, st);
       // absolute-index kernels: shift bases so index lo lands on element 0
       launch_leaf_decode16(J, E, 1, draws - lo, d_bits, st);
       launch_leaf_apply(eb, J, E, 1, data, (void*)(scratch - lo * eb), draws - lo, lscr, (uint32_t)m, 1, st);
@@ -854,6 +854,7 @@ int sk_debug_set(int key, int value) {
   if (key == 1) { debug_set_leaf_stop(value); return 0; }
   if (key == 2) { debug_set_seg_variant(value); return 0; }
   if (key == 4) { debug_set_tree_force_direct(value); return 0; }
+  if (key == 5) { debug_set_leaf_variant(value); return 0; }
   return -1;
 }
 const char* sk_last_error(void) { return g_err.c_str(); }

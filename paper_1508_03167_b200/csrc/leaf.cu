@@ -21,6 +21,8 @@ namespace sk {
 
 // debug: stop the leaf-apply pipeline after phase k (phase timing experiments)
 __device__ int g_leaf_stop = 99;
+// host: 0 = leaf_apply_reg_kernel for leaves > 8192 (default), 1 = leaf_apply_kernel
+static int g_leaf_variant = 1;
 
 // One lane per leaf, one fast-dice-roller *iteration* per loop trip (so lanes
 // whose draws reject do not stall the others), bits served from a per-lane ring
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
   const uint32_t ms = (mmax + 1) & ~1u;
   constexpr bool kStage = BLOCK == 256;
   V* sdata = reinterpret_cast<V*>(sh + ((cw + ((mmax + 1) >> 1) + 1) & ~1u));  // after the buckets, 8-byte aligned
-  uint16_t* Nn = scratch + (uint64_t)blockIdx.x * 2 * ms;
+  uint16_t* Nn = scratch + (uint64_t)blockIdx.x * leaf_scratch_stride(mmax);
   uint16_t* Hg = Nn + ms;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr uint32_t NW = BLOCK / 32;
@@ -344,6 +346,231 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
   }
 }
 
+// Leaf apply with the leaf's draws held in registers (leaves of 8193 .. 65536
+// elements; leaf_apply_kernel keeps the small-leaf configuration).
+//
+// 512 threads; thread t owns steps s = 4096k + 8t + e (k < K, e < 8), whose
+// draws j_s stay in 4K registers (two per register) for the whole leaf, so the
+// bucket passes never re-read them.  Per target half (the upper half first):
+// histogram, scan and scatter of the steps into per-target buckets in shared
+// memory, as in leaf_apply_kernel; then
+//  * every owned step finds its successor N(s) = min{b in bucket(j_s) : b > s}
+//    by scanning its bucket (~3 entries on average) and replaces j_s by it in
+//    its register.  N(s) > s >= j_s, so the 16-bit value tells the two cases
+//    apart, and the upper half's replaced values (> s >= 32768) fail the
+//    lower half's target test;
+//  * every target x of the half stores H(x) = min{b in bucket(x) : b > x}
+//    (coalesced) to the CTA's scratch.
+// Finally H is reloaded into shared memory and each owned output gathers
+// orig[W(N(s))] (W: follow H to its root) or orig[j_s].  No successor table
+// is stored (leaf_apply_kernel's random Nn scatter to L2 is gone), and the
+// outputs go out as 16-byte stores.
+template <typename V, int K, int MINB>
+__global__ void __launch_bounds__(512, MINB)
+    leaf_apply_reg_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves, const V* __restrict__ in, V* __restrict__ out,
+                          const uint16_t* __restrict__ draws, uint16_t* __restrict__ scratch, uint32_t mmax,
+                          const uint64_t* __restrict__ list) {
+  constexpr uint32_t BLOCK = 512;
+  extern __shared__ uint32_t sh[];
+  __shared__ uint32_t warp_tot[BLOCK / 32];
+  const uint32_t half = mmax < kLeafHalf ? mmax : kLeafHalf;
+  const uint32_t cw = (half + 1) >> 1;
+  uint16_t* cur = reinterpret_cast<uint16_t*>(sh);         // [half] bucket cursors
+  uint16_t* bkt = reinterpret_cast<uint16_t*>(sh + cw);    // [mmax] buckets
+  const uint16_t* Hs = reinterpret_cast<const uint16_t*>(sh);  // [mmax] H, at the end
+  // per-CTA scratch: H (16-byte aligned, read back as uint4) and the long-bucket staging
+  uint16_t* Hg = reinterpret_cast<uint16_t*>(
+      ((uintptr_t)(scratch + (uint64_t)blockIdx.x * leaf_scratch_stride(mmax)) + 15) & ~(uintptr_t)15);
+  uint16_t* tmp = Hg + ((mmax + 7) & ~7u) + 8;
+  const uint32_t tid = threadIdx.x;
+
+  for (uint64_t g = blockIdx.x; g < nleaves; g += gridDim.x) {
+    LeafDesc L;
+    if (list) {
+      L.lo = list[2 * g];
+      L.hi = list[2 * g + 1];
+    } else {
+      L = leaf_desc(J, E, g);
+    }
+    const uint32_t m = (uint32_t)(L.hi - L.lo);
+    const V* src_in = in + L.lo;
+    V* dst = out + L.lo;
+    if (m < 2) {
+      if (m == 1 && tid == 0) dst[0] = src_in[0];
+      continue;
+    }
+    const uint16_t* __restrict__ dr = draws + L.lo;
+    if (tid == 0 && g + gridDim.x < nleaves) {  // the next leaf's draws into L2
+      uint64_t nlo, nhi;
+      if (list) {
+        nlo = list[2 * (g + gridDim.x)];
+        nhi = list[2 * (g + gridDim.x) + 1];
+      } else {
+        const LeafDesc Ln = leaf_desc(J, E, g + gridDim.x);
+        nlo = Ln.lo;
+        nhi = Ln.hi;
+      }
+      l2_prefetch(draws + nlo, (size_t)(nhi - nlo) * 2);
+    }
+    uint32_t r[K][4];
+    const bool dvec = (((uintptr_t)dr) & 15) == 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t s0 = (uint32_t)k * 4096 + tid * 8;
+      if (dvec && s0 + 8 <= m) {
+        const uint4 q = *reinterpret_cast<const uint4*>(dr + s0);
+        r[k][0] = q.x; r[k][1] = q.y; r[k][2] = q.z; r[k][3] = q.w;
+      } else {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t a = s0 + 2 * w;
+          const uint32_t lo16 = a < m ? (uint32_t)dr[a] : 0u;
+          const uint32_t hi16 = a + 1 < m ? (uint32_t)dr[a + 1] : 0u;
+          r[k][w] = lo16 | (hi16 << 16);
+        }
+      }
+    }
+    for (int hh = m > kLeafHalf ? 1 : 0; hh >= 0; --hh) {
+      const uint32_t T0 = (uint32_t)hh * kLeafHalf;
+      const uint32_t nt = min(kLeafHalf, m - T0);
+      if (tid == 0 && hh == 0) l2_prefetch(src_in, (size_t)m * sizeof(V));  // gathered next
+      for (uint32_t w = tid; w < ((nt + 1) >> 1); w += BLOCK) sh[w] = 0;
+      __syncthreads();
+      // 1. histogram of the half's targets
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t s = (uint32_t)k * 4096 + tid * 8 + e;
+          const uint32_t jj = ((r[k][e >> 1] >> ((e & 1) << 4)) & 0xFFFFu) - T0;
+          if (s - 1u < m - 1u && jj < nt) atomicAdd(&sh[jj >> 1], 1u << ((jj & 1) << 4));
+        }
+      __syncthreads();
+      if (g_leaf_stop <= 1) continue;
+      // 2. bucket starts
+      scan_counts16(cur, nt, warp_tot);
+      __syncthreads();
+      if (g_leaf_stop <= 2) continue;
+      // 3. scatter step ids into their buckets (cursors end at the bucket ends);
+      //    each step keeps its slot in place of j_s (and a bit in `mine`)
+      uint32_t mine[(K * 8 + 31) / 32];
+#pragma unroll
+      for (int q = 0; q < (K * 8 + 31) / 32; ++q) mine[q] = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t s = (uint32_t)k * 4096 + tid * 8 + e;
+          const uint32_t sh16 = (e & 1) << 4;
+          const uint32_t jj = ((r[k][e >> 1] >> sh16) & 0xFFFFu) - T0;
+          if (s - 1u < m - 1u && jj < nt) {
+            const uint32_t old = atomicAdd(&sh[jj >> 1], 1u << ((jj & 1) << 4));
+            const uint32_t slot = (old >> ((jj & 1) << 4)) & 0xFFFFu;
+            bkt[slot] = (uint16_t)s;
+            r[k][e >> 1] = (r[k][e >> 1] & ~(0xFFFFu << sh16)) | (slot << sh16);
+            mine[(k * 8 + e) >> 5] |= 1u << ((k * 8 + e) & 31);
+          }
+        }
+      __syncthreads();
+      if (g_leaf_stop <= 3) continue;
+      // 4. per target x of the half: every bucket entry b is replaced by its
+      //    successor min{b' in bucket : b' > b} or, if none, by x (<= b), and
+      //    H(x) = min{b in bucket : b > x} goes to the scratch
+      for (uint32_t x = tid; x < nt; x += BLOCK) {
+        const uint32_t st = x ? (uint32_t)cur[x - 1] : 0u, n = (uint32_t)cur[x] - st;
+        const uint32_t p = T0 + x;
+        uint32_t H = 0x10000u;
+        if (n <= 4) {
+          uint32_t v[4], res[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = (uint32_t)i < n ? (uint32_t)bkt[st + i] : 0u;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint32_t best = 0x10000u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) best = (v[j] > v[i] && v[j] < best) ? v[j] : best;
+            res[i] = best < 0x10000u ? best : p;
+            H = (v[i] > p && v[i] < H) ? v[i] : H;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if ((uint32_t)i < n) bkt[st + i] = (uint16_t)res[i];
+        } else {  // long buckets (small targets): results staged in the scratch
+          for (uint32_t i = 0; i < n; ++i) {
+            const uint32_t vi = bkt[st + i];
+            uint32_t best = 0x10000u;
+            for (uint32_t j = 0; j < n; ++j) {
+              const uint32_t vj = bkt[st + j];
+              best = (vj > vi && vj < best) ? vj : best;
+            }
+            tmp[st + i] = (uint16_t)(best < 0x10000u ? best : p);
+            H = (vi > p && vi < H) ? vi : H;
+          }
+          for (uint32_t i = 0; i < n; ++i) bkt[st + i] = tmp[st + i];
+        }
+        Hg[p] = (uint16_t)(H & 0xFFFFu);
+      }
+      __syncthreads();
+      if (g_leaf_stop <= 4) continue;
+      // 5. the owned steps of the half pick up N(s) or j_s from their slot
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (mine[(k * 8 + e) >> 5] & (1u << ((k * 8 + e) & 31))) {
+            const uint32_t sh16 = (e & 1) << 4;
+            const uint32_t slot = (r[k][e >> 1] >> sh16) & 0xFFFFu;
+            r[k][e >> 1] = (r[k][e >> 1] & ~(0xFFFFu << sh16)) | ((uint32_t)bkt[slot] << sh16);
+          }
+        }
+      __syncthreads();
+    }
+    if (g_leaf_stop <= 5) continue;
+    // H into shared memory (over the cursors and buckets)
+    for (uint32_t w = tid; w < ((m + 7) >> 3); w += BLOCK)
+      reinterpret_cast<uint4*>(sh)[w] = reinterpret_cast<const uint4*>(Hg)[w];
+    __syncthreads();
+    // 6. gather: final[s] = orig[W(N(s))] or orig[j_s]; final[0] = orig[W(0)]
+    const bool ovec = (((uintptr_t)dst) & 15) == 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t s0 = (uint32_t)k * 4096 + tid * 8;
+      if (s0 < m) {
+        V v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t s = s0 + e;
+          const uint32_t x = (r[k][e >> 1] >> ((e & 1) << 4)) & 0xFFFFu;
+          uint32_t src = x;
+          if (s == 0 || x > s) {
+            uint32_t y = s == 0 ? 0u : x, h;
+            while ((h = Hs[y]) != 0) y = h;
+            src = y;
+          }
+          v[e] = s < m ? (g_leaf_stop == 6 ? (V)src : src_in[src]) : V(0);
+        }
+        if (ovec && s0 + 8 <= m) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + s0);
+          if constexpr (sizeof(V) == 4) {
+            d4[0] = make_uint4(v[0], v[1], v[2], v[3]);
+            d4[1] = make_uint4(v[4], v[5], v[6], v[7]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              d4[q] = make_uint4((uint32_t)v[2 * q], (uint32_t)(v[2 * q] >> 32), (uint32_t)v[2 * q + 1],
+                                 (uint32_t)(v[2 * q + 1] >> 32));
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (s0 + e < m) dst[s0 + e] = v[e];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Fallback for leaves larger than 65536 elements (non-default cutoffs and
 // fisher_yates on long arrays): one thread per leaf runs the reference loop
 // directly on `out` (which already holds a copy of the input).
@@ -367,6 +594,7 @@ __global__ void leaf_serial_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
 }
 
 // ---------------------------------------------------------------- launchers
+void debug_set_leaf_variant(int v) { g_leaf_variant = v; }
 void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int)); }
 
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
@@ -392,7 +620,21 @@ static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nlea
                          const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid,
                          const uint64_t* list, cudaStream_t st) {
   size_t smem = leaf_apply_smem(mmax, (int)sizeof(V));
-  if (mmax > 8192) {
+  if (mmax > 8192 && g_leaf_variant == 0) {
+    if (mmax <= 16384) {
+      auto k = leaf_apply_reg_kernel<V, 4, 2>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
+    } else if (mmax <= 32768) {
+      auto k = leaf_apply_reg_kernel<V, 8, 1>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
+    } else {
+      auto k = leaf_apply_reg_kernel<V, 16, 1>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
+    }
+  } else if (mmax > 8192) {
     auto k = leaf_apply_kernel<V, 1024>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<grid, 1024, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
@@ -410,6 +652,8 @@ uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms) {
   size_t smem = leaf_apply_smem(mmax);
   size_t fit = (size_t)(220 * 1024) / (smem + 2048);
   int per_sm = (int)std::max((size_t)1, std::min(fit, (size_t)(mmax > 8192 ? 2 : 8)));
+  if (mmax > 8192 && g_leaf_variant == 0)  // register-resident draws: 512 threads, 1-3 CTAs per SM
+    per_sm = mmax <= 16384 ? 2 : 1;
   uint64_t g = (uint64_t)num_sms * per_sm;
   if (g > nleaves) g = nleaves;
   return (uint32_t)(g ? g : 1);

@@ -917,8 +917,23 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
   //    most 64 positions on, warp 0 finishes alone with warp barriers.
   const uint32_t ltmask = ~(0xffffffffu >> lane);
   int h = 0;
+  constexpr uint32_t NWp = kTreeBlock / 32;
   for (; h + 1 < nw && goff[h + 1] - goff[h] > 2; ++h) {
-    for (uint32_t G = goff[h] + wid; G < goff[h + 1]; G += kTreeBlock / 32) {
+    // two groups per trip (independent slots): their smem round trips overlap
+    const uint32_t g1 = goff[h + 1];
+    uint32_t G = goff[h] + wid;
+    for (; G + NWp < g1; G += 2 * NWp) {
+      const uint4 d0 = gdesc[G], d1 = gdesc[G + NWp];
+      const bool on0 = (d0.x << lane) >> 31, on1 = (d1.x << lane) >> 31;
+      const uint32_t ia0 = d0.y + lane, ib0 = d0.z + __popc(d0.x & ltmask);
+      const uint32_t ia1 = d1.y + lane, ib1 = d1.z + __popc(d1.x & ltmask);
+      V va0, vb0, va1, vb1;
+      if (on0) { va0 = stage[ia0]; vb0 = stage[ib0]; }
+      if (on1) { va1 = stage[ia1]; vb1 = stage[ib1]; }
+      if (on0) { stage[ia0] = vb0; stage[ib0] = va0; }
+      if (on1) { stage[ia1] = vb1; stage[ib1] = va1; }
+    }
+    if (G < g1) {
       const uint4 d = gdesc[G];
       if ((d.x << lane) >> 31) {
         const uint32_t ia = d.y + lane, ib = d.z + __popc(d.x & ltmask);
