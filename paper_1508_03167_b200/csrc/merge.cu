@@ -791,50 +791,56 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
   const uint64_t* R = rank + Pp->rank_off;
   // TMA needs in[] and out[] (every part) equally aligned mod 16 bytes
   const bool tma = acc.same_alignment();
+  // 1. windows: lane h owns window h.  Every warp derives the same staging
+  //    layout in registers (no block barrier before the bits are ranked);
+  //    warp 0 publishes it to shared memory and issues the TMA loads.
+  uint64_t a = 0, b = 0;
+  if (lane < (uint32_t)kTreeD) {
+    a = ca[lane];
+    b = ca[kTreeD + lane];
+  }
+  const uint32_t emp = __ballot_sync(0xffffffffu, lane < (uint32_t)kTreeD && a == b);
+  const uint32_t nw = emp ? (uint32_t)(__ffs(emp) - 1) : (uint32_t)kTreeD;
+  const bool act = lane < nw;
+  const uint64_t len = act ? b - a : 0;
+  const bool big = len > C::SCAP;
+  uint32_t mis = 0, reg = 0, gc = 0, lo = 0, hi = 0, bytes = 0;
+  if (act && !big) {
+    const uintptr_t A0 = reinterpret_cast<uintptr_t>(acc.src(a));
+    mis = (uint32_t)((A0 & 15) / sizeof(V));
+    reg = (mis + (uint32_t)len + C::E - 1) & ~(C::E - 1);
+    gc = (uint32_t)((len + 31) >> 5);
+    const uint64_t l0 = (C::E - mis) & (C::E - 1);  // first 16-byte aligned offset
+    const uint64_t l1 = ((mis + len) & ~(uint64_t)(C::E - 1)) - mis;
+    if (tma && l1 > l0 && l1 <= len) {
+      lo = (uint32_t)l0;
+      hi = (uint32_t)l1;
+      bytes = (uint32_t)((l1 - l0) * sizeof(V));
+    }
+  }
+  uint32_t sreg = reg, sgc = gc, sby = bytes;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y1 = __shfl_up_sync(0xffffffffu, sreg, o);
+    const uint32_t y2 = __shfl_up_sync(0xffffffffu, sgc, o);
+    const uint32_t y3 = __shfl_up_sync(0xffffffffu, sby, o);
+    if (lane >= (uint32_t)o) { sreg += y1; sgc += y2; sby += y3; }
+  }
+  const uint32_t treg = __shfl_sync(0xffffffffu, sreg, 31), tgc = __shfl_sync(0xffffffffu, sgc, 31);
+  const uint32_t tby = __shfl_sync(0xffffffffu, sby, 31);
+  const bool ok = nw < (uint32_t)kTreeD && !__any_sync(0xffffffffu, big) && treg <= C::SCAP && tgc <= C::GCAP &&
+                  !g_tree_force_direct;
+  const uint32_t r_stoff = sreg - reg + mis, r_goff = act ? sgc - gc : tgc;
+  const uint32_t r_ilo = hi > lo ? lo : (uint32_t)len, r_ihi = hi > lo ? hi : (uint32_t)len;
   if (wid == 0) {
-    // 1. windows: lane h owns window h
-    uint64_t a = 0, b = 0;
     if (lane < (uint32_t)kTreeD) {
-      a = ca[lane];
-      b = ca[kTreeD + lane];
       ach[lane] = a;
       bch[lane] = b;
     }
-    const uint32_t emp = __ballot_sync(0xffffffffu, lane < (uint32_t)kTreeD && a == b);
-    const uint32_t nw = emp ? (uint32_t)(__ffs(emp) - 1) : (uint32_t)kTreeD;
-    const bool act = lane < nw;
-    const uint64_t len = act ? b - a : 0;
-    const bool big = len > C::SCAP;
-    uint32_t mis = 0, reg = 0, gc = 0, lo = 0, hi = 0, bytes = 0;
-    if (act && !big) {
-      const uintptr_t A0 = reinterpret_cast<uintptr_t>(acc.src(a));
-      mis = (uint32_t)((A0 & 15) / sizeof(V));
-      reg = (mis + (uint32_t)len + C::E - 1) & ~(C::E - 1);
-      gc = (uint32_t)((len + 31) >> 5);
-      const uint64_t l0 = (C::E - mis) & (C::E - 1);  // first 16-byte aligned offset
-      const uint64_t l1 = ((mis + len) & ~(uint64_t)(C::E - 1)) - mis;
-      if (tma && l1 > l0 && l1 <= len) {
-        lo = (uint32_t)l0;
-        hi = (uint32_t)l1;
-        bytes = (uint32_t)((l1 - l0) * sizeof(V));
-      }
-    }
-    uint32_t sreg = reg, sgc = gc, sby = bytes;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y1 = __shfl_up_sync(0xffffffffu, sreg, o);
-      const uint32_t y2 = __shfl_up_sync(0xffffffffu, sgc, o);
-      const uint32_t y3 = __shfl_up_sync(0xffffffffu, sby, o);
-      if (lane >= (uint32_t)o) { sreg += y1; sgc += y2; sby += y3; }
-    }
-    const uint32_t treg = __shfl_sync(0xffffffffu, sreg, 31), tgc = __shfl_sync(0xffffffffu, sgc, 31);
-    const uint32_t tby = __shfl_sync(0xffffffffu, sby, 31);
-    const bool ok = nw < (uint32_t)kTreeD && !__any_sync(0xffffffffu, big) && treg <= C::SCAP && tgc <= C::GCAP &&
-                    !g_tree_force_direct;
     if (act) {
-      stoff[lane] = sreg - reg + mis;
-      goff[lane] = sgc - gc;
-      ilo_s[lane] = hi > lo ? lo : (uint32_t)len;
-      ihi_s[lane] = hi > lo ? hi : (uint32_t)len;
+      stoff[lane] = r_stoff;
+      goff[lane] = r_goff;
+      ilo_s[lane] = r_ilo;
+      ihi_s[lane] = r_ihi;
     }
     if (lane == 0) {
       goff[nw] = tgc;
@@ -846,38 +852,48 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
     }
     __syncwarp();
     if (ok && act && hi > lo) {
-      V* st = stage + (sreg - reg + mis);
+      V* st = stage + r_stoff;
       acc.runs(a + lo, a + hi, [&](uint64_t x0, uint64_t x1) {
         bulk_g2s(st + (x0 - a), acc.src(x0), (uint32_t)((x1 - x0) * sizeof(V)), &bar);
       });
     }
   }
-  __syncthreads();
-  const int nw = nwin_s;
-  if (nw < 0) {
+  if (!ok) {
+    __syncthreads();
     tree_windows_direct<V>(acc, stage, sd, R, n1, t, ach, bch, wsum, nxt, wF);
     return;
   }
-  const uint32_t ngroups = goff[nw];
+  const uint32_t ngroups = tgc;
   // ragged ends (outside the 16-byte aligned interiors) by plain loads, a warp
   // per window; they complete while the bits are being ranked
-  for (int h = wid; h < nw; h += kTreeBlock / 32) {
-    const uint32_t L = (uint32_t)(bch[h] - ach[h]), lo = ilo_s[h], hi = ihi_s[h];
-    V* st = stage + stoff[h];
-    for (uint32_t i = lane; i < lo; i += 32) st[i] = acc.ld(ach[h] + i);
-    for (uint32_t i = hi + lane; i < L; i += 32) st[i] = acc.ld(ach[h] + i);
+  for (int h = wid; h < (int)nw; h += kTreeBlock / 32) {
+    const uint64_t ah = __shfl_sync(0xffffffffu, a, h);
+    const uint32_t L = (uint32_t)__shfl_sync(0xffffffffu, len, h);
+    const uint32_t wlo = __shfl_sync(0xffffffffu, r_ilo, h), whi = __shfl_sync(0xffffffffu, r_ihi, h);
+    V* st = stage + __shfl_sync(0xffffffffu, r_stoff, h);
+    for (uint32_t i = lane; i < wlo; i += 32) st[i] = acc.ld(ah + i);
+    for (uint32_t i = whi + lane; i < L; i += 32) st[i] = acc.ld(ah + i);
   }
   // 3. group masks (two consecutive groups per thread) and their ones
   uint32_t cnt2[2], hh[2], mm[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const uint32_t G = 2 * tid + e;
-    uint32_t m = 0, h = 0;
+    // window of group G: the last h < nw with goff[h] <= G (binary search over the lanes)
+    uint32_t h = 0;
+#pragma unroll
+    for (uint32_t step = 16; step; step >>= 1) {
+      const uint32_t c = h + step;
+      const uint32_t gc_ = __shfl_sync(0xffffffffu, r_goff, c & 31);
+      h = (c < nw && gc_ <= G) ? c : h;
+    }
+    const uint64_t wa = __shfl_sync(0xffffffffu, a, h), wb = __shfl_sync(0xffffffffu, b, h);
+    const uint32_t wg = __shfl_sync(0xffffffffu, r_goff, h);
+    uint32_t m = 0;
     if (G < ngroups) {
-      while (goff[h + 1] <= G) ++h;
-      const uint64_t p = ach[h] + 32ull * (G - goff[h]);
+      const uint64_t p = wa + 32ull * (G - wg);
       if (p < t) {
-        const uint64_t nv = min(bch[h] - p, t - p);
+        const uint64_t nv = min(wb - p, t - p);
         m = (uint32_t)(bits64_at(sd, p) >> 32);
         if (nv < 32) m &= ~(0xffffffffu >> nv);
       }
