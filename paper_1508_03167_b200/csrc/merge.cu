@@ -779,7 +779,7 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
   uint4* gdesc = reinterpret_cast<uint4*>(stage + C::SCAP);
   __shared__ uint32_t wsum[kTreeBlock / 32];
   __shared__ uint64_t ach[kTreeD], bch[kTreeD], nxt[2];
-  __shared__ uint32_t stoff[kTreeD], goff[kTreeD + 1], gpre_s[C::GCAP];
+  __shared__ uint32_t stoff[kTreeD], goff[kTreeD + 1];
   __shared__ uint32_t ilo_s[kTreeD], ihi_s[kTreeD];
   __shared__ int nwin_s;
   __shared__ __align__(8) uint64_t bar;
@@ -830,6 +830,13 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
   const bool ok = nw < (uint32_t)kTreeD && !__any_sync(0xffffffffu, big) && treg <= C::SCAP && tgc <= C::GCAP &&
                   !g_tree_force_direct;
   const uint32_t r_stoff = sreg - reg + mis, r_goff = act ? sgc - gc : tgc;
+  // ones of the windows before h = sum of the lengths of windows 1..h
+  // (|window w+1| = ones of window w below t)
+  uint32_t r_onesb = lane >= 1 ? (uint32_t)len : 0u;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, r_onesb, o);
+    if (lane >= (uint32_t)o) r_onesb += y;
+  }
   const uint32_t r_ilo = hi > lo ? lo : (uint32_t)len, r_ihi = hi > lo ? hi : (uint32_t)len;
   if (wid == 0) {
     if (lane < (uint32_t)kTreeD) {
@@ -875,7 +882,7 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
     for (uint32_t i = whi + lane; i < L; i += 32) st[i] = acc.ld(ah + i);
   }
   // 3. group masks (two consecutive groups per thread) and their ones
-  uint32_t cnt2[2], hh[2], mm[2];
+  uint32_t cnt2[2], mm[2], gy[2], gz[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const uint32_t G = 2 * tid + e;
@@ -899,7 +906,12 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
       }
     }
     cnt2[e] = __popc(m);
-    hh[e] = h;
+    // descriptor parts known now: stage index of the group's first position,
+    // and of its window's B slots minus the ones of the windows before h
+    const uint32_t st_h = __shfl_sync(0xffffffffu, r_stoff, h), st_h1 = __shfl_sync(0xffffffffu, r_stoff, (h + 1) & 31);
+    const uint32_t ob = __shfl_sync(0xffffffffu, r_onesb, h);
+    gy[e] = st_h + 32 * (G - wg);
+    gz[e] = st_h1 - ob;
     mm[e] = m;
   }
   const uint32_t c2 = cnt2[0] + cnt2[1];
@@ -914,17 +926,10 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
 #pragma unroll
   for (int w = 0; w < kTreeBlock / 32; ++w) before += (w < (int)wid) ? wsum[w] : 0u;
   const uint32_t ex0 = before + x - c2, ex1 = ex0 + cnt2[0];
-  if (2 * tid < ngroups) gpre_s[2 * tid] = ex0;
-  if (2 * tid + 1 < ngroups) gpre_s[2 * tid + 1] = ex1;
-  __syncthreads();
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const uint32_t G = 2 * tid + e;
-    if (G < ngroups) {
-      const uint32_t h = hh[e];
-      const uint32_t k = (e ? ex1 : ex0) - gpre_s[goff[h]];  // rank of the group's first one in window h
-      gdesc[G] = make_uint4(mm[e], stoff[h] + 32 * (G - goff[h]), stoff[h + 1] + k, 0u);
-    }
+    if (G < ngroups) gdesc[G] = make_uint4(mm[e], gy[e], gz[e] + (e ? ex1 : ex0), 0u);
   }
   __syncthreads();
   mbar_wait(&bar, 0);
