@@ -872,14 +872,38 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
   }
   const uint32_t ngroups = tgc;
   // ragged ends (outside the 16-byte aligned interiors) by plain loads, a warp
-  // per window; they complete while the bits are being ranked
-  for (int h = wid; h < (int)nw; h += kTreeBlock / 32) {
-    const uint64_t ah = __shfl_sync(0xffffffffu, a, h);
-    const uint32_t L = (uint32_t)__shfl_sync(0xffffffffu, len, h);
-    const uint32_t wlo = __shfl_sync(0xffffffffu, r_ilo, h), whi = __shfl_sync(0xffffffffu, r_ihi, h);
-    V* st = stage + __shfl_sync(0xffffffffu, r_stoff, h);
-    for (uint32_t i = lane; i < wlo; i += 32) st[i] = acc.ld(ah + i);
-    for (uint32_t i = whi + lane; i < L; i += 32) st[i] = acc.ld(ah + i);
+  // per window.  With TMA they are short (head < 2E-1, tail < E elements):
+  // loaded into registers now, stored to shared memory after the bits are
+  // ranked, so their latency overlaps that work.
+  constexpr int kRagW = (kTreeD + kTreeBlock / 32 - 1) / (kTreeBlock / 32);  // windows per warp
+  V rag[kRagW];
+  uint32_t ragi[kRagW];
+  if (tma) {
+#pragma unroll
+    for (int k = 0; k < kRagW; ++k) {
+      const int h = wid + k * (kTreeBlock / 32);
+      ragi[k] = 0xffffffffu;
+      if (h < (int)nw) {
+        const uint64_t ah = __shfl_sync(0xffffffffu, a, h);
+        const uint32_t L = (uint32_t)__shfl_sync(0xffffffffu, len, h);
+        const uint32_t wlo = __shfl_sync(0xffffffffu, r_ilo, h), whi = __shfl_sync(0xffffffffu, r_ihi, h);
+        const uint32_t so = __shfl_sync(0xffffffffu, r_stoff, h);
+        const uint32_t i = lane < 8 ? lane : whi + lane - 8;
+        if (lane < 16 && i < (lane < 8 ? wlo : L)) {
+          ragi[k] = so + i;
+          rag[k] = acc.ld(ah + i);
+        }
+      }
+    }
+  } else {
+    for (int h = wid; h < (int)nw; h += kTreeBlock / 32) {
+      const uint64_t ah = __shfl_sync(0xffffffffu, a, h);
+      const uint32_t L = (uint32_t)__shfl_sync(0xffffffffu, len, h);
+      const uint32_t wlo = __shfl_sync(0xffffffffu, r_ilo, h), whi = __shfl_sync(0xffffffffu, r_ihi, h);
+      V* st = stage + __shfl_sync(0xffffffffu, r_stoff, h);
+      for (uint32_t i = lane; i < wlo; i += 32) st[i] = acc.ld(ah + i);
+      for (uint32_t i = whi + lane; i < L; i += 32) st[i] = acc.ld(ah + i);
+    }
   }
   // 3. group masks (two consecutive groups per thread) and their ones
   uint32_t cnt2[2], mm[2], gy[2], gz[2];
@@ -921,6 +945,11 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
     if (lane >= (uint32_t)o) x += y;
   }
   if (lane == 31) wsum[wid] = x;
+  if (tma) {
+#pragma unroll
+    for (int k = 0; k < kRagW; ++k)
+      if (ragi[k] != 0xffffffffu) stage[ragi[k]] = rag[k];
+  }
   __syncthreads();
   uint32_t before = 0;
 #pragma unroll
