@@ -21,8 +21,10 @@ namespace sk {
 
 // debug: stop the leaf-apply pipeline after phase k (phase timing experiments)
 __device__ int g_leaf_stop = 99;
-// host: 0 = leaf_apply_reg_kernel for leaves > 8192 (default), 1 = leaf_apply_kernel
-static int g_leaf_variant = 1;
+// host, leaves > 8192: 2 = leaf_apply_v3_kernel (default), 1 = leaf_apply_kernel,
+// 0 = leaf_apply_reg_kernel
+static int g_leaf_variant = 2;
+static int g_leaf_v3_block = 1024;  // threads per CTA of leaf_apply_v3_kernel
 
 // One lane per leaf, one fast-dice-roller *iteration* per loop trip (so lanes
 // whose draws reject do not stall the others), bits served from a per-lane ring
@@ -571,6 +573,390 @@ __global__ void __launch_bounds__(512, MINB)
   }
 }
 
+// Leaf apply, one pass over all targets (leaves of 8193 .. 65536 elements).
+//
+// 1024 threads; thread t owns steps s = 8192k + 8t + e (k, e < 8), whose 16-bit
+// values (the draw j_s, then its bucket slot, then N(s) or j_s) stay in 32
+// registers.  The per-target counters are BYTES (four per word, 64 KB for
+// 65536 targets) grouped by 16 targets, with one 16-bit start per group, so
+// the counters, the group starts and the whole bucket array (128 KB) fit in
+// shared memory together and no target halves are needed:
+//  1. histogram: one byte atomic per step;
+//  2. per group of 16 targets: its total and the in-group exclusive prefixes
+//     (in place, dp4a + a byte-prefix multiply), block scan of the totals.
+//     A group total above 255 (never seen: the counts near target 0 are
+//     ~ln(m/p), a group of 16 holds ~150 at most) or a lost carry (byte sum
+//     != m - 1) sends the leaf to the serial fallback;
+//  3. scatter: the byte atomic returns the step's slot in its bucket; the
+//     counters end as the bucket ends;
+//  4. per target (four per counter word, consecutive targets on consecutive
+//     lanes): buckets of <= 2 steps are resolved branch-free in place
+//     (slot <- successor N(s), or the target itself when s is the bucket's
+//     last step); H(p) = min{b in bucket(p) : b > p} goes to the CTA's
+//     scratch; larger buckets are queued;
+//  5. queued buckets: <= 8 entries in registers, longer ones through the
+//     scratch (O(k^2), k ~ ln(m/p): only the first few hundred targets);
+//  6. each owned step picks up its slot's value;
+//  7. H into shared memory (over the buckets), then every output gathers
+//     orig[W(N(s))] (W: follow H to its root) or orig[j_s]; 16-byte stores.
+__device__ int g_leaf_force_fallback = 0;
+
+__device__ __forceinline__ void cx(uint32_t& a, uint32_t& b) {
+  const uint32_t lo = min(a, b), hi = max(a, b);
+  a = lo;
+  b = hi;
+}
+// Batcher odd-even merge sorts (19 and 63 compare-exchanges), ascending
+__device__ __forceinline__ void sort_net8(uint32_t* k) {
+#pragma unroll
+  for (int p = 1; p < 8; p <<= 1)
+#pragma unroll
+    for (int q = p; q >= 1; q >>= 1)
+#pragma unroll
+      for (int j = q % p; j + q < 8; j += 2 * q)
+#pragma unroll
+        for (int i = 0; i < q; ++i)
+          if ((i + j) / (2 * p) == (i + j + q) / (2 * p) && i + j + q < 8) cx(k[i + j], k[i + j + q]);
+}
+__device__ __forceinline__ void sort_net16(uint32_t* k) {
+#pragma unroll
+  for (int p = 1; p < 16; p <<= 1)
+#pragma unroll
+    for (int q = p; q >= 1; q >>= 1)
+#pragma unroll
+      for (int j = q % p; j + q < 16; j += 2 * q)
+#pragma unroll
+        for (int i = 0; i < q; ++i)
+          if ((i + j) / (2 * p) == (i + j + q) / (2 * p) && i + j + q < 16) cx(k[i + j], k[i + j + q]);
+}
+
+template <typename V, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, 1)
+    leaf_apply_v3_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves, const V* __restrict__ in, V* __restrict__ out,
+                         const uint16_t* __restrict__ draws, uint16_t* scratch, uint32_t mmax,
+                         const uint64_t* __restrict__ list) {
+  constexpr uint32_t NP = 32768 / BLOCK;   // step pairs per thread
+  constexpr uint32_t GPT = 4096 / BLOCK;   // groups of 16 targets per thread (phase 2)
+  extern __shared__ __align__(16) uint32_t sh[];
+  __shared__ uint32_t wsum[BLOCK / 32];
+  __shared__ uint32_t s_nlong, s_bad;
+  __shared__ __align__(8) uint64_t s_bar;
+  uint32_t s_phase = 0;
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  const uint32_t nwmax = ((mmax + 15) >> 4) << 2;  // counter words, whole groups of 16 targets
+  uint32_t* cnt = sh;
+  uint16_t* gst = reinterpret_cast<uint16_t*>(sh + nwmax);
+  const uint32_t bkt_w = nwmax + (((nwmax >> 2) + 7) >> 3 << 2);
+  uint16_t* bkt = reinterpret_cast<uint16_t*>(sh + bkt_w);
+  // the gather stages the leaf's data through the whole allocation in chunks
+  const uint32_t chunk = ((bkt_w * 4 + ((mmax + 7) & ~7u) * 2) / (uint32_t)sizeof(V)) & ~3u;
+  V* sdata = reinterpret_cast<V*>(sh);
+  const uint32_t mr = (mmax + 15) & ~15u;
+  uint16_t* Hg = reinterpret_cast<uint16_t*>(
+      ((uintptr_t)(scratch + (uint64_t)blockIdx.x * leaf_scratch_stride(mmax)) + 15) & ~(uintptr_t)15);
+  uint16_t* lst = Hg + mr;
+  uint16_t* tmp = lst + mr;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  for (uint64_t g = blockIdx.x; g < nleaves; g += gridDim.x) {
+    LeafDesc L;
+    if (list) {
+      L.lo = list[2 * g];
+      L.hi = list[2 * g + 1];
+    } else {
+      L = leaf_desc(J, E, g);
+    }
+    const uint32_t m = (uint32_t)(L.hi - L.lo);
+    const V* src_in = in + L.lo;
+    V* dst = out + L.lo;
+    if (m < 2) {
+      if (m == 1 && tid == 0) dst[0] = src_in[0];
+      continue;
+    }
+    const uint16_t* __restrict__ dr = draws + L.lo;
+    if (tid == 0 && g + gridDim.x < nleaves) {  // the next leaf's draws into L2
+      uint64_t nlo, nhi;
+      if (list) {
+        nlo = list[2 * (g + gridDim.x)];
+        nhi = list[2 * (g + gridDim.x) + 1];
+      } else {
+        const LeafDesc Ln = leaf_desc(J, E, g + gridDim.x);
+        nlo = Ln.lo;
+        nhi = Ln.hi;
+      }
+      l2_prefetch(draws + nlo, (size_t)(nhi - nlo) * 2);
+    }
+    const uint32_t nw = ((m + 15) >> 4) << 2;  // this leaf's counter words
+    for (uint32_t w = tid; w < (nw >> 2); w += BLOCK) reinterpret_cast<uint4*>(cnt)[w] = make_uint4(0, 0, 0, 0);
+    if (tid == 0) {
+      s_nlong = 0;
+      s_bad = g_leaf_force_fallback;
+    }
+    // r[i]: steps 2P and 2P+1 of pair P = tid + 1024 i (low / high half-word)
+    uint32_t r[NP];
+    const bool dal = (((uintptr_t)dr) & 3) == 0;
+#pragma unroll
+    for (int i = 0; i < (int)NP; ++i) {
+      const uint32_t s0 = 2 * (tid + BLOCK * i);
+      if (dal && s0 + 2 <= m) {
+        r[i] = *reinterpret_cast<const uint32_t*>(dr + s0);
+      } else {
+        const uint32_t lo16 = s0 < m ? (uint32_t)dr[s0] : 0u;
+        const uint32_t hi16 = s0 + 1 < m ? (uint32_t)dr[s0 + 1] : 0u;
+        r[i] = lo16 | (hi16 << 16);
+      }
+    }
+    __syncthreads();
+    // 1. histogram (byte counters)
+#pragma unroll
+    for (int i = 0; i < (int)NP; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t s = 2 * (tid + BLOCK * i) + h;
+        const uint32_t j = (r[i] >> (16 * h)) & 0xFFFFu;
+        if (s - 1u < m - 1u) atomicAdd(&cnt[j >> 2], 1u << ((j & 3) << 3));
+      }
+    __syncthreads();
+    if (g_leaf_stop <= 1) continue;
+    // 2. group totals and in-group prefixes; thread t: groups GPT*t .. GPT*t+GPT-1
+    {
+      const uint32_t ng = nw >> 2;
+      uint32_t tot[GPT], tsum = 0;
+      bool bad = false;
+#pragma unroll
+      for (int q = 0; q < (int)GPT; ++q) {
+        const uint32_t G = GPT * tid + q;
+        tot[q] = 0;
+        if (G < ng) {
+          uint4 c4 = reinterpret_cast<uint4*>(cnt)[G];
+          const uint32_t s0 = __dp4a(c4.x, 0x01010101u, 0u), s1 = __dp4a(c4.y, 0x01010101u, 0u);
+          const uint32_t s2 = __dp4a(c4.z, 0x01010101u, 0u), s3 = __dp4a(c4.w, 0x01010101u, 0u);
+          const uint32_t b1 = s0, b2 = s0 + s1, b3 = b2 + s2, T = b3 + s3;
+          c4.x = c4.x * 0x01010100u;
+          c4.y = c4.y * 0x01010100u + b1 * 0x01010101u;
+          c4.z = c4.z * 0x01010100u + b2 * 0x01010101u;
+          c4.w = c4.w * 0x01010100u + b3 * 0x01010101u;
+          reinterpret_cast<uint4*>(cnt)[G] = c4;
+          tot[q] = T;
+          bad |= T > 255u;
+          tsum += T;
+        }
+      }
+      uint32_t x = tsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+      }
+      if (lane == 31) wsum[wid] = x;
+      if (bad) s_bad = 1;
+      __syncthreads();
+      if (wid == 0) {
+        const uint32_t v = lane < BLOCK / 32 ? wsum[lane] : 0u;
+        uint32_t z = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+          if (lane >= (uint32_t)o) z += y;
+        }
+        if (lane < BLOCK / 32) wsum[lane] = z - v;
+        if (lane == 31 && z != m - 1) s_bad = 1;  // a byte counter wrapped
+      }
+      __syncthreads();
+      uint32_t base = wsum[wid] + x - tsum;
+#pragma unroll
+      for (int q = 0; q < (int)GPT; ++q) {
+        const uint32_t G = GPT * tid + q;
+        if (G < ng) gst[G] = (uint16_t)base;
+        base += tot[q];
+      }
+    }
+    __syncthreads();
+    if (s_bad) {
+      // serial fallback (counter overflow: not expected to ever happen)
+      for (uint32_t i = tid; i < m; i += BLOCK) dst[i] = src_in[i];
+      __syncthreads();
+      if (tid == 0)
+        for (uint32_t i = m - 1; i >= 1; --i) {
+          const uint32_t j = dr[i];
+          const V t = dst[i];
+          dst[i] = dst[j];
+          dst[j] = t;
+        }
+      __syncthreads();
+      continue;
+    }
+    if (g_leaf_stop <= 2) continue;
+    // 3. scatter step ids into their buckets; the byte atomic gives the slot
+#pragma unroll
+    for (int i = 0; i < (int)NP; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t s = 2 * (tid + BLOCK * i) + h;
+        const uint32_t j = (r[i] >> (16 * h)) & 0xFFFFu;
+        if (s - 1u < m - 1u) {
+          const uint32_t sh8 = (j & 3) << 3;
+          const uint32_t old = atomicAdd(&cnt[j >> 2], 1u << sh8);
+          const uint32_t slot = (uint32_t)gst[j >> 4] + ((old >> sh8) & 0xFFu);
+          bkt[slot] = (uint16_t)s;
+          r[i] = (r[i] & ~(0xFFFFu << (16 * h))) | (slot << (16 * h));
+        }
+      }
+    __syncthreads();
+    if (g_leaf_stop <= 3) continue;
+    if (tid == 0) l2_prefetch(src_in, (size_t)m * sizeof(V));  // staged in phase 8
+    // 4. targets, four per counter word (the counters now hold in-group bucket ends)
+    for (uint32_t w = tid; w < nw; w += BLOCK) {
+      const uint32_t e4 = cnt[w];
+      const uint32_t pe = (w & 3) ? (cnt[w - 1] >> 24) : 0u;
+      const uint32_t base = gst[w >> 2];
+      uint32_t Hq[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t p = 4 * w + q;
+        const uint32_t en = (e4 >> (8 * q)) & 0xFFu;
+        const uint32_t sn = q ? ((e4 >> (8 * (q - 1))) & 0xFFu) : pe;
+        const uint32_t k = p < m ? en - sn : 0u;
+        const uint32_t st = base + sn;
+        const uint32_t v0 = k >= 1 ? (uint32_t)bkt[st] : 0u;
+        const uint32_t v1 = k >= 2 ? (uint32_t)bkt[st + 1] : 0u;
+        uint32_t H = 0;
+        if (k >= 3) {
+          lst[atomicAdd(&s_nlong, 1u)] = (uint16_t)p;
+        } else if (k == 1) {
+          bkt[st] = (uint16_t)p;
+          H = v0 > p ? v0 : 0u;
+        } else if (k == 2) {
+          bkt[st] = (uint16_t)(v0 < v1 ? v1 : p);
+          bkt[st + 1] = (uint16_t)(v1 < v0 ? v0 : p);
+          const uint32_t lo = min(v0, v1), hi = max(v0, v1);
+          H = lo > p ? lo : hi;
+        }
+        Hq[q] = H;
+      }
+      *reinterpret_cast<uint2*>(Hg + 4 * w) = make_uint2(Hq[0] | (Hq[1] << 16), Hq[2] | (Hq[3] << 16));
+    }
+    __syncthreads();
+    if (g_leaf_stop <= 4) continue;
+    // 5. queued buckets (>= 3 steps): keys (step << 16 | slot) through a sorting
+    //    network; the entry at sorted position a gets the step at a + 1
+    for (uint32_t i = tid; i < s_nlong; i += BLOCK) {
+      const uint32_t p = lst[i];
+      const uint32_t w = p >> 2, q = p & 3;
+      const uint32_t cw = cnt[w];
+      const uint32_t en = (cw >> (8 * q)) & 0xFFu;
+      const uint32_t sn = q ? ((cw >> (8 * (q - 1))) & 0xFFu) : ((w & 3) ? (cnt[w - 1] >> 24) : 0u);
+      const uint32_t k = en - sn, st = (uint32_t)gst[w >> 2] + sn;
+      uint32_t H;
+      if (k <= 8) {
+        uint32_t key[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+          key[a] = (uint32_t)a < k ? (((uint32_t)bkt[st + a] << 16) | (st + a)) : 0xFFFFFFFFu;
+        sort_net8(key);
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+          if ((uint32_t)a < k)
+            bkt[key[a] & 0xFFFFu] = (uint16_t)((uint32_t)(a + 1) < k ? (key[a < 7 ? a + 1 : 7] >> 16) : p);
+        H = (key[0] >> 16) > p ? (key[0] >> 16) : (key[1] >> 16);
+      } else {  // the first few targets only: O(k^2) through the scratch
+        H = 0x10000u;
+        for (uint32_t a = 0; a < k; ++a) {
+          const uint32_t va = bkt[st + a];
+          uint32_t best = 0x10000u;
+          for (uint32_t b = 0; b < k; ++b) {
+            const uint32_t vb = bkt[st + b];
+            best = (vb > va && vb < best) ? vb : best;
+          }
+          tmp[st + a] = (uint16_t)(best < 0x10000u ? best : p);
+          H = (va > p && va < H) ? va : H;
+        }
+        for (uint32_t a = 0; a < k; ++a) bkt[st + a] = tmp[st + a];
+        H &= 0xFFFFu;
+      }
+      Hg[p] = (uint16_t)H;
+    }
+    __syncthreads();
+    if (g_leaf_stop <= 5) continue;
+    // 6. every owned step picks up N(s) (> s) or its target j_s (<= s)
+#pragma unroll
+    for (int i = 0; i < (int)NP; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t s = 2 * (tid + BLOCK * i) + h;
+        if (s - 1u < m - 1u) {
+          const uint32_t slot = (r[i] >> (16 * h)) & 0xFFFFu;
+          r[i] = (r[i] & ~(0xFFFFu << (16 * h))) | ((uint32_t)bkt[slot] << (16 * h));
+        }
+      }
+    __syncthreads();
+    // 7. H into shared memory (over the buckets); every output's source:
+    //    W(N(s)) (follow H to its root) or j_s; W(0) for output 0
+    for (uint32_t w = tid; w < ((m + 7) >> 3); w += BLOCK)
+      reinterpret_cast<uint4*>(bkt)[w] = reinterpret_cast<const uint4*>(Hg)[w];
+    __syncthreads();
+    if (g_leaf_stop <= 6) continue;
+    {
+      const uint16_t* Hs = bkt;
+#pragma unroll
+      for (int i = 0; i < (int)NP; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t s = 2 * (tid + BLOCK * i) + h;
+          const uint32_t x = (r[i] >> (16 * h)) & 0xFFFFu;
+          if (s < m && (s == 0 || x > s)) {
+            uint32_t y = s == 0 ? 0u : x, hh;
+            while ((hh = Hs[y]) != 0) y = hh;
+            r[i] = (r[i] & ~(0xFFFFu << (16 * h))) | (y << (16 * h));
+          }
+          if (s >= m) r[i] |= 0xFFFFu << (16 * h);  // no output: a source no chunk holds
+        }
+    }
+    __syncthreads();
+    if (g_leaf_stop == 7) continue;
+    // 8. gather through shared memory: the leaf's data in chunks over the whole
+    //    allocation (H is dead); each output is stored in the pass holding its source
+    const bool sal = (((uintptr_t)src_in) & 15) == 0;
+    for (uint32_t c0 = 0; c0 < m; c0 += chunk) {
+      const uint32_t cn = min(chunk, m - c0);
+      if (sal && (cn * (uint32_t)sizeof(V)) % 16 == 0) {
+        // one TMA bulk copy (the chunk is 16-byte aligned and sized)
+        if (tid == 0) {
+          fence_proxy_async_smem();  // earlier generic accesses of this smem first
+          if (g_leaf_stop != 11) {
+            mbar_arrive_expect_tx(&s_bar, cn * (uint32_t)sizeof(V));
+            for (uint32_t o = 0; o < cn * (uint32_t)sizeof(V); o += 65536u)
+              bulk_g2s(reinterpret_cast<char*>(sdata) + o, reinterpret_cast<const char*>(src_in + c0) + o,
+                       min(65536u, cn * (uint32_t)sizeof(V) - o), &s_bar);
+          } else {
+            mbar_arrive_expect_tx(&s_bar, 0u);  // timing: no staging
+          }
+        }
+        mbar_wait(&s_bar, s_phase);
+        s_phase ^= 1u;
+      } else {
+        for (uint32_t w = tid; w < cn; w += BLOCK) sdata[w] = src_in[c0 + w];
+      }
+      __syncthreads();
+      // (a per-pass copy of the output pointer keeps the 64 store addresses
+      // from being hoisted out of the chunk loop into registers)
+      V* dpass;
+      asm volatile("mov.b64 %0, %1;" : "=l"(dpass) : "l"(dst + 2 * tid));
+      // ... and the per-output source extraction from being hoisted likewise
+#pragma unroll
+      for (int i = 0; i < (int)NP; ++i) asm volatile("" : "+r"(r[i]));
+#pragma unroll
+      for (int i = 0; i < (int)NP; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t src = ((r[i] >> (16 * h)) & 0xFFFFu) - c0;
+          if (src < cn && g_leaf_stop != 10) dpass[2 * BLOCK * i + h] = g_leaf_stop == 8 ? (V)src : sdata[src];
+        }
+      __syncthreads();
+    }
+  }
+}
+
 // Fallback for leaves larger than 65536 elements (non-default cutoffs and
 // fisher_yates on long arrays): one thread per leaf runs the reference loop
 // directly on `out` (which already holds a copy of the input).
@@ -594,7 +980,11 @@ __global__ void leaf_serial_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
 }
 
 // ---------------------------------------------------------------- launchers
-void debug_set_leaf_variant(int v) { g_leaf_variant = v; }
+void debug_set_leaf_variant(int v) {
+  if (v >= 10) g_leaf_v3_block = v == 10 ? 512 : 1024;
+  else g_leaf_variant = v;
+}
+void debug_set_leaf_fallback(int v) { cudaMemcpyToSymbol(g_leaf_force_fallback, &v, sizeof(int)); }
 void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int)); }
 
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
@@ -615,12 +1005,29 @@ static size_t leaf_apply_smem(uint32_t mmax, int eb = 0) {
   return words * 4;
 }
 
+// v3: byte counters (whole groups of 16 targets), 16-bit group starts, buckets
+static size_t leaf_apply_v3_smem(uint32_t mmax) {
+  const size_t nw = ((size_t)(mmax + 15) >> 4) << 2;
+  return (nw + ((((nw >> 2) + 7) >> 3) << 2)) * 4 + (size_t)((mmax + 7) & ~7u) * 2;
+}
+
 template <typename V>
 static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, const void* in, void* out,
                          const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid,
                          const uint64_t* list, cudaStream_t st) {
   size_t smem = leaf_apply_smem(mmax, (int)sizeof(V));
-  if (mmax > 8192 && g_leaf_variant == 0) {
+  if (mmax > 8192 && g_leaf_variant == 2 && in != out) {  // v3 assumes distinct buffers
+    smem = leaf_apply_v3_smem(mmax);
+    if (g_leaf_v3_block == 512) {
+      auto k = leaf_apply_v3_kernel<V, 512>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
+    } else {
+      auto k = leaf_apply_v3_kernel<V, 1024>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k<<<grid, 1024, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
+    }
+  } else if (mmax > 8192 && g_leaf_variant == 0) {
     if (mmax <= 16384) {
       auto k = leaf_apply_reg_kernel<V, 4, 2>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -652,6 +1059,7 @@ uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms) {
   size_t smem = leaf_apply_smem(mmax);
   size_t fit = (size_t)(220 * 1024) / (smem + 2048);
   int per_sm = (int)std::max((size_t)1, std::min(fit, (size_t)(mmax > 8192 ? 2 : 8)));
+  if (mmax > 8192 && g_leaf_variant == 2) per_sm = 1;  // v3: 1024 threads, ~200 KB
   if (mmax > 8192 && g_leaf_variant == 0)  // register-resident draws: 512 threads, 1-3 CTAs per SM
     per_sm = mmax <= 16384 ? 2 : 1;
   uint64_t g = (uint64_t)num_sms * per_sm;

@@ -14,7 +14,7 @@ void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nle
                           unsigned long long* bits, cudaStream_t st);
 uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms);
 // per-CTA leaf-apply scratch (uint16 elements)
-__host__ __device__ inline uint64_t leaf_scratch_stride(uint64_t mmax) { return 2 * ((mmax + 7) & ~7ULL) + 16; }
+__host__ __device__ inline uint64_t leaf_scratch_stride(uint64_t mmax) { return 3 * ((mmax + 15) & ~15ULL) + 16; }
 void launch_leaf_apply(int eb, const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, const void* in, void* out,
                        const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid, cudaStream_t st,
                        const uint64_t* list = nullptr);
@@ -23,6 +23,7 @@ void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64
 
 void debug_set_leaf_stop(int v);
 void debug_set_leaf_variant(int v);
+void debug_set_leaf_fallback(int v);
 void debug_set_seg_variant(int v);
 bool merge_tree_active();
 void debug_set_tree_force_direct(int v);

@@ -321,3 +321,31 @@ def test_merge_shuffle_multi_single_process(world, n, dt):
     ref, rbits = O.merge_shuffle_perm(n, cutoff, seed)
     assert bits == rbits
     assert np.array_equal(torch.cat(shards).cpu().numpy().astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("variant", ["v3", "halves", "reg", "fallback"])
+def test_leaf_apply_variants(variant):
+    # leaves of 8193..65536 elements: the one-pass byte-counter kernel (v3,
+    # default), the target-halves kernel, the register kernel, and v3's serial
+    # fallback (counter overflow, forced for every leaf): same permutations
+    import ctypes
+    from paper_1508_03167_b200 import _lib
+    lib = _lib.load()
+    lib.sk_debug_set.argtypes = [ctypes.c_int, ctypes.c_int]
+    knobs = {"v3": [(5, 2)], "halves": [(5, 1)], "reg": [(5, 0)], "fallback": [(5, 2), (6, 1)]}[variant]
+    for k, v in knobs:
+        lib.sk_debug_set(k, v)
+    try:
+        cases = [(1 << 20, 65536, 0), (1_000_000, 65536, 7), (300_007, 16384, 1234), (65536, 65536, 5),
+                 (65535, 65536, 6), (40_000, 10_000, 8), (8193 * 2, 8193, 9)]
+        if variant == "fallback":
+            cases = cases[2:]
+        for n, cutoff, seed in cases:
+            for dt in (torch.int32, torch.int64):
+                x, rep = gpu_perm(n, cutoff, seed, dt)
+                ref, rbits = O.merge_shuffle_perm(n, cutoff, seed)
+                assert rep.bits == rbits
+                assert np.array_equal(x.cpu().numpy().astype(np.int64), ref), (n, cutoff, seed, dt)
+    finally:
+        lib.sk_debug_set(5, 2)
+        lib.sk_debug_set(6, 0)
