@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
   constexpr uint32_t GPT = 4096 / BLOCK;   // groups of 16 targets per thread (phase 2)
   extern __shared__ __align__(16) uint32_t sh[];
   __shared__ uint32_t wsum[BLOCK / 32];
-  __shared__ uint32_t s_nlong, s_bad;
+  __shared__ uint32_t s_nlong, s_nhuge, s_bad;
   __shared__ __align__(8) uint64_t s_bar;
   uint32_t s_phase = 0;
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
@@ -690,6 +690,7 @@ __global__ void __launch_bounds__(BLOCK, 1)
     for (uint32_t w = tid; w < (nw >> 2); w += BLOCK) reinterpret_cast<uint4*>(cnt)[w] = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
       s_nlong = 0;
+      s_nhuge = 0;
       s_bad = g_leaf_force_fallback;
     }
     // r[i]: steps 2P and 2P+1 of pair P = tid + 1024 i (low / high half-word)
@@ -821,7 +822,9 @@ __global__ void __launch_bounds__(BLOCK, 1)
         const uint32_t v0 = k >= 1 ? (uint32_t)bkt[st] : 0u;
         const uint32_t v1 = k >= 2 ? (uint32_t)bkt[st + 1] : 0u;
         uint32_t H = 0;
-        if (k >= 3) {
+        if (k >= 9) {  // queued from the top of the list area
+          lst[mr - 1 - atomicAdd(&s_nhuge, 1u)] = (uint16_t)p;
+        } else if (k >= 3) {
           lst[atomicAdd(&s_nlong, 1u)] = (uint16_t)p;
         } else if (k == 1) {
           bkt[st] = (uint16_t)p;
@@ -838,8 +841,9 @@ __global__ void __launch_bounds__(BLOCK, 1)
     }
     __syncthreads();
     if (g_leaf_stop <= 4) continue;
-    // 5. queued buckets (>= 3 steps): keys (step << 16 | slot) through a sorting
-    //    network; the entry at sorted position a gets the step at a + 1
+    // 5. queued buckets of 3..8 steps, one per thread: keys (step << 16 | slot)
+    //    through a sorting network; the entry at sorted position a gets the
+    //    step at a + 1 (or the target itself at the end)
     for (uint32_t i = tid; i < s_nlong; i += BLOCK) {
       const uint32_t p = lst[i];
       const uint32_t w = p >> 2, q = p & 3;
@@ -847,20 +851,42 @@ __global__ void __launch_bounds__(BLOCK, 1)
       const uint32_t en = (cw >> (8 * q)) & 0xFFu;
       const uint32_t sn = q ? ((cw >> (8 * (q - 1))) & 0xFFu) : ((w & 3) ? (cnt[w - 1] >> 24) : 0u);
       const uint32_t k = en - sn, st = (uint32_t)gst[w >> 2] + sn;
-      uint32_t H;
-      if (k <= 8) {
-        uint32_t key[8];
+      uint32_t key[8];
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
-          key[a] = (uint32_t)a < k ? (((uint32_t)bkt[st + a] << 16) | (st + a)) : 0xFFFFFFFFu;
-        sort_net8(key);
+      for (int a = 0; a < 8; ++a)
+        key[a] = (uint32_t)a < k ? (((uint32_t)bkt[st + a] << 16) | (st + a)) : 0xFFFFFFFFu;
+      sort_net8(key);
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
-          if ((uint32_t)a < k)
-            bkt[key[a] & 0xFFFFu] = (uint16_t)((uint32_t)(a + 1) < k ? (key[a < 7 ? a + 1 : 7] >> 16) : p);
-        H = (key[0] >> 16) > p ? (key[0] >> 16) : (key[1] >> 16);
-      } else {  // the first few targets only: O(k^2) through the scratch
-        H = 0x10000u;
+      for (int a = 0; a < 8; ++a)
+        if ((uint32_t)a < k)
+          bkt[key[a] & 0xFFFFu] = (uint16_t)((uint32_t)(a + 1) < k ? (key[a < 7 ? a + 1 : 7] >> 16) : p);
+      Hg[p] = (uint16_t)((key[0] >> 16) > p ? (key[0] >> 16) : (key[1] >> 16));
+    }
+    //    buckets of >= 9 steps (the first few hundred targets), one per warp:
+    //    a warp bitonic sort of the keys (<= 32 entries)
+    for (uint32_t i = wid; i < s_nhuge; i += BLOCK / 32) {
+      const uint32_t p = lst[mr - 1 - i];
+      const uint32_t w = p >> 2, q = p & 3;
+      const uint32_t cw = cnt[w];
+      const uint32_t en = (cw >> (8 * q)) & 0xFFu;
+      const uint32_t sn = q ? ((cw >> (8 * (q - 1))) & 0xFFu) : ((w & 3) ? (cnt[w - 1] >> 24) : 0u);
+      const uint32_t k = en - sn, st = (uint32_t)gst[w >> 2] + sn;
+      if (k <= 32 && g_leaf_stop != 12) {  // (12: timing/test knob, all through the O(k^2) path)
+        uint32_t key = lane < k ? (((uint32_t)bkt[st + lane] << 16) | (st + lane)) : 0xFFFFFFFFu;
+#pragma unroll
+        for (uint32_t kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+          for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, key, jj);
+            const bool up = (lane & kk) == 0, low = (lane & jj) == 0;
+            key = (low == up) ? min(key, o) : max(key, o);
+          }
+        const uint32_t nxt = __shfl_down_sync(0xffffffffu, key, 1);
+        const uint32_t k1 = __shfl_sync(0xffffffffu, key, 1);
+        if (lane < k) bkt[key & 0xFFFFu] = (uint16_t)(lane + 1 < k ? (nxt >> 16) : p);
+        if (lane == 0) Hg[p] = (uint16_t)((key >> 16) > p ? (key >> 16) : (k1 >> 16));
+      } else if (lane == 0) {  // > 32 steps on one target: O(k^2) through the scratch
+        uint32_t H = 0x10000u;
         for (uint32_t a = 0; a < k; ++a) {
           const uint32_t va = bkt[st + a];
           uint32_t best = 0x10000u;
@@ -872,9 +898,9 @@ __global__ void __launch_bounds__(BLOCK, 1)
           H = (va > p && va < H) ? va : H;
         }
         for (uint32_t a = 0; a < k; ++a) bkt[st + a] = tmp[st + a];
-        H &= 0xFFFFu;
+        Hg[p] = (uint16_t)(H & 0xFFFFu);
       }
-      Hg[p] = (uint16_t)H;
+      __syncwarp();
     }
     __syncthreads();
     if (g_leaf_stop <= 5) continue;
