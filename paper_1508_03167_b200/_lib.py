@@ -10,7 +10,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libshufflekit_b200.so")
+# SK_LIB_PATH: load another build of the same library (performance experiments)
+SO_PATH = os.environ.get("SK_LIB_PATH") or os.path.join(_HERE, "libshufflekit_b200.so")
 _lock = threading.Lock()
 _lib = None
 

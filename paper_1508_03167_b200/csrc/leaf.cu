@@ -143,6 +143,109 @@ __global__ void __launch_bounds__(kDecodeBlock) leaf_decode16_kernel(ArrayJob J,
   }
 }
 
+// Leaner decode (same draws, same bit accounting): the step index i drives
+// everything -- the store address (dr + i), the flush condition ((lo + i) % 8
+// == 0), the head test (i > ih: draws whose 16-byte chunk reaches past the
+// leaf's last draw go out as single 16-bit stores) -- instead of a running
+// 64-bit pointer, the 8-draw shift register is four 32-bit words advanced by
+// byte permutes, and the FDR bit extraction is two funnel shifts.
+static int g_decode_variant = 1;  // 1 = leaf_decode16b_kernel, 0 = leaf_decode16_kernel
+
+template <bool FRESH>
+__global__ void __launch_bounds__(kDecodeBlock) leaf_decode16b_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
+                                                                      uint16_t* __restrict__ draws,
+                                                                      unsigned long long* __restrict__ bits) {
+  __shared__ uint32_t ring[16][kDecodeBlock];
+  const uint32_t lane = threadIdx.x;
+  const uint64_t g = (uint64_t)blockIdx.x * kDecodeBlock + lane;
+  LeafDesc L;
+  uint32_t m = 0;
+  if (g < nleaves) {
+    L = leaf_desc(J, E, g);
+    m = (uint32_t)(L.hi - L.lo);
+  } else {
+    L.lo = 0; L.hi = 0; L.array = 0; L.sd = fresh_stream(0);
+  }
+  uint32_t i = m >= 2 ? m - 1 : 0;  // current step; its bound is i + 1
+  uint16_t* const dr = draws + L.lo;
+  const uint32_t al = (uint32_t)(L.lo & 7);
+  // draws i > ih are stored singly; chunks [i, i+7] with (lo + i) % 8 == 0 and i <= ih - 7 are flushed
+  const int32_t ih = (int32_t)m - 1 - (int32_t)((al + m) & 7);
+  uint64_t gw = 0;
+  uint32_t wr = 0;
+  if (i) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      uint64_t x = leaf_word<FRESH>(L.sd, gw++);
+      ring[wr & 15][lane] = (uint32_t)(x >> 32);
+      ring[(wr + 1) & 15][lane] = (uint32_t)x;
+      wr += 2;
+    }
+  }
+  uint32_t A = ring[0][lane], B = ring[1][lane], C = ring[2][lane], D = ring[3][lane];
+  uint32_t rd = 4;
+  uint32_t pos = 0;
+  uint32_t v = 1, c = 0;
+  uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;  // last 8 packed draws, newest in w0's low half
+  while (__any_sync(0xffffffffu, i != 0)) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (i != 0 && wr - rd <= 14) {
+        uint64_t x = leaf_word<FRESH>(L.sd, gw++);
+        ring[wr & 15][lane] = (uint32_t)(x >> 32);
+        ring[(wr + 1) & 15][lane] = (uint32_t)x;
+        wr += 2;
+      }
+    }
+#pragma unroll 4
+    for (int tr = 0; tr < kDecodeTrips; ++tr) {
+      const bool act = i != 0;
+      const uint32_t b = i + 1;
+      uint32_t k = __clz(v) - __clz(b);  // smallest k with v << k >= b
+      k += ((v << k) < b) ? 1u : 0u;
+      const uint32_t x = __funnelshift_l(B, A, pos);
+      const uint32_t cc = __funnelshift_l(x, c, k);  // (c << k) | top k bits of x
+      const bool acc = act && cc < b;
+      const bool single = acc && (int32_t)i > ih;
+      const bool push = acc && (int32_t)i <= ih;
+      uint16_t* const a = dr + i;
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.global.u16 [%1], %2;\n}" ::"r"(
+                       single ? 1u : 0u),
+                   "l"(a), "h"((unsigned short)cc));
+      if (push) {
+        w3 = __byte_perm(w2, w3, 0x5432);
+        w2 = __byte_perm(w1, w2, 0x5432);
+        w1 = __byte_perm(w0, w1, 0x5432);
+        w0 = __byte_perm(cc, w0, 0x5410);
+      }
+      const bool fl = push && ((al + i) & 7) == 0;
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.global.v4.u32 [%1], {%2, %3, %4, %5};\n}" ::"r"(
+                       fl ? 1u : 0u),
+                   "l"(a), "r"(w0), "r"(w1), "r"(w2), "r"(w3));
+      c = acc ? 0u : cc - b;
+      v = acc ? 1u : (v << k) - b;
+      i -= acc ? 1u : 0u;
+      pos += act ? k : 0u;
+      const bool cross = pos >= 32;
+      const uint32_t nxt = ring[rd & 15][lane];
+      pos = cross ? pos - 32 : pos;
+      A = cross ? B : A;
+      B = cross ? C : B;
+      C = cross ? D : C;
+      D = cross ? nxt : D;
+      rd += cross ? 1u : 0u;
+    }
+  }
+  if (m >= 2) {
+    // the pending (< 8) packed draws: dr[1 ..], draw 1 in w0's low half
+    const uint32_t f = 8 - ((al + 1) & 7) == 8 ? 1u : 8 - ((al + 1) & 7) + 1;  // first flush point >= 1
+    const uint32_t pend = (ih >= 8 && (int32_t)f + 7 <= ih) ? f - 1 : (ih > 0 ? (uint32_t)ih : 0u);
+    const uint32_t wv[4] = {w0, w1, w2, w3};
+    for (uint32_t k = 0; k < pend; ++k) dr[1 + k] = (uint16_t)(wv[k >> 1] >> (16 * (k & 1)));
+    atomicAdd(&bits[L.array], 32ull * (rd - 4) + pos);  // bits consumed = halves passed + pos
+  }
+}
+
 // Warp-segmented exclusive scan over `m` 16-bit counters packed in smem.
 // Each warp owns [w*S, (w+1)*S); lanes walk it 32 entries per round.
 __device__ __forceinline__ void scan_counts16(uint16_t* c16, uint32_t m, uint32_t* warp_tot) {
@@ -1010,6 +1113,7 @@ void debug_set_leaf_variant(int v) {
   if (v >= 10) g_leaf_v3_block = v == 10 ? 512 : 1024;
   else g_leaf_variant = v;
 }
+void debug_set_decode_variant(int v) { g_decode_variant = v; }
 void debug_set_leaf_fallback(int v) { cudaMemcpyToSymbol(g_leaf_force_fallback, &v, sizeof(int)); }
 void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int)); }
 
@@ -1017,10 +1121,14 @@ void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nle
                           unsigned long long* bits, cudaStream_t st) {
   if (!nleaves) return;
   unsigned blocks = (unsigned)((nleaves + kDecodeBlock - 1) / kDecodeBlock);
-  if (E.active && E.sd.plen != 0)
-    leaf_decode16_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
-  else
-    leaf_decode16_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
+  const bool fresh = !(E.active && E.sd.plen != 0);
+  if (g_decode_variant == 1) {
+    if (fresh) leaf_decode16b_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
+    else leaf_decode16b_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
+  } else {
+    if (fresh) leaf_decode16_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
+    else leaf_decode16_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
+  }
   count_launch();
 }
 

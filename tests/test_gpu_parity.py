@@ -323,7 +323,7 @@ def test_merge_shuffle_multi_single_process(world, n, dt):
     assert np.array_equal(torch.cat(shards).cpu().numpy().astype(np.int64), ref)
 
 
-@pytest.mark.parametrize("variant", ["v3", "halves", "reg", "fallback", "quadratic"])
+@pytest.mark.parametrize("variant", ["v3", "halves", "reg", "fallback", "quadratic", "decode0"])
 def test_leaf_apply_variants(variant):
     # leaves of 8193..65536 elements: the one-pass byte-counter kernel (v3,
     # default), the target-halves kernel, the register kernel, and v3's serial
@@ -334,7 +334,7 @@ def test_leaf_apply_variants(variant):
     lib.sk_debug_set.argtypes = [ctypes.c_int, ctypes.c_int]
     # quadratic: v3 with every bucket of >= 9 steps through the O(k^2) path
     knobs = {"v3": [(5, 2)], "halves": [(5, 1)], "reg": [(5, 0)], "fallback": [(5, 2), (6, 1)],
-             "quadratic": [(5, 2), (1, 12)]}[variant]
+             "quadratic": [(5, 2), (1, 12)], "decode0": [(7, 0)]}[variant]
     for k, v in knobs:
         lib.sk_debug_set(k, v)
     try:
@@ -352,3 +352,4 @@ def test_leaf_apply_variants(variant):
         lib.sk_debug_set(5, 2)
         lib.sk_debug_set(6, 0)
         lib.sk_debug_set(1, 99)
+        lib.sk_debug_set(7, 1)
