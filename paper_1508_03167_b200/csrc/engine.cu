@@ -139,6 +139,7 @@ struct LevelBufs {
   uint32_t tpp = 1;                          // tree tiles per pair
   // tails
   uint64_t total = 0;
+  std::vector<uint64_t> tail_prefix;         // host: first tail record of pair g (g = 0..npairs)
   uint64_t* rec_key = nullptr;
   uint32_t* rec_pair = nullptr;
   uint64_t* skey = nullptr;
@@ -151,6 +152,28 @@ struct LevelBufs {
   void* tmp = nullptr;
   cudaEvent_t ev_tail{};
 };
+
+__global__ void tail_len_kernel(const PairPlan* __restrict__ plans, uint64_t n, uint64_t* __restrict__ out) {
+  uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < n) out[g] = plans[g].tail_len;
+}
+
+// Small host->device uploads as kernel parameters (no copy engine).
+struct PokeBuf {
+  unsigned char b[2048];
+};
+__global__ void poke_kernel(unsigned char* dst, PokeBuf p, uint32_t n) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = p.b[i];
+}
+static void poke(void* dst, const void* src, size_t n, cudaStream_t st) {
+  for (size_t o = 0; o < n; o += sizeof(PokeBuf)) {
+    PokeBuf p;
+    const size_t k = std::min(sizeof(PokeBuf), n - o);
+    memcpy(p.b, (const unsigned char*)src + o, k);
+    poke_kernel<<<1, 256, 0, st>>>((unsigned char*)dst + o, p, (uint32_t)k);
+    count_launch();
+  }
+}
 
 __global__ void set_tail_off_kernel(PairPlan* plans, const uint64_t* offs, uint64_t n) {
   uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -210,17 +233,30 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
   std::vector<uint64_t> offs(tot_pairs);
   for (int i = 0; i < nl; ++i) {
     uint64_t acc = 0;
+    lv[i].tail_prefix.resize(lv[i].npairs + 1);
     for (uint64_t g = 0; g < lv[i].npairs; ++g) {
       offs[pprefix[i] + g] = acc;
+      lv[i].tail_prefix[g] = acc;
       acc += hplans[pprefix[i] + g].tail_len;
     }
+    lv[i].tail_prefix[lv[i].npairs] = acc;
     lv[i].total = acc;
   }
+  // (no host->device copies here: on the host entry they would queue behind
+  // the big H2D transfer on the copy engine.  The tail offsets are scanned on
+  // the device; the small level tables go up as kernel parameters.)
   uint64_t* d_offs = A.alloc<uint64_t>(tot_pairs, ps);
-  CK(cudaMemcpyAsync(d_offs, offs.data(), tot_pairs * 8, cudaMemcpyHostToDevice, ps));
   std::vector<LevelTail> ht(nl);
   for (int i = 0; i < nl; ++i) {
     auto& L = lv[i];
+    uint64_t* lens = A.alloc<uint64_t>(L.npairs, ps);
+    tail_len_kernel<<<(unsigned)((L.npairs + 255) / 256), 256, 0, ps>>>(L.plans, L.npairs, lens);
+    count_launch();
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, lens, d_offs + pprefix[i], (int)L.npairs, ps));
+    void* ts = A.alloc<unsigned char>(tb, ps);
+    CK(cub::DeviceScan::ExclusiveSum(ts, tb, lens, d_offs + pprefix[i], (int)L.npairs, ps));
+    count_launch();
     set_tail_off_kernel<<<(unsigned)((L.npairs + 255) / 256), 256, 0, ps>>>(L.plans, d_offs + pprefix[i], L.npairs);
     count_launch();
     L.rec_key = A.alloc<uint64_t>(L.total, ps);
@@ -229,8 +265,8 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
   }
   LevelTail* d_lt = A.alloc<LevelTail>(nl, ps);
   uint64_t* d_pp = A.alloc<uint64_t>(nl + 1, ps);
-  CK(cudaMemcpyAsync(d_lt, ht.data(), nl * sizeof(LevelTail), cudaMemcpyHostToDevice, ps));
-  CK(cudaMemcpyAsync(d_pp, pprefix.data(), (nl + 1) * 8, cudaMemcpyHostToDevice, ps));
+  poke(d_lt, ht.data(), nl * sizeof(LevelTail), ps);
+  poke(d_pp, pprefix.data(), (nl + 1) * 8, ps);
   launch_tail_decode(d_lt, nl, d_pp, tot_pairs, d_bits, ps);
   // per round: sort tail targets, build (dst, src)
   uint64_t nbits_key = 1;
@@ -288,9 +324,22 @@ static cudaStream_t side_stream() {
 // and only the last round writes `other` (plus the untouched [X, N) regions).
 // The segment-pass debug kernels park elements in their input and need the
 // ping-pong.  Returns the buffer holding the result.
-static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* other, cudaStream_t st) {
+// Pairs [p0, p1) of one round, in place (tree merge), with their tail insertions.
+static void run_round_range(LevelBufs& L, int eb, void* buf, uint64_t p0, uint64_t p1, cudaStream_t st) {
+  {
+    StageTimer tm(2, st);
+    launch_merge_tree_range(eb, buf, buf, L.plans, p0, p1, L.rank, L.chains, L.tpp, st);
+  }
+  StageTimer tm(3, st);
+  CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
+  const uint64_t s0 = 2 * L.tail_prefix[p0], s1 = 2 * L.tail_prefix[p1];
+  launch_tail_apply(eb, buf, L.dst + s0, L.src + s0, (unsigned char*)L.tmp + s0 * eb, s1 - s0, st);
+}
+
+static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* other, cudaStream_t st,
+                        size_t first = 0) {
   const bool in_place = merge_tree_active();
-  for (size_t r = 0; r < lv.size(); ++r) {
+  for (size_t r = first; r < lv.size(); ++r) {
     auto& L = lv[r];
     const bool last = r + 1 == lv.size();
     void* out = (in_place && !last) ? cur : other;
@@ -397,6 +446,11 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
   A.release(st);
 }
 
+static cudaStream_t round_stream() {
+  static thread_local SideStream rs;
+  return rs.s;
+}
+
 static cudaStream_t copy_stream() {
   static thread_local SideStream cs;
   return cs.s;
@@ -404,9 +458,12 @@ static cudaStream_t copy_stream() {
 
 // The host entry for big arrays: the H2D copy runs in 2^k chunks on a copy
 // stream; the leaf draws (no data needed) and the merge plans are prepared
-// meanwhile, and chunk j's leaves are applied as soon as chunk j has landed,
-// so the leaf stage hides under the transfer.  Then the merge rounds, then
-// the D2H copy.  Same result as copy + sk_merge_shuffle_parallel + copy.
+// meanwhile, chunk j's leaves are applied as soon as chunk j has landed, and
+// its local rounds (1 .. c-k: pairs inside the chunk) follow on a round
+// stream, so everything but the top k rounds hides under the transfer.  Then
+// the top rounds, then the D2H copy.  Same result as copy +
+// sk_merge_shuffle_parallel + copy.  (build_plans makes no host->device
+// copies: on this path they would queue behind the big H2D on the copy engine.)
 static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned long long* d_bits, cudaStream_t st) {
   const uint64_t n = J.len;
   const int c = J.c;
@@ -436,6 +493,12 @@ static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned 
       StageTimer tm(0, st);
       launch_leaf_decode16(J, E0, nleaves, draws, d_bits, st);  // needs no data
     }
+    // leaves per chunk as it lands (on st), then the plans (host-blocking on
+    // the side stream), then each chunk's local rounds -- rounds 1 .. c-k
+    // merge pairs inside one chunk -- on the round stream, in place on the
+    // scratch, after that chunk's leaves (the tree merge runs in place; the
+    // debug segment-pass kernels do not)
+    std::vector<cudaEvent_t> evl(K, nullptr);
     for (uint64_t j = 0; j < K; ++j) {
       const uint64_t lo = bound_at(n, j * B, c);
       CK(cudaStreamWaitEvent(st, ev[j], 0));
@@ -443,11 +506,26 @@ static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned 
       Jj.blk0 = j * B;
       Jj.lognblk = c - k;
       Jj.elem0 = lo;
-      StageTimer tm(1, st);
-      launch_leaf_apply(eb, Jj, E0, B, dev + lo * eb, scr + lo * eb, draws + lo, lscr, mmax, grid, st);
+      {
+        StageTimer tm(1, st);
+        launch_leaf_apply(eb, Jj, E0, B, dev + lo * eb, scr + lo * eb, draws + lo, lscr, mmax, grid, st);
+      }
+      CK(cudaEventCreateWithFlags(&evl[j], cudaEventDisableTiming));
+      CK(cudaEventRecord(evl[j], st));
     }
     build_plans(lv, eb, d_bits, A, ps, st);
-    void* res = run_rounds(lv, eb, scr, dev, st);
+    const size_t nloc = merge_tree_active() ? (size_t)std::max(0, std::min((int)lv.size() - 1, c - k)) : 0;
+    cudaStream_t rs = round_stream();  // ordered after st by the per-chunk events only
+    for (uint64_t j = 0; j < K; ++j) {
+      CK(cudaStreamWaitEvent(rs, evl[j], 0));
+      for (size_t r = 0; r < nloc; ++r) {
+        const uint64_t pp = B >> (r + 1);  // pairs of round r+1 per chunk
+        run_round_range(lv[r], eb, scr, j * pp, (j + 1) * pp, rs);
+      }
+    }
+    for (auto e : evl) cudaEventDestroy(e);
+    fork_side(rs, st);  // st after the local rounds
+    void* res = run_rounds(lv, eb, scr, dev, st, nloc);
     if (res != dev) CK(cudaMemcpyAsync(dev, res, n * eb, cudaMemcpyDeviceToDevice, st));
     CK(cudaEventCreateWithFlags(&ev[K], cudaEventDisableTiming));
     CK(cudaEventRecord(ev[K], st));

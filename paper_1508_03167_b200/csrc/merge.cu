@@ -1099,6 +1099,13 @@ static void merge_tree_t(void* in, void* out, const PairPlan* plans, uint64_t np
   count_launch();
 }
 
+// Pairs [p0, p1) of a round only (the host entry's chunk-local rounds).
+void launch_merge_tree_range(int eb, void* in, void* out, const PairPlan* plans, uint64_t p0, uint64_t p1,
+                             const uint64_t* rank, const uint64_t* chains, uint32_t tpp, cudaStream_t st) {
+  if (p1 <= p0) return;
+  launch_merge_tree(eb, in, out, plans + p0, p1 - p0, rank, chains + p0 * (tpp + 1) * kTreeD, tpp, st);
+}
+
 void launch_merge_tree(int eb, void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
                        const uint64_t* chains, uint32_t tpp, cudaStream_t st) {
   if (!npairs) return;

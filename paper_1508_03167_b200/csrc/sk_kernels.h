@@ -57,6 +57,8 @@ uint32_t tree_tiles_per_pair(const LevelJob& LJ, int eb);
 uint64_t tree_chain_words(uint64_t npairs, uint32_t tpp);
 void launch_tree_chains(int eb, const PairPlan* plans, uint64_t npairs, const uint64_t* rank, uint32_t tpp,
                         uint64_t* chains, cudaStream_t st);
+void launch_merge_tree_range(int eb, void* in, void* out, const PairPlan* plans, uint64_t p0, uint64_t p1,
+                             const uint64_t* rank, const uint64_t* chains, uint32_t tpp, cudaStream_t st);
 void launch_merge_tree(int eb, void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
                        const uint64_t* chains, uint32_t tpp, cudaStream_t st);
 void launch_copy_tail_region(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs,

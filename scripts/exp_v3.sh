@@ -1,4 +1,2 @@
-python scripts/prof_run.py 30 3 --check
-for v in scat8 quad4; do SK_LIB_PATH=build/variants/$v.so python scripts/prof_run.py 30 3 --check; done
-for v in scat8 quad4; do SK_LIB_PATH=build/variants/$v.so python scripts/prof_run.py 30 3 1=4; done
-python scripts/prof_run.py 30 3 1=4
+python -m pytest tests/test_gpu_parity.py -q -x -k "host_entry or numpy_host or config1" 2>&1 | tail -2
+python bench.py --steps 3 --no-cpu-baseline --e2e-steps 3 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e'], d['roofline']['stage_ms_per_step'])"
