@@ -8,7 +8,7 @@ bit-exact with the reference) of the resident 4 GiB array.  Timing: CUDA
 events on the launching stream, barrier + synchronize on both sides, max over
 ranks.  The array (4 GiB) is 32x the L2, so no flush is needed between steps.
 
-Extra keys: roofline (dominant kernel = one merge round, segment-pass kernels),
+Extra keys: roofline (dominant kernel = one merge round: merge_tree_kernel),
 cpu_baseline (the C oracle port on the host cores, bounded sample), e2e
 (through the C ABI host entry with pinned host buffers, H2D+D2H inside the
 timed region), gpu_launches, clocks.
