@@ -30,12 +30,13 @@ def main():
         k, v = kv.split("=")
         assert lib.sk_debug_set(int(k), int(v)) == 0, kv
     n = 1 << log2n
-    x = torch.arange(n, dtype=torch.int32, device="cuda")
+    eb = 8 if "--u64" in sys.argv else 4
+    x = torch.arange(n, dtype=torch.int64 if eb == 8 else torch.int32, device="cuda")
     st = torch.cuda.current_stream()
     sp = ctypes.c_void_p(st.cuda_stream)
     bits = ctypes.c_uint64(0)
     for _ in range(2):
-        _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), 4, n, 65536, 0, ctypes.byref(bits), sp))
+        _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), eb, n, 65536, 0, ctypes.byref(bits), sp))
     torch.cuda.synchronize()
     ok = None
     if "--check" in sys.argv and log2n in BITS:
@@ -44,14 +45,14 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for _ in range(steps):
-        _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), 4, n, 65536, 0, None, sp))
+        _lib.check(lib.sk_merge_shuffle_parallel(ctypes.c_void_p(x.data_ptr()), eb, n, 65536, 0, None, sp))
     e1.record(st)
     torch.cuda.synchronize()
     sm = (ctypes.c_double * 5)()
     lib.sk_profile_read(sm, None, 5)
     lib.sk_profile_enable(0)
     names = ["leaf_decode", "leaf_apply", "merge_rounds", "identity+tail", "final_copy"]
-    print(json.dumps({"log2n": log2n, "knobs": knobs, "ms_per_step": round(e0.elapsed_time(e1) / steps, 3),
+    print(json.dumps({"log2n": log2n, "eb": eb, "knobs": knobs, "ms_per_step": round(e0.elapsed_time(e1) / steps, 3),
                       "stages": {k: round(sm[i] / steps, 3) for i, k in enumerate(names)}, "bits_ok": ok}))
 
 
