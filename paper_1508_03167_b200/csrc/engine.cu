@@ -397,7 +397,7 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
     bool fast_leaf = mmax <= 65536;
     if (fast_leaf) {
       draws = A.alloc<uint16_t>(ntot, st);
-      grid = leaf_apply_grid(nleaves, (uint32_t)mmax, num_sms());
+      grid = leaf_apply_grid(nleaves, (uint32_t)mmax, num_sms(), eb);
       lscr = A.alloc<uint16_t>((uint64_t)grid * leaf_scratch_stride(mmax) + 8, st);
     }
     fork_side(st, ps);
@@ -476,7 +476,7 @@ static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned 
   uint16_t* draws = A.alloc<uint16_t>(n, st);
   const uint64_t nleaves = J.q, K = 1ull << k, B = nleaves >> k;
   const uint32_t mmax = (uint32_t)((n + J.q - 1) >> c);
-  const uint32_t grid = leaf_apply_grid(B, mmax, num_sms());
+  const uint32_t grid = leaf_apply_grid(B, mmax, num_sms(), eb);
   uint16_t* lscr = A.alloc<uint16_t>((uint64_t)grid * leaf_scratch_stride(mmax) + 8, st);
   std::vector<cudaEvent_t> ev(K + 1, nullptr);
   ExplicitTask E0{};
@@ -766,7 +766,7 @@ static uint64_t run_rs_tasks(int eb, void* buf0, void* buf1, const std::vector<R
     if (!cnt) continue;
     uint64_t* dl = A.alloc<uint64_t>(lst[par].size(), st);
     CK(cudaMemcpyAsync(dl, lst[par].data(), lst[par].size() * 8, cudaMemcpyHostToDevice, st));
-    const uint32_t grid = leaf_apply_grid(cnt, mmax[par], num_sms());
+    const uint32_t grid = leaf_apply_grid(cnt, mmax[par], num_sms(), eb);
     uint16_t* lscr = A.alloc<uint16_t>((uint64_t)grid * leaf_scratch_stride(mmax[par]) + 8, st);
     launch_leaf_apply(eb, J0, E0, cnt, par ? buf1 : buf0, par ? buf0 : buf1, draws, lscr, mmax[par], grid, st, dl);
   }

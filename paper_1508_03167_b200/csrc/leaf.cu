@@ -733,13 +733,17 @@ __device__ __forceinline__ void sort_net16(uint32_t* k) {
           if ((i + j) / (2 * p) == (i + j + q) / (2 * p) && i + j + q < 16) cx(k[i + j], k[i + j + q]);
 }
 
-template <typename V, int BLOCK>
-__global__ void __launch_bounds__(BLOCK, 1)
+// (BLOCK, NP): 1024 threads x 32 step pairs for leaves of 8193..65536, 256 x
+// 16 / 256 x 8 for leaves of <= 8192 / 4096 (several CTAs per SM).  The
+// gather stages `chunk` elements per pass; when one chunk holds the whole
+// leaf every source is read before any output is written, so in == out is
+// allowed (the pure Fisher-Yates jobs run in place).
+template <typename V, int BLOCK, int NP>
+__global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
     leaf_apply_v3_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves, const V* __restrict__ in, V* __restrict__ out,
                          const uint16_t* __restrict__ draws, uint16_t* scratch, uint32_t mmax,
                          const uint64_t* __restrict__ list) {
-  constexpr uint32_t NP = 32768 / BLOCK;   // step pairs per thread
-  constexpr uint32_t GPT = 4096 / BLOCK;   // groups of 16 targets per thread (phase 2)
+  constexpr uint32_t GPT = NP / 8 > 0 ? NP / 8 : 1;  // groups of 16 targets per thread (phase 2)
   extern __shared__ __align__(16) uint32_t sh[];
   __shared__ uint32_t wsum[BLOCK / 32];
   __shared__ uint32_t s_nlong, s_nhuge, s_bad;
@@ -752,7 +756,9 @@ __global__ void __launch_bounds__(BLOCK, 1)
   const uint32_t bkt_w = nwmax + (((nwmax >> 2) + 7) >> 3 << 2);
   uint16_t* bkt = reinterpret_cast<uint16_t*>(sh + bkt_w);
   // the gather stages the leaf's data through the whole allocation in chunks
-  const uint32_t chunk = ((bkt_w * 4 + ((mmax + 7) & ~7u) * 2) / (uint32_t)sizeof(V)) & ~3u;
+  // (leaves of <= 8192: the allocation holds the whole leaf, see leaf_apply_v3_smem)
+  uint32_t chunk = ((bkt_w * 4 + ((mmax + 7) & ~7u) * 2) / (uint32_t)sizeof(V)) & ~3u;
+  if (NP <= 16) chunk = max(chunk, (mmax + 3) & ~3u);
   V* sdata = reinterpret_cast<V*>(sh);
   const uint32_t mr = (mmax + 15) & ~15u;
   uint16_t* Hg = reinterpret_cast<uint16_t*>(
@@ -1139,10 +1145,13 @@ static size_t leaf_apply_smem(uint32_t mmax, int eb = 0) {
   return words * 4;
 }
 
-// v3: byte counters (whole groups of 16 targets), 16-bit group starts, buckets
-static size_t leaf_apply_v3_smem(uint32_t mmax) {
+// v3: byte counters (whole groups of 16 targets), 16-bit group starts,
+// buckets; leaves of <= 8192 also room to stage the whole leaf (one chunk)
+static size_t leaf_apply_v3_smem(uint32_t mmax, int eb) {
   const size_t nw = ((size_t)(mmax + 15) >> 4) << 2;
-  return (nw + ((((nw >> 2) + 7) >> 3) << 2)) * 4 + (size_t)((mmax + 7) & ~7u) * 2;
+  const size_t s = (nw + ((((nw >> 2) + 7) >> 3) << 2)) * 4 + (size_t)((mmax + 7) & ~7u) * 2;
+  if (mmax > 8192) return s;
+  return std::max(s, (size_t)((mmax + 3) & ~3u) * (size_t)eb);
 }
 
 template <typename V>
@@ -1150,14 +1159,23 @@ static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nlea
                          const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid,
                          const uint64_t* list, cudaStream_t st) {
   size_t smem = leaf_apply_smem(mmax, (int)sizeof(V));
-  if (mmax > 8192 && g_leaf_variant == 2 && in != out) {  // v3 assumes distinct buffers
-    smem = leaf_apply_v3_smem(mmax);
-    if (g_leaf_v3_block == 512) {
-      auto k = leaf_apply_v3_kernel<V, 512>;
+  if (g_leaf_variant == 2 && mmax > 2048 && (mmax <= 8192 || in != out)) {
+    // v3 (leaves > 8192 gather in two or more chunks: distinct buffers only)
+    smem = leaf_apply_v3_smem(mmax, (int)sizeof(V));
+    if (mmax <= 4096) {
+      auto k = leaf_apply_v3_kernel<V, 256, 8>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k<<<grid, 256, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
+    } else if (mmax <= 8192) {
+      auto k = leaf_apply_v3_kernel<V, 256, 16>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k<<<grid, 256, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
+    } else if (g_leaf_v3_block == 512) {
+      auto k = leaf_apply_v3_kernel<V, 512, 64>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
     } else {
-      auto k = leaf_apply_v3_kernel<V, 1024>;
+      auto k = leaf_apply_v3_kernel<V, 1024, 32>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k<<<grid, 1024, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
     }
@@ -1187,13 +1205,15 @@ static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nlea
   count_launch();
 }
 
-uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms) {
+uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms, int eb) {
   // Persistent CTAs: as many as fit (the per-CTA scratch is reused per leaf and
   // stays L2-resident).
   size_t smem = leaf_apply_smem(mmax);
   size_t fit = (size_t)(220 * 1024) / (smem + 2048);
   int per_sm = (int)std::max((size_t)1, std::min(fit, (size_t)(mmax > 8192 ? 2 : 8)));
   if (mmax > 8192 && g_leaf_variant == 2) per_sm = 1;  // v3: 1024 threads, ~200 KB
+  if (mmax > 2048 && mmax <= 8192 && g_leaf_variant == 2)  // v3, 256 threads
+    per_sm = (int)std::max((size_t)1, std::min((size_t)4, (size_t)(220 * 1024) / (leaf_apply_v3_smem(mmax, eb) + 2048)));
   if (mmax > 8192 && g_leaf_variant == 0)  // register-resident draws: 512 threads, 1-3 CTAs per SM
     per_sm = mmax <= 16384 ? 2 : 1;
   uint64_t g = (uint64_t)num_sms * per_sm;

@@ -12,7 +12,7 @@ int num_sms();
 // leaf.cu
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
                           unsigned long long* bits, cudaStream_t st);
-uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms);
+uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms, int eb = 8);
 // per-CTA leaf-apply scratch (uint16 elements)
 __host__ __device__ inline uint64_t leaf_scratch_stride(uint64_t mmax) { return 3 * ((mmax + 15) & ~15ULL) + 16; }
 void launch_leaf_apply(int eb, const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, const void* in, void* out,
