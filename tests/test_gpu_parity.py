@@ -294,7 +294,7 @@ def test_merge_fallback_paths(mode):
 
 @pytest.mark.parametrize("n,cutoff,seed,dt", [((1 << 25) + 17, 65536, 3, np.uint32), (1 << 24, 4096, 4, np.int64),
                                               (50_000_001, 65536, 5, np.float32),
-                                              # c = 3 / 4 / 5: no, one, two chunk-local rounds
+                                              # leaves above 65536 elements: the unchunked host path
                                               (1 << 24, 1 << 21, 6, np.uint32), ((1 << 24) + 3, 1 << 20, 7, np.int64),
                                               (1 << 24, 1 << 19, 8, np.uint32)])
 def test_host_entry_pipelined(n, cutoff, seed, dt):
