@@ -187,6 +187,24 @@ def test_full_size_2p30_validity_and_bits():
     del s, seen
 
 
+def test_full_size_2p30_host_entry_equals_device_path():
+    # the pipelined host entry (chunked H2D, per-chunk leaves and local rounds
+    # on two streams, top rounds, D2H) at n = 2^30: same bits and the same
+    # permutation as the device-resident path
+    n = 1 << 30
+    x = torch.arange(n, dtype=torch.int32, device="cuda")
+    rep = sk.merge_shuffle_parallel(x, sk.ShuffleConfig(), sk.BitSource(0))
+    host = torch.arange(n, dtype=torch.int32).pin_memory()
+    import ctypes
+    from paper_1508_03167_b200 import _lib
+    bits = ctypes.c_uint64(0)
+    _lib.check(_lib.load().sk_merge_shuffle_parallel_host(ctypes.c_void_p(host.data_ptr()), 4, n, 65536, 0,
+                                                          ctypes.byref(bits),
+                                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    assert bits.value == rep.bits == 31908987766
+    assert torch.equal(host.to("cuda"), x)
+
+
 def test_determinism_and_seed_sensitivity():
     a, _ = gpu_perm(300_000, 1000, 5, torch.int32)
     b, _ = gpu_perm(300_000, 1000, 5, torch.int32)
