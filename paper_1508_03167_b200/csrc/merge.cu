@@ -958,7 +958,9 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const uint32_t G = 2 * tid + e;
-    if (G < ngroups) gdesc[G] = make_uint4(mm[e], gy[e], gz[e] + (e ? ex1 : ex0), 0u);
+    // (stage offsets in bytes: the swap loop adds them straight to the shared base)
+    if (G < ngroups)
+      gdesc[G] = make_uint4(mm[e], gy[e] * (uint32_t)sizeof(V), (gz[e] + (e ? ex1 : ex0)) * (uint32_t)sizeof(V), 0u);
   }
   __syncthreads();
   mbar_wait(&bar, 0);
@@ -966,6 +968,10 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
   //    shrink (|window h+1| = ones of window h); from the first window of at
   //    most 64 positions on, warp 0 finishes alone with warp barriers.
   const uint32_t ltmask = ~(0xffffffffu >> lane);
+  constexpr uint32_t kSh = sizeof(V) == 4 ? 2u : 3u;
+  const uint32_t lb = lane << kSh;
+  char* const sb = reinterpret_cast<char*>(stage);
+  auto at = [&](uint32_t off) -> V& { return *reinterpret_cast<V*>(sb + off); };
   int h = 0;
   constexpr uint32_t NWp = kTreeBlock / 32;
   for (; h + 1 < nw && goff[h + 1] - goff[h] > 2; ++h) {
@@ -975,21 +981,21 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
     for (; G + NWp < g1; G += 2 * NWp) {
       const uint4 d0 = gdesc[G], d1 = gdesc[G + NWp];
       const bool on0 = (d0.x << lane) >> 31, on1 = (d1.x << lane) >> 31;
-      const uint32_t ia0 = d0.y + lane, ib0 = d0.z + __popc(d0.x & ltmask);
-      const uint32_t ia1 = d1.y + lane, ib1 = d1.z + __popc(d1.x & ltmask);
+      const uint32_t ia0 = d0.y + lb, ib0 = d0.z + (__popc(d0.x & ltmask) << kSh);
+      const uint32_t ia1 = d1.y + lb, ib1 = d1.z + (__popc(d1.x & ltmask) << kSh);
       V va0, vb0, va1, vb1;
-      if (on0) { va0 = stage[ia0]; vb0 = stage[ib0]; }
-      if (on1) { va1 = stage[ia1]; vb1 = stage[ib1]; }
-      if (on0) { stage[ia0] = vb0; stage[ib0] = va0; }
-      if (on1) { stage[ia1] = vb1; stage[ib1] = va1; }
+      if (on0) { va0 = at(ia0); vb0 = at(ib0); }
+      if (on1) { va1 = at(ia1); vb1 = at(ib1); }
+      if (on0) { at(ia0) = vb0; at(ib0) = va0; }
+      if (on1) { at(ia1) = vb1; at(ib1) = va1; }
     }
     if (G < g1) {
       const uint4 d = gdesc[G];
       if ((d.x << lane) >> 31) {
-        const uint32_t ia = d.y + lane, ib = d.z + __popc(d.x & ltmask);
-        const V va = stage[ia], vb = stage[ib];
-        stage[ia] = vb;
-        stage[ib] = va;
+        const uint32_t ia = d.y + lb, ib = d.z + (__popc(d.x & ltmask) << kSh);
+        const V va = at(ia), vb = at(ib);
+        at(ia) = vb;
+        at(ib) = va;
       }
     }
     __syncthreads();
@@ -999,10 +1005,10 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
       for (uint32_t G = goff[h]; G < goff[h + 1]; ++G) {
         const uint4 d = gdesc[G];
         if ((d.x << lane) >> 31) {
-          const uint32_t ia = d.y + lane, ib = d.z + __popc(d.x & ltmask);
-          const V va = stage[ia], vb = stage[ib];
-          stage[ia] = vb;
-          stage[ib] = va;
+          const uint32_t ia = d.y + lb, ib = d.z + (__popc(d.x & ltmask) << kSh);
+          const V va = at(ia), vb = at(ib);
+          at(ia) = vb;
+          at(ib) = va;
         }
       }
       __syncwarp();
