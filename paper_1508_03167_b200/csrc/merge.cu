@@ -1028,12 +1028,24 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
       bulk_commit();
     }
   }
-  for (int hw = wid; hw < nw; hw += kTreeBlock / 32) {
-    const uint32_t L = (uint32_t)(bch[hw] - ach[hw]);
-    const uint32_t lo = ilo_s[hw], hi = ihi_s[hw];
-    const V* st = stage + stoff[hw];
-    for (uint32_t i = lane; i < lo; i += 32) acc.st(ach[hw] + i, st[i]);
-    for (uint32_t i = hi + lane; i < L; i += 32) acc.st(ach[hw] + i, st[i]);
+  if (tma) {
+    // ragged ends: a window's head is < 2E-1 and its tail < E elements, so 16
+    // slots per window (8 head, 8 tail) cover them: one pass of the block
+    for (uint32_t t = tid; t < (uint32_t)nw * 16u; t += kTreeBlock) {
+      const uint32_t hw = t >> 4, k = t & 15u;
+      const uint32_t lo = ilo_s[hw], hi = ihi_s[hw];
+      const uint32_t i = k < 8 ? k : hi + (k - 8);
+      const uint32_t lim = k < 8 ? lo : (uint32_t)(bch[hw] - ach[hw]);
+      if (i < lim) acc.st(ach[hw] + i, stage[stoff[hw] + i]);
+    }
+  } else {
+    for (int hw = wid; hw < nw; hw += kTreeBlock / 32) {
+      const uint32_t L = (uint32_t)(bch[hw] - ach[hw]);
+      const uint32_t lo = ilo_s[hw], hi = ihi_s[hw];
+      const V* st = stage + stoff[hw];
+      for (uint32_t i = lane; i < lo; i += 32) acc.st(ach[hw] + i, st[i]);
+      for (uint32_t i = hi + lane; i < L; i += 32) acc.st(ach[hw] + i, st[i]);
+    }
   }
   if (tma && wid == 0) bulk_wait_read0();  // the shared source must outlive the copies
 }
