@@ -951,9 +951,14 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
       if (ragi[k] != 0xffffffffu) stage[ragi[k]] = rag[k];
   }
   __syncthreads();
-  uint32_t before = 0;
+  // warp totals' exclusive prefix by a shuffle scan over the first lanes
+  uint32_t ws = lane < (uint32_t)(kTreeBlock / 32) ? wsum[lane] : 0u;
 #pragma unroll
-  for (int w = 0; w < kTreeBlock / 32; ++w) before += (w < (int)wid) ? wsum[w] : 0u;
+  for (int o = 1; o < kTreeBlock / 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, ws, o);
+    if (lane >= (uint32_t)o) ws += y;
+  }
+  const uint32_t before = __shfl_sync(0xffffffffu, ws, (wid + 31) & 31) * (wid ? 1u : 0u);
   const uint32_t ex0 = before + x - c2, ex1 = ex0 + cnt2[0];
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
@@ -1056,7 +1061,7 @@ __global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __re
                                                                 const PairPlan* __restrict__ plans,
                                                                 const uint64_t* __restrict__ rank,
                                                                 const uint64_t* __restrict__ chains, uint32_t tpp) {
-  const uint64_t g = blockIdx.x / tpp, tau = blockIdx.x - g * tpp;
+  const uint32_t g = blockIdx.x / tpp, tau = blockIdx.x - g * tpp;  // (32-bit: grid < 2^31)
   const PairPlan* Pp = plans + g;
   if (tau * (uint64_t)TreeCfg<V>::T0 >= Pp->n1) return;
   const FlatAcc<V> acc{in + Pp->s, out + Pp->s};
