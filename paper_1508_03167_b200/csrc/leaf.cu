@@ -761,10 +761,20 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
   if (NP <= 16) chunk = max(chunk, (mmax + 3) & ~3u);
   V* sdata = reinterpret_cast<V*>(sh);
   const uint32_t mr = (mmax + 15) & ~15u;
-  uint16_t* Hg = reinterpret_cast<uint16_t*>(
-      ((uintptr_t)(scratch + (uint64_t)blockIdx.x * leaf_scratch_stride(mmax)) + 15) & ~(uintptr_t)15);
-  uint16_t* lst = Hg + mr;
-  uint16_t* tmp = lst + mr;
+  // the CTA's scratch (H, queue, spill) and the timing knob: loaded from shared
+  // memory where used, so the compiler neither keeps them in registers nor
+  // rematerialises the address arithmetic (64-register cap)
+  __shared__ uint16_t* s_hg;
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) {
+    s_hg = reinterpret_cast<uint16_t*>(
+        ((uintptr_t)(scratch + (uint64_t)blockIdx.x * leaf_scratch_stride(mmax)) + 15) & ~(uintptr_t)15);
+    s_stop = g_leaf_stop;
+  }
+  __syncthreads();
+#define Hg (s_hg)
+#define lst (s_hg + mr)
+#define tmp (s_hg + 2 * mr)
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
   for (uint64_t g = blockIdx.x; g < nleaves; g += gridDim.x) {
@@ -827,7 +837,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
         if (s - 1u < m - 1u) atomicAdd(&cnt[j >> 2], 1u << ((j & 3) << 3));
       }
     __syncthreads();
-    if (g_leaf_stop <= 1) continue;
+    if (s_stop <= 1) continue;
     // 2. group totals and in-group prefixes; thread t: groups GPT*t .. GPT*t+GPT-1
     {
       const uint32_t ng = nw >> 2;
@@ -896,7 +906,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
       __syncthreads();
       continue;
     }
-    if (g_leaf_stop <= 2) continue;
+    if (s_stop <= 2) continue;
     // 3. scatter step ids into their buckets; the byte atomic gives the slot
 #pragma unroll
     for (int i = 0; i < (int)NP; ++i)
@@ -913,7 +923,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
         }
       }
     __syncthreads();
-    if (g_leaf_stop <= 3) continue;
+    if (s_stop <= 3) continue;
     if (tid == 0) l2_prefetch(src_in, (size_t)m * sizeof(V));  // staged in phase 8
     // 4. targets, four per counter word (the counters now hold in-group bucket ends)
     for (uint32_t w = tid; w < nw; w += BLOCK) {
@@ -949,7 +959,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
       *reinterpret_cast<uint2*>(Hg + 4 * w) = make_uint2(Hq[0] | (Hq[1] << 16), Hq[2] | (Hq[3] << 16));
     }
     __syncthreads();
-    if (g_leaf_stop <= 4) continue;
+    if (s_stop <= 4) continue;
     // 5. queued buckets of 3..8 steps, one per thread: keys (step << 16 | slot)
     //    through a sorting network; the entry at sorted position a gets the
     //    step at a + 1 (or the target itself at the end)
@@ -980,7 +990,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
       const uint32_t en = (cw >> (8 * q)) & 0xFFu;
       const uint32_t sn = q ? ((cw >> (8 * (q - 1))) & 0xFFu) : ((w & 3) ? (cnt[w - 1] >> 24) : 0u);
       const uint32_t k = en - sn, st = (uint32_t)gst[w >> 2] + sn;
-      if (k <= 32 && g_leaf_stop != 12) {  // (12: timing/test knob, all through the O(k^2) path)
+      if (k <= 32 && s_stop != 12) {  // (12: timing/test knob, all through the O(k^2) path)
         uint32_t key = lane < k ? (((uint32_t)bkt[st + lane] << 16) | (st + lane)) : 0xFFFFFFFFu;
 #pragma unroll
         for (uint32_t kk = 2; kk <= 32; kk <<= 1)
@@ -1012,7 +1022,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
       __syncwarp();
     }
     __syncthreads();
-    if (g_leaf_stop <= 5) continue;
+    if (s_stop <= 5) continue;
     // 6. every owned step picks up N(s) (> s) or its target j_s (<= s)
 #pragma unroll
     for (int i = 0; i < (int)NP; ++i)
@@ -1030,7 +1040,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
     for (uint32_t w = tid; w < ((m + 7) >> 3); w += BLOCK)
       reinterpret_cast<uint4*>(bkt)[w] = reinterpret_cast<const uint4*>(Hg)[w];
     __syncthreads();
-    if (g_leaf_stop <= 6) continue;
+    if (s_stop <= 6) continue;
     {
       const uint16_t* Hs = bkt;
 #pragma unroll
@@ -1048,7 +1058,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
         }
     }
     __syncthreads();
-    if (g_leaf_stop == 7) continue;
+    if (s_stop == 7) continue;
     // 8. gather through shared memory: the leaf's data in chunks over the whole
     //    allocation (H is dead); each output is stored in the pass holding its source
     const bool sal = (((uintptr_t)src_in) & 15) == 0;
@@ -1058,7 +1068,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
         // one TMA bulk copy (the chunk is 16-byte aligned and sized)
         if (tid == 0) {
           fence_proxy_async_smem();  // earlier generic accesses of this smem first
-          if (g_leaf_stop != 11) {
+          if (s_stop != 11) {
             mbar_arrive_expect_tx(&s_bar, cn * (uint32_t)sizeof(V));
             for (uint32_t o = 0; o < cn * (uint32_t)sizeof(V); o += 65536u)
               bulk_g2s(reinterpret_cast<char*>(sdata) + o, reinterpret_cast<const char*>(src_in + c0) + o,
@@ -1085,12 +1095,15 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t src = ((r[i] >> (16 * h)) & 0xFFFFu) - c0;
-          if (src < cn && g_leaf_stop != 10) dpass[2 * BLOCK * i + h] = g_leaf_stop == 8 ? (V)src : sdata[src];
+          if (src < cn && s_stop != 10) dpass[2 * BLOCK * i + h] = s_stop == 8 ? (V)src : sdata[src];
         }
       __syncthreads();
     }
   }
 }
+#undef Hg
+#undef lst
+#undef tmp
 
 // Fallback for leaves larger than 65536 elements (non-default cutoffs and
 // fisher_yates on long arrays): one thread per leaf runs the reference loop
