@@ -907,36 +907,47 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
   }
   // 3. group masks (two consecutive groups per thread) and their ones
   uint32_t cnt2[2], mm[2], gy[2], gz[2];
-#pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    const uint32_t G = 2 * tid + e;
-    // window of group G: the last h < nw with goff[h] <= G (binary search over the lanes)
-    uint32_t h = 0;
+  {
+    // window of group 2*tid: the last h < nw with goff[h] <= G (binary search
+    // over the lanes); group 2*tid+1 lies in the same window or the next one
+    // (windows h < nw are non-empty)
+    const uint32_t G0 = 2 * tid;
+    uint32_t h0 = 0;
 #pragma unroll
     for (uint32_t step = 16; step; step >>= 1) {
-      const uint32_t c = h + step;
+      const uint32_t c = h0 + step;
       const uint32_t gc_ = __shfl_sync(0xffffffffu, r_goff, c & 31);
-      h = (c < nw && gc_ <= G) ? c : h;
+      h0 = (c < nw && gc_ <= G0) ? c : h0;
     }
-    const uint64_t wa = __shfl_sync(0xffffffffu, a, h), wb = __shfl_sync(0xffffffffu, b, h);
-    const uint32_t wg = __shfl_sync(0xffffffffu, r_goff, h);
-    uint32_t m = 0;
-    if (G < ngroups) {
-      const uint64_t p = wa + 32ull * (G - wg);
-      if (p < t) {
-        const uint64_t nv = min(wb - p, t - p);
-        m = (uint32_t)(bits64_at(sd, p) >> 32);
-        if (nv < 32) m &= ~(0xffffffffu >> nv);
+    const uint32_t gnext = __shfl_sync(0xffffffffu, r_goff, (h0 + 1) & 31);
+    const bool step1 = h0 + 1 < nw && gnext <= G0 + 1;
+    const uint32_t hh[2] = {h0, step1 ? h0 + 1 : h0};
+    uint64_t bits0 = 0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const uint32_t G = G0 + e, h = hh[e];
+      const uint64_t wa = __shfl_sync(0xffffffffu, a, h), wb = __shfl_sync(0xffffffffu, b, h);
+      const uint32_t wg = __shfl_sync(0xffffffffu, r_goff, h);
+      uint32_t m = 0;
+      if (G < ngroups) {
+        const uint64_t p = wa + 32ull * (G - wg);
+        if (p < t) {
+          const uint64_t nv = min(wb - p, t - p);
+          // group 2*tid+1 in the same window: the low half of group 2*tid's 64 bits
+          if (e == 0) bits0 = bits64_at(sd, p);
+          m = (e == 0 || step1) ? (uint32_t)((e == 0 ? bits0 : bits64_at(sd, p)) >> 32) : (uint32_t)bits0;
+          if (nv < 32) m &= ~(0xffffffffu >> nv);
+        }
       }
+      cnt2[e] = __popc(m);
+      // descriptor parts known now: stage index of the group's first position,
+      // and of its window's B slots minus the ones of the windows before h
+      const uint32_t st_h = __shfl_sync(0xffffffffu, r_stoff, h), st_h1 = __shfl_sync(0xffffffffu, r_stoff, (h + 1) & 31);
+      const uint32_t ob = __shfl_sync(0xffffffffu, r_onesb, h);
+      gy[e] = st_h + 32 * (G - wg);
+      gz[e] = st_h1 - ob;
+      mm[e] = m;
     }
-    cnt2[e] = __popc(m);
-    // descriptor parts known now: stage index of the group's first position,
-    // and of its window's B slots minus the ones of the windows before h
-    const uint32_t st_h = __shfl_sync(0xffffffffu, r_stoff, h), st_h1 = __shfl_sync(0xffffffffu, r_stoff, (h + 1) & 31);
-    const uint32_t ob = __shfl_sync(0xffffffffu, r_onesb, h);
-    gy[e] = st_h + 32 * (G - wg);
-    gz[e] = st_h1 - ob;
-    mm[e] = m;
   }
   const uint32_t c2 = cnt2[0] + cnt2[1];
   uint32_t x = c2;
