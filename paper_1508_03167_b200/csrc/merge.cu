@@ -818,15 +818,14 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
       bytes = (uint32_t)((l1 - l0) * sizeof(V));
     }
   }
-  uint32_t sreg = reg, sgc = gc, sby = bytes;
+  uint32_t sreg = reg, sgc = gc;
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y1 = __shfl_up_sync(0xffffffffu, sreg, o);
     const uint32_t y2 = __shfl_up_sync(0xffffffffu, sgc, o);
-    const uint32_t y3 = __shfl_up_sync(0xffffffffu, sby, o);
-    if (lane >= (uint32_t)o) { sreg += y1; sgc += y2; sby += y3; }
+    if (lane >= (uint32_t)o) { sreg += y1; sgc += y2; }
   }
   const uint32_t treg = __shfl_sync(0xffffffffu, sreg, 31), tgc = __shfl_sync(0xffffffffu, sgc, 31);
-  const uint32_t tby = __shfl_sync(0xffffffffu, sby, 31);
+  const uint32_t tby = __reduce_add_sync(0xffffffffu, bytes);  // TMA bytes (only the total is needed)
   const bool ok = nw < (uint32_t)kTreeD && !__any_sync(0xffffffffu, big) && treg <= C::SCAP && tgc <= C::GCAP &&
                   !g_tree_force_direct;
   const uint32_t r_stoff = sreg - reg + mis, r_goff = act ? sgc - gc : tgc;
