@@ -807,15 +807,16 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
   uint32_t mis = 0, reg = 0, gc = 0, lo = 0, hi = 0, bytes = 0;
   if (act && !big) {
     const uintptr_t A0 = reinterpret_cast<uintptr_t>(acc.src(a));
+    const uint32_t l32 = (uint32_t)len;  // (<= SCAP here)
     mis = (uint32_t)((A0 & 15) / sizeof(V));
-    reg = (mis + (uint32_t)len + C::E - 1) & ~(C::E - 1);
-    gc = (uint32_t)((len + 31) >> 5);
-    const uint64_t l0 = (C::E - mis) & (C::E - 1);  // first 16-byte aligned offset
-    const uint64_t l1 = ((mis + len) & ~(uint64_t)(C::E - 1)) - mis;
-    if (tma && l1 > l0 && l1 <= len) {
-      lo = (uint32_t)l0;
-      hi = (uint32_t)l1;
-      bytes = (uint32_t)((l1 - l0) * sizeof(V));
+    reg = (mis + l32 + C::E - 1) & ~(C::E - 1);
+    gc = (l32 + 31) >> 5;
+    const uint32_t l0 = (C::E - mis) & (C::E - 1);  // first 16-byte aligned offset
+    const uint32_t l1 = ((mis + l32) & ~(C::E - 1)) - mis;
+    if (tma && l1 > l0 && l1 <= l32) {
+      lo = l0;
+      hi = l1;
+      bytes = (l1 - l0) * (uint32_t)sizeof(V);
     }
   }
   uint32_t sreg = reg, sgc = gc;
