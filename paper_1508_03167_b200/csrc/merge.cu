@@ -994,8 +994,11 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
     // two groups per trip (independent slots): their smem round trips overlap
     const uint32_t g1 = goff[h + 1];
     uint32_t G = goff[h] + wid;
-    for (; G + NWp < g1; G += 2 * NWp) {
-      const uint4 d0 = gdesc[G], d1 = gdesc[G + NWp];
+    const uint4* dp = gdesc + G;
+    for (int trips = G + NWp < g1 ? (int)((g1 - G - NWp - 1) / (2 * NWp)) + 1 : 0; trips > 0; --trips) {
+      const uint4 d0 = dp[0], d1 = dp[NWp];
+      dp += 2 * NWp;
+      G += 2 * NWp;
       const bool on0 = (d0.x << lane) >> 31, on1 = (d1.x << lane) >> 31;
       const uint32_t ia0 = d0.y + lb, ib0 = d0.z + (__popc(d0.x & ltmask) << kSh);
       const uint32_t ia1 = d1.y + lb, ib1 = d1.z + (__popc(d1.x & ltmask) << kSh);
