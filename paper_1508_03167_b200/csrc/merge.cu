@@ -990,10 +990,15 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
   auto at = [&](uint32_t off) -> V& { return *reinterpret_cast<V*>(sb + off); };
   int h = 0;
   constexpr uint32_t NWp = kTreeBlock / 32;
-  for (; h + 1 < nw && goff[h + 1] - goff[h] > 2; ++h) {
+  // windows of more than two groups (a prefix: window sizes about halve) go
+  // to the whole block; their group ranges come from the lanes' registers
+  const uint32_t r_gnx = __shfl_down_sync(0xffffffffu, r_goff, 1);  // goff[h + 1] in lane h
+  const uint32_t bwin = __ballot_sync(0xffffffffu, lane + 1 < nw && r_gnx - r_goff > 2);
+  const int nbw = __ffs(~bwin) - 1;
+  for (; h < nbw; ++h) {
     // two groups per trip (independent slots): their smem round trips overlap
-    const uint32_t g1 = goff[h + 1];
-    uint32_t G = goff[h] + wid;
+    const uint32_t g1 = __shfl_sync(0xffffffffu, r_gnx, h);
+    uint32_t G = __shfl_sync(0xffffffffu, r_goff, h) + wid;
     const uint4* dp = gdesc + G;
     for (int trips = G + NWp < g1 ? (int)((g1 - G - NWp - 1) / (2 * NWp)) + 1 : 0; trips > 0; --trips) {
       const uint4 d0 = dp[0], d1 = dp[NWp];
