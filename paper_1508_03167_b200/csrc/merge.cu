@@ -769,7 +769,7 @@ uint32_t tree_tile(int eb) { return eb == 4 ? TreeCfg<uint32_t>::T0 : TreeCfg<un
 //  5. TMA bulk stores of every window from shared memory to out[].
 // Each element is read once and written once; no global round trip between.
 template <typename V, class Acc>
-__device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* __restrict__ Pp,
+__device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* __restrict__ Pp, uint64_t a, uint64_t b,
                                                 const uint64_t* __restrict__ rank, const uint64_t* __restrict__ ca) {
   using C = TreeCfg<V>;
   extern __shared__ __align__(128) unsigned char tree_smem[];
@@ -794,11 +794,7 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
   // 1. windows: lane h owns window h.  Every warp derives the same staging
   //    layout in registers (no block barrier before the bits are ranked);
   //    warp 0 publishes it to shared memory and issues the TMA loads.
-  uint64_t a = 0, b = 0;
-  if (lane < (uint32_t)kTreeD) {
-    a = ca[lane];
-    b = ca[kTreeD + lane];
-  }
+  // (a, b): window h's start and end in lane h, loaded by the caller first
   const uint32_t emp = __ballot_sync(0xffffffffu, lane < (uint32_t)kTreeD && a == b);
   const uint32_t nw = emp ? (uint32_t)(__ffs(emp) - 1) : (uint32_t)kTreeD;
   const bool act = lane < nw;
@@ -1082,9 +1078,17 @@ __global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __re
                                                                 const uint64_t* __restrict__ chains, uint32_t tpp) {
   const uint32_t g = blockIdx.x / tpp, tau = blockIdx.x - g * tpp;  // (32-bit: grid < 2^31)
   const PairPlan* Pp = plans + g;
+  // the window chain first: its load overlaps the plan's
+  const uint64_t* ca = chains + ((uint64_t)g * (tpp + 1) + tau) * kTreeD;
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t a = 0, b = 0;
+  if (lane < (uint32_t)kTreeD) {
+    a = ca[lane];
+    b = ca[kTreeD + lane];
+  }
   if (tau * (uint64_t)TreeCfg<V>::T0 >= Pp->n1) return;
   const FlatAcc<V> acc{in + Pp->s, out + Pp->s};
-  merge_tree_tile<V>(acc, Pp, rank, chains + (g * (tpp + 1) + tau) * kTreeD);
+  merge_tree_tile<V>(acc, Pp, a, b, rank, chains + ((uint64_t)g * (tpp + 1) + tau) * kTreeD);
 }
 
 // One pair split over peer buffers (in place); this launch takes the tiles
@@ -1098,7 +1102,14 @@ __global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_peer_kernel(const Pe
   const uint64_t tau = part + (uint64_t)blockIdx.x * nparts;
   if (tau >= tpp || tau * (uint64_t)TreeCfg<V>::T0 >= plans->n1) return;
   const PeerAcc<V> acc{parts};
-  merge_tree_tile<V>(acc, plans, rank, chains + tau * kTreeD);
+  const uint64_t* ca = chains + tau * kTreeD;
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t a = 0, b = 0;
+  if (lane < (uint32_t)kTreeD) {
+    a = ca[lane];
+    b = ca[kTreeD + lane];
+  }
+  merge_tree_tile<V>(acc, plans, a, b, rank, ca);
 }
 
 template <typename V>
