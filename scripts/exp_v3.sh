@@ -1,6 +1,5 @@
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_edges.py -q -x 2>&1 | tail -2
 python scripts/prof_run.py 30 3 --check
-SK_LIB_PATH=build/variants/sstop.so python scripts/prof_run.py 30 3 --check
-SK_LIB_PATH=build/variants/noknob.so python scripts/prof_run.py 30 3 --check
-python scripts/prof_run.py 30 3
-SK_LIB_PATH=build/variants/sstop.so python scripts/prof_run.py 30 3
-SK_LIB_PATH=build/variants/noknob.so python scripts/prof_run.py 30 3
+python scripts/prof_run.py 30 3 8=0 --check
+python scripts/prof_run.py 30 3 --u64 --check
+python scripts/prof_run.py 30 3 --u64 8=0
