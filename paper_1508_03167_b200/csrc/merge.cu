@@ -21,6 +21,7 @@
 // the rank tables, stop points, window chains, tail draws and tail plans are
 // built on a side stream while the leaf stage runs.
 #include <algorithm>
+#include <stdexcept>
 #include "sk_kernels.h"
 
 namespace sk {
@@ -1075,8 +1076,11 @@ template <typename V>
 __global__ void __launch_bounds__(kTreeBlock, 5) merge_tree_kernel(const V* __restrict__ in, V* __restrict__ out,
                                                                 const PairPlan* __restrict__ plans,
                                                                 const uint64_t* __restrict__ rank,
-                                                                const uint64_t* __restrict__ chains, uint32_t tpp) {
-  const uint32_t g = blockIdx.x / tpp, tau = blockIdx.x - g * tpp;  // (32-bit: grid < 2^31)
+                                                                const uint64_t* __restrict__ chains, uint32_t tpp,
+                                                                uint32_t pair_in_y) {
+  // 2-D grid (no division): tiles of a pair along x, pairs along y -- or the
+  // transpose when there are more than 65535 pairs
+  const uint32_t g = pair_in_y ? blockIdx.y : blockIdx.x, tau = pair_in_y ? blockIdx.x : blockIdx.y;
   const PairPlan* Pp = plans + g;
   // the window chain first: its load overlaps the plan's
   const uint64_t* ca = chains + ((uint64_t)g * (tpp + 1) + tau) * kTreeD;
@@ -1147,8 +1151,10 @@ static void merge_tree_t(void* in, void* out, const PairPlan* plans, uint64_t np
                          const uint64_t* chains, uint32_t tpp, cudaStream_t st) {
   const size_t smem = TreeCfg<V>::SMEM;
   cudaFuncSetAttribute(merge_tree_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  merge_tree_kernel<V><<<(unsigned)(npairs * tpp), kTreeBlock, smem, st>>>((const V*)in, (V*)out, plans, rank,
-                                                                             chains, tpp);
+  const bool piy = npairs <= 65535;
+  if (!piy && tpp > 65535) throw std::runtime_error("merge round: too many pairs and tiles for the grid");
+  const dim3 grid = piy ? dim3(tpp, (unsigned)npairs) : dim3((unsigned)npairs, tpp);
+  merge_tree_kernel<V><<<grid, kTreeBlock, smem, st>>>((const V*)in, (V*)out, plans, rank, chains, tpp, piy ? 1u : 0u);
   count_launch();
 }
 

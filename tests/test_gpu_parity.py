@@ -374,3 +374,13 @@ def test_leaf_apply_variants(variant):
         lib.sk_debug_set(6, 0)
         lib.sk_debug_set(1, 99)
         lib.sk_debug_set(7, 1)
+
+
+def test_more_than_65535_pairs_in_a_round():
+    # n = 2^22 at cutoff 16: 2^18 leaves, 131072 pairs in round 1 (the tree
+    # merge's transposed launch grid: pairs along x)
+    for dt in (torch.int32, torch.int64):
+        x, rep = gpu_perm(1 << 22, 16, 21, dt)
+        ref, rbits = O.merge_shuffle_perm(1 << 22, 16, 21)
+        assert rep.bits == rbits
+        assert np.array_equal(x.cpu().numpy().astype(np.int64), ref)
