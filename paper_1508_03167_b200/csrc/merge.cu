@@ -1021,6 +1021,37 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
     }
     __syncthreads();
   }
+  // Windows below h are final now (a window is written only by its own swaps
+  // and by the previous window's): with TMA their stores start while warp 0
+  // finishes the short windows -- warp 1 issues the bulk stores, warps 2..7
+  // the ragged ends.
+  const int hf = h;
+  auto store_ragged = [&](int h0, int h1, uint32_t t0, uint32_t nthr) {
+    // a window's head is < 2E-1 and its tail < E elements: 16 slots per window
+    for (uint32_t t = t0; t < (uint32_t)(h1 - h0) * 16u; t += nthr) {
+      const uint32_t hw = (uint32_t)h0 + (t >> 4), k = t & 15u;
+      const uint32_t lo = ilo_s[hw], hi = ihi_s[hw];
+      const uint32_t i = k < 8 ? k : hi + (k - 8);
+      const uint32_t lim = k < 8 ? lo : (uint32_t)(bch[hw] - ach[hw]);
+      if (i < lim) acc.st(ach[hw] + i, stage[stoff[hw] + i]);
+    }
+  };
+  auto store_tma = [&](int h0, int h1) {  // one lane per window
+    if (lane >= (uint32_t)h0 && lane < (uint32_t)h1 && ihi_s[lane] > ilo_s[lane]) {
+      const uint64_t a = ach[lane];
+      const V* st = stage + stoff[lane];
+      acc.runs(a + ilo_s[lane], a + ihi_s[lane], [&](uint64_t x0, uint64_t x1) {
+        bulk_s2g(acc.dst(x0), st + (x0 - a), (uint32_t)((x1 - x0) * sizeof(V)));
+      });
+    }
+    bulk_commit();
+  };
+  if (tma) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (wid == 1) store_tma(0, hf);
+    else if (wid >= 2) store_ragged(0, hf, tid - 64, kTreeBlock - 64);
+  }
   if (wid == 0) {
     for (; h + 1 < nw; ++h) {
       for (uint32_t G = goff[h]; G < goff[h + 1]; ++G) {
@@ -1034,31 +1065,13 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
       }
       __syncwarp();
     }
+    if (tma) fence_proxy_async_smem();
   }
-  // 5. stores: aligned interiors by TMA (one lane per window), ragged ends plain
+  // 5. the remaining stores
   __syncthreads();
   if (tma) {
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (wid == 0 && lane < (uint32_t)nw && ihi_s[lane] > ilo_s[lane]) {
-      const uint64_t a = ach[lane];
-      const V* st = stage + stoff[lane];
-      acc.runs(a + ilo_s[lane], a + ihi_s[lane], [&](uint64_t x0, uint64_t x1) {
-        bulk_s2g(acc.dst(x0), st + (x0 - a), (uint32_t)((x1 - x0) * sizeof(V)));
-      });
-      bulk_commit();
-    }
-  }
-  if (tma) {
-    // ragged ends: a window's head is < 2E-1 and its tail < E elements, so 16
-    // slots per window (8 head, 8 tail) cover them: one pass of the block
-    for (uint32_t t = tid; t < (uint32_t)nw * 16u; t += kTreeBlock) {
-      const uint32_t hw = t >> 4, k = t & 15u;
-      const uint32_t lo = ilo_s[hw], hi = ihi_s[hw];
-      const uint32_t i = k < 8 ? k : hi + (k - 8);
-      const uint32_t lim = k < 8 ? lo : (uint32_t)(bch[hw] - ach[hw]);
-      if (i < lim) acc.st(ach[hw] + i, stage[stoff[hw] + i]);
-    }
+    if (wid == 0) store_tma(hf, (int)nw);
+    store_ragged(hf, (int)nw, tid, kTreeBlock);
   } else {
     for (int hw = wid; hw < nw; hw += kTreeBlock / 32) {
       const uint32_t L = (uint32_t)(bch[hw] - ach[hw]);
@@ -1068,7 +1081,7 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
       for (uint32_t i = hi + lane; i < L; i += 32) acc.st(ach[hw] + i, st[i]);
     }
   }
-  if (tma && wid == 0) bulk_wait_read0();  // the shared source must outlive the copies
+  if (tma && wid <= 1) bulk_wait_read0();  // the shared source must outlive the copies
 }
 
 // One CTA per (pair, tile) of a round.
