@@ -704,7 +704,9 @@ static uint64_t run_rs_tasks(int eb, void* buf0, void* buf1, const std::vector<R
     CK(cudaMemsetAsync(counts, 0, 3 * 8, st));
     CK(cudaMemsetAsync(tbits, 0, nt * 8, st));
     // per-task bit counts: RsTask.array indexes tbits
-    launch_rs_plan(dT, nt, cutoff, draws, dN, counts, ncap, dL, lcap, tbits, st);
+    uint64_t maxsz = 0;
+    for (const auto& tk : tasks) maxsz = std::max<uint64_t>(maxsz, tk.hi - tk.lo);
+    launch_rs_plan(dT, nt, cutoff, draws, dN, counts, ncap, dL, lcap, tbits, st, maxsz > (1ull << 31));
     unsigned long long hc[3];
     CK(cudaMemcpyAsync(hc, counts, 24, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

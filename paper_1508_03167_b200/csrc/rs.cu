@@ -16,6 +16,7 @@
 //    decoded into the u16 draws array) and records the split nodes and the
 //    leaves; then every split node is applied (CTA per node, level by level)
 //    and every leaf through the closed-form leaf kernel (leaf.cu, list mode).
+#include <type_traits>
 #include "sk_kernels.h"
 
 namespace sk {
@@ -178,6 +179,7 @@ void launch_rs_split(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchu
 // ------------------------------------------------------------ small tasks
 // One lane per task: the sequential order of _kernels.py:148-179 on sizes
 // only.  Leaves of at most 65536 elements get their draws in draws[lo + i].
+template <bool WIDE>
 __global__ void rs_plan_kernel(const RsTask* __restrict__ T, uint32_t ntasks, uint64_t cutoff,
                                uint16_t* __restrict__ draws, RsNode* __restrict__ nodes,
                                unsigned long long* __restrict__ counts, uint64_t node_cap,
@@ -191,7 +193,10 @@ __global__ void rs_plan_kernel(const RsTask* __restrict__ T, uint32_t ntasks, ui
   uint32_t sdep[kStack];
   int top = 0;
   slo[0] = tk.lo; shi[0] = tk.hi; sdep[0] = 0; top = 1;
-  Reader64 rd;
+  // 32-bit reader and dice roller when every task is at most 2^31 elements
+  // (a split's bits 32 at a time); WIDE: the 64-bit ones
+  using Rd = typename std::conditional<WIDE, Reader64, Reader32>::type;
+  Rd rd;
   rd.init(tk.sd, 0);
   uint64_t off = 0;
   while (top > 0) {
@@ -203,7 +208,9 @@ __global__ void rs_plan_kernel(const RsTask* __restrict__ T, uint32_t ntasks, ui
       const unsigned long long li = atomicAdd(&counts[1], 1ull);
       if (li < leaf_cap) leaves[li] = RsLeaf{lo, hi, off, t, dep};
       for (uint64_t i = size; i >= 2; --i) {  // steps i-1 .. 1, bound i
-        const uint64_t j = fdr64(rd, i, off);
+        uint64_t j;
+        if constexpr (WIDE) j = fdr64(rd, i, off);
+        else j = fdr32(rd, (uint32_t)i, off);
         if (size <= 65536) draws[lo + i - 1] = (uint16_t)j;
       }
       continue;
@@ -211,9 +218,10 @@ __global__ void rs_plan_kernel(const RsTask* __restrict__ T, uint32_t ntasks, ui
     const unsigned long long ni = atomicAdd(&counts[0], 1ull);
     if (ni < node_cap) nodes[ni] = RsNode{lo, hi, off, t, dep};
     uint64_t ones = 0;
-    for (uint64_t k = 0; k < size; k += 64) {
-      const uint32_t kk = (uint32_t)min((uint64_t)64, size - k);
-      ones += __popcll(rd.take(kk));
+    constexpr uint32_t kw = WIDE ? 64u : 32u;
+    for (uint64_t k = 0; k < size; k += kw) {
+      const uint32_t kk = (uint32_t)min((uint64_t)kw, size - k);
+      ones += __popcll((uint64_t)rd.take(kk));
     }
     off += size;
     const uint64_t nz = size - ones;
@@ -229,10 +237,14 @@ __global__ void rs_plan_kernel(const RsTask* __restrict__ T, uint32_t ntasks, ui
 
 void launch_rs_plan(const RsTask* T, uint32_t ntasks, uint64_t cutoff, uint16_t* draws, RsNode* nodes,
                     unsigned long long* counts, uint64_t node_cap, RsLeaf* leaves, uint64_t leaf_cap,
-                    unsigned long long* bits, cudaStream_t st) {
+                    unsigned long long* bits, cudaStream_t st, bool wide) {
   if (!ntasks) return;
-  rs_plan_kernel<<<(ntasks + 63) / 64, 64, 0, st>>>(T, ntasks, cutoff, draws, nodes, counts, node_cap, leaves,
-                                                     leaf_cap, bits);
+  if (wide)
+    rs_plan_kernel<true><<<(ntasks + 63) / 64, 64, 0, st>>>(T, ntasks, cutoff, draws, nodes, counts, node_cap, leaves,
+                                                            leaf_cap, bits);
+  else
+    rs_plan_kernel<false><<<(ntasks + 63) / 64, 64, 0, st>>>(T, ntasks, cutoff, draws, nodes, counts, node_cap,
+                                                             leaves, leaf_cap, bits);
   count_launch();
 }
 

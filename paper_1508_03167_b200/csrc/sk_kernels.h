@@ -97,7 +97,7 @@ void launch_rs_split(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchu
                      const uint64_t* nz, const void* in, void* out, cudaStream_t st);
 void launch_rs_plan(const RsTask* T, uint32_t ntasks, uint64_t cutoff, uint16_t* draws, RsNode* nodes,
                     unsigned long long* counts, uint64_t node_cap, RsLeaf* leaves, uint64_t leaf_cap,
-                    unsigned long long* bits, cudaStream_t st);
+                    unsigned long long* bits, cudaStream_t st, bool wide);
 void launch_rs_nodes(int eb, const RsNode* nodes, uint32_t count, const RsTask* T, void* buf0, void* buf1,
                      cudaStream_t st);
 void launch_rs_leaf_serial(int eb, const RsLeaf* L, uint32_t count, const RsTask* T, void* buf0, void* buf1,
