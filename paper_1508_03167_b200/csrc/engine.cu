@@ -817,7 +817,7 @@ static uint64_t run_rs_parallel(int eb, void* data, uint64_t n, uint64_t cutoff,
       const uint32_t nr = (uint32_t)big.size();
       RsRange* dR = A.alloc<RsRange>(nr, st);
       CK(cudaMemcpyAsync(dR, big.data(), nr * sizeof(RsRange), cudaMemcpyHostToDevice, st));
-      uint64_t* cz = A.alloc<uint64_t>(nch, st);
+      uint64_t* cz = A.alloc<uint64_t>(2 * nch, st);  // zero counts, then the chunk -> range map
       uint64_t* dnz = A.alloc<uint64_t>(nr, st);
       launch_rs_level(eb, dR, nr, nch, cz, dnz, st);
       const uint32_t par = (uint32_t)(depth & 1);

@@ -34,9 +34,11 @@ __device__ __forceinline__ uint32_t rs_range_of_chunk(const RsRange* R, uint32_t
 }
 
 // zeros among the chunk's coin flips (one word per lane of warp 0)
-__global__ void rs_chunk_zeros_kernel(const RsRange* __restrict__ R, uint32_t nr, uint64_t* __restrict__ cz) {
+__global__ void rs_chunk_zeros_kernel(const RsRange* __restrict__ R, uint32_t nr, uint64_t* __restrict__ cz,
+                                      uint32_t* __restrict__ rmap) {
   const uint64_t c = blockIdx.x;
   const uint32_t r = rs_range_of_chunk(R, nr, c);
+  if (threadIdx.x == 0) rmap[c] = r;  // (the split kernel reads it instead of searching again)
   const RsRange rg = R[r];
   const uint64_t size = rg.hi - rg.lo;
   const uint64_t cs = (c - rg.chunk0) * kRsChunk;
@@ -145,10 +147,10 @@ template <typename V>
 __global__ void __launch_bounds__(256) rs_split_kernel(const RsRange* __restrict__ R, uint32_t nr,
                                                        const uint64_t* __restrict__ czp,
                                                        const uint64_t* __restrict__ nz, const V* __restrict__ in,
-                                                       V* __restrict__ out) {
+                                                       V* __restrict__ out, const uint32_t* __restrict__ rmap) {
   __shared__ uint32_t wsum[8];
   const uint64_t c = blockIdx.x;
-  const uint32_t r = rs_range_of_chunk(R, nr, c);
+  const uint32_t r = rmap[c];
   const RsRange rg = R[r];
   const uint64_t size = rg.hi - rg.lo;
   const uint64_t cs = (c - rg.chunk0) * kRsChunk;
@@ -158,7 +160,8 @@ __global__ void __launch_bounds__(256) rs_split_kernel(const RsRange* __restrict
 
 void launch_rs_level(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, uint64_t* cz, uint64_t* nz,
                      cudaStream_t st) {
-  rs_chunk_zeros_kernel<<<(unsigned)nchunks, 32, 0, st>>>(d_ranges, nr, cz);
+  // (cz holds 2 * nchunks words: the zero counts, then the chunk -> range map)
+  rs_chunk_zeros_kernel<<<(unsigned)nchunks, 32, 0, st>>>(d_ranges, nr, cz, reinterpret_cast<uint32_t*>(cz + nchunks));
   rs_range_scan_kernel<<<nr, 256, 0, st>>>(d_ranges, cz, nz);
   count_launch();
   count_launch();
@@ -167,12 +170,13 @@ void launch_rs_level(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchu
 
 void launch_rs_split(int eb, const RsRange* d_ranges, uint32_t nr, uint64_t nchunks, const uint64_t* czp,
                      const uint64_t* nz, const void* in, void* out, cudaStream_t st) {
+  const uint32_t* rmap = reinterpret_cast<const uint32_t*>(czp + nchunks);
   if (eb == 4)
     rs_split_kernel<uint32_t><<<(unsigned)nchunks, 256, 0, st>>>(d_ranges, nr, czp, nz, (const uint32_t*)in,
-                                                                  (uint32_t*)out);
+                                                                  (uint32_t*)out, rmap);
   else
     rs_split_kernel<unsigned long long><<<(unsigned)nchunks, 256, 0, st>>>(
-        d_ranges, nr, czp, nz, (const unsigned long long*)in, (unsigned long long*)out);
+        d_ranges, nr, czp, nz, (const unsigned long long*)in, (unsigned long long*)out, rmap);
   count_launch();
 }
 
