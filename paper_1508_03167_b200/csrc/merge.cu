@@ -816,24 +816,26 @@ __device__ __forceinline__ void merge_tree_tile(const Acc& acc, const PairPlan* 
       bytes = (l1 - l0) * (uint32_t)sizeof(V);
     }
   }
-  uint32_t sreg = reg, sgc = gc;
+  // one scan for three prefixes: staged elements, and packed in 16-bit halves
+  // the groups (low) and the ones of the windows before h (high) = the
+  // lengths of windows 1..h (|window w+1| = ones of window w below t).  No
+  // carry crosses the halves: a tile's group total is < 2^16 (big windows
+  // count none), and the high half is used only when the tile is staged
+  // (total length <= SCAP < 2^16).
+  uint32_t sreg = reg;
+  uint32_t spk = gc | ((lane >= 1 ? (uint32_t)min(len, (uint64_t)0xFFFFu) : 0u) << 16);
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y1 = __shfl_up_sync(0xffffffffu, sreg, o);
-    const uint32_t y2 = __shfl_up_sync(0xffffffffu, sgc, o);
-    if (lane >= (uint32_t)o) { sreg += y1; sgc += y2; }
+    const uint32_t y2 = __shfl_up_sync(0xffffffffu, spk, o);
+    if (lane >= (uint32_t)o) { sreg += y1; spk += y2; }
   }
+  const uint32_t sgc = spk & 0xFFFFu;
   const uint32_t treg = __shfl_sync(0xffffffffu, sreg, 31), tgc = __shfl_sync(0xffffffffu, sgc, 31);
   const uint32_t tby = __reduce_add_sync(0xffffffffu, bytes);  // TMA bytes (only the total is needed)
   const bool ok = nw < (uint32_t)kTreeD && !__any_sync(0xffffffffu, big) && treg <= C::SCAP && tgc <= C::GCAP &&
                   !g_tree_force_direct;
   const uint32_t r_stoff = sreg - reg + mis, r_goff = act ? sgc - gc : tgc;
-  // ones of the windows before h = sum of the lengths of windows 1..h
-  // (|window w+1| = ones of window w below t)
-  uint32_t r_onesb = lane >= 1 ? (uint32_t)len : 0u;
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, r_onesb, o);
-    if (lane >= (uint32_t)o) r_onesb += y;
-  }
+  const uint32_t r_onesb = spk >> 16;
   const uint32_t r_ilo = hi > lo ? lo : (uint32_t)len, r_ihi = hi > lo ? hi : (uint32_t)len;
   if (wid == 0) {
     if (lane < (uint32_t)kTreeD) {
