@@ -1087,9 +1087,28 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
       // from being hoisted out of the chunk loop into registers)
       V* dpass;
       asm volatile("mov.b64 %0, %1;" : "=l"(dpass) : "l"(dst + 2 * tid));
+      const bool pair8 = ((((uintptr_t)dst) & (2 * sizeof(V) - 1)) == 0) && s_stop < 8;
       // ... and the per-output source extraction from being hoisted likewise
 #pragma unroll
       for (int i = 0; i < (int)NP; ++i) asm volatile("" : "+r"(r[i]));
+      if (pair8) {
+        // a step pair whose two sources are in this chunk goes out as one
+        // 2-element store, otherwise the one present element singly
+#pragma unroll
+        for (int i = 0; i < (int)NP; ++i) {
+          const uint32_t s0 = (r[i] & 0xFFFFu) - c0, s1 = (r[i] >> 16) - c0;
+          const bool i0 = s0 < cn, i1 = s1 < cn;
+          if (i0 && i1) {
+            if constexpr (sizeof(V) == 4) {
+              *reinterpret_cast<uint2*>(dpass + 2 * BLOCK * i) = make_uint2(sdata[s0], sdata[s1]);
+            } else {
+              *reinterpret_cast<ulonglong2*>(dpass + 2 * BLOCK * i) = make_ulonglong2(sdata[s0], sdata[s1]);
+            }
+          } else if (i0 || i1) {
+            dpass[2 * BLOCK * i + (i1 ? 1 : 0)] = sdata[i1 ? s1 : s0];
+          }
+        }
+      } else {
 #pragma unroll
       for (int i = 0; i < (int)NP; ++i)
 #pragma unroll
@@ -1097,6 +1116,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
           const uint32_t src = ((r[i] >> (16 * h)) & 0xFFFFu) - c0;
           if (src < cn && s_stop != 10) dpass[2 * BLOCK * i + h] = s_stop == 8 ? (V)src : sdata[src];
         }
+      }
       __syncthreads();
     }
   }
