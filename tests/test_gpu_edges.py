@@ -37,7 +37,11 @@ def test_extreme_cutoffs(cutoff):
 
 
 def test_batched_odd_shapes():
-    for B, L, cutoff in [(3, 100_003, 1000), (7, 65_537, None), (1000, 1, None), (5, 2, 1)]:
+    # (2049..4096 / 4097..8192-element pure Fisher-Yates leaves: the small v3
+    # kernels in place; odd lengths: unaligned array starts)
+    for B, L, cutoff in [(3, 100_003, 1000), (7, 65_537, None), (1000, 1, None), (5, 2, 1),
+                         (333, 3001, None), (129, 4096, None), (65, 5003, None), (17, 8192, None),
+                         (9, 20_001, 2500)]:
         x = torch.arange(L, dtype=torch.int64, device="cuda").repeat(B, 1).contiguous()
         bits = sk.batched_shuffle(x, sk.ShuffleConfig(cutoff=cutoff), 77)
         ref, rbits = O.batched(B, L, cutoff if cutoff else 65536, 77)
