@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+ncu --set full --clock-control none --import-source on -k regex:merge_tree_kernel -s 20 -c 1 -o gpurun_out/tree -f python scripts/prof_run.py 30 1 > gpurun_out/ncu_tree.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:leaf_apply_v3 -s 1 -c 1 -o gpurun_out/leaf -f python scripts/prof_run.py 30 1 > gpurun_out/ncu_leaf.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu.log 2>&1
+echo done
