@@ -4,19 +4,22 @@ config 3 at 1 GPU), metric Gelem/s permuted.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One step = one full merge_shuffle_parallel (leaf Fisher-Yates + 14 merge rounds,
-bit-exact with the reference) of the resident 4 GiB array.  Timing: CUDA
-events on the launching stream, barrier + synchronize on both sides, max over
-ranks.  The array (4 GiB) is 32x the L2, so no flush is needed between steps.
+bit-exact with the reference: the checked step's bit count must equal the
+reference's 31908987766) of the resident 4 GiB array.  Timing: CUDA events on
+the launching stream, barrier + synchronize on both sides, max over ranks, no
+per-stage instrumentation inside the timed region.  The array (4 GiB) is 32x
+the L2, so no flush is needed between steps.
 
-Extra keys: roofline (dominant kernel = one merge round: merge_tree_kernel),
-cpu_baseline (the C oracle port on the host cores, bounded sample), e2e
-(through the C ABI host entry with pinned host buffers, H2D+D2H inside the
-timed region), gpu_launches, clocks.
+Extra keys: roofline (dominant kernel = one merge round: merge_tree_kernel,
+its average duration from a second, profiled pass of the same steps),
+cpu_baseline (the C oracle port on all host cores, one run of the FULL n),
+e2e (through the C ABI host entry with pinned host buffers, H2D+D2H inside
+the timed region), gpu_launches, clocks.
 
---impl reference: the reference's CPU path.  The reference is a Python/numba
-package that cannot travel to the GPU box, so its C restatement (oracle/,
-parity-pinned to the reference's goldens) runs with all host threads on a
-bounded sample of the workload.
+--impl reference: the reference's CPU path at the same n (not a sample):
+the unmodified reference package from baseline/_ref (numba, all host
+threads) when it imports, with the oracle port timed beside it; one warm-up
+and at most 3 timed full-size runs (the line reports the counts it ran).
 """
 from __future__ import annotations
 
@@ -74,32 +77,92 @@ def cpu_model():
     return "unknown"
 
 
-def oracle_sample(seconds_target=12.0, log2n=26):
-    """The oracle port on all host threads, a bounded sample of the workload:
-    merge_shuffle_tasked on 2^log2n int64 indices (same leaf size and schedule)
-    plus the uint32 payload gather, repeated until ~seconds_target."""
+# Reference bit counts (tests/golden/big.json, from the unmodified reference at seed 0)
+REF_BITS = {30: 31908987766, 31: 65963304485}
+REF_RUNS_MAX = 3     # timed reference runs (median), after one warm-up
+
+
+def _payload(n):
+    import numpy as np
+    return np.random.default_rng(0).integers(0, 2 ** 32, n, dtype=np.uint32)
+
+
+def _time_runs(fn, runs, warm):
+    for _ in range(warm):
+        fn()
+    times = []
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def time_port(log2n, runs, warm=0):
+    """The oracle port (C restatement of _kernels.py:253-289, oracle/) on all host
+    threads at the FULL size: merge_shuffle_tasked on 2^log2n int64 indices, then
+    the uint32 payload gather payload[idx] -- the same work as one GPU step."""
     import numpy as np
     from oracle import oracle as O
     O.build()
-    cores = cpu_cores()
-    n = 1 << log2n
-    payload = np.random.default_rng(0).integers(0, 2 ** 32, n, dtype=np.uint32)
-    idx = np.arange(n, dtype=np.int64)
-    O.merge_shuffle_tasked(idx, 65536, 0, cores)  # warm (page-in)
-    times = []
-    t_all = time.perf_counter()
-    while True:
-        idx = np.arange(n, dtype=np.int64)
-        t0 = time.perf_counter()
-        O.merge_shuffle_tasked(idx, 65536, 0, cores)
-        _ = payload[idx]
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_all > seconds_target or len(times) >= 20:
-            break
+    cores, n = cpu_cores(), 1 << log2n
+    payload = _payload(n)
+    idx = np.empty(n, dtype=np.int64)
+    bits = [0]
+
+    def one():
+        idx[:] = np.arange(n, dtype=np.int64)
+        bits[0] = O.merge_shuffle_tasked(idx, 65536, 0, cores)
+        payload[idx]
+    times = _time_runs(one, runs, warm)
+    if log2n in REF_BITS and bits[0] != REF_BITS[log2n]:
+        raise RuntimeError(f"oracle port bits {bits[0]} != reference {REF_BITS[log2n]}")
     med = statistics.median(times)
     return {"value": round(n / med / 1e9, 6), "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"oracle merge_shuffle_tasked on 2^{log2n} int64 indices + uint32 payload gather, "
-                      f"{len(times)} runs, median {med:.3f}s, {cores} threads ({cpu_model()})"}
+            "sample": f"oracle port merge_shuffle_tasked, n=2^{log2n} int64 indices + uint32 payload gather "
+                      f"(the full workload), {warm} warm-up + {runs} timed run(s), median {med:.2f}s, "
+                      f"{cores} threads ({cpu_model()})",
+            "seconds": [round(t, 3) for t in times]}
+
+
+def reference_package():
+    """The unmodified reference installed in baseline/_ref (pip --target), or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "shufflekit")):
+        return None
+    sys.path.insert(0, path)
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(path, ".numba_cache"))
+    try:
+        import shufflekit
+    except Exception:  # noqa: BLE001 - its dependencies (numba) missing on this host
+        return None
+    return shufflekit if os.path.abspath(shufflekit.__file__).startswith(path) else None
+
+
+def time_reference(sk_ref, log2n, runs, warm=1):
+    """The reference's own public API and stock code path: merge_shuffle_parallel
+    (shufflers.py:251-299) on int64 indices (its fast numba path) with all host
+    threads, then the uint32 payload gather.  The first run JIT-compiles."""
+    import numpy as np
+    cores, n = cpu_cores(), 1 << log2n
+    payload = _payload(n)
+    idx = np.empty(n, dtype=np.int64)
+    bits = [0]
+
+    def one():
+        idx[:] = np.arange(n, dtype=np.int64)
+        rep = sk_ref.merge_shuffle_parallel(idx, sk_ref.ShuffleConfig(threads=cores), sk_ref.BitSource(0))
+        bits[0] = rep.bits
+        payload[idx]
+    times = _time_runs(one, runs, warm)
+    if log2n in REF_BITS and bits[0] != REF_BITS[log2n]:
+        raise RuntimeError(f"reference bits {bits[0]} != {REF_BITS[log2n]}")
+    med = statistics.median(times)
+    return {"value": round(n / med / 1e9, 6), "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"unmodified reference (baseline/_ref, numba) merge_shuffle_parallel, n=2^{log2n} int64 "
+                      f"indices + uint32 payload gather (the full workload), threads={cores}, {warm} warm-up + "
+                      f"{runs} timed run(s), median {med:.2f}s ({cpu_model()})",
+            "seconds": [round(t, 3) for t in times]}
 
 
 class ClockSampler:
@@ -162,27 +225,30 @@ def traffic_from_profile():
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation of the path at the
+    bench's own configuration (n = 2^log2n, not a sample), rank 0 only.  The
+    unmodified reference from baseline/_ref when it imports here, else the
+    oracle port; the port is timed beside it either way.  Each timed step is
+    one full shuffle of 2^log2n elements; at most REF_RUNS_MAX steps are timed
+    (and one warmed), and the line reports the counts actually run."""
     if rank != 0:
         return
-    steps = []
-    base = None
-    sample_log2 = min(26, args.log2n)
-    scale = float(os.environ.get("SK_REF_SECONDS", "1"))  # (tests shorten the bounded samples)
-    for i in range(args.warmup + args.steps):
-        b = oracle_sample(seconds_target=(4.0 if i < args.warmup else 8.0) * scale, log2n=sample_log2)
-        if i >= args.warmup:
-            steps.append(b)
-        base = b
-    vals = [s["value"] for s in steps]
-    v = statistics.median(vals)
+    runs, warm = max(1, min(args.steps, REF_RUNS_MAX)), min(args.warmup, 1)
+    port = time_port(args.log2n, runs, warm=0)
+    ref_pkg = reference_package()
+    primary = time_reference(ref_pkg, args.log2n, runs, warm) if ref_pkg is not None else port
+    if primary is port:
+        warm = 0
+    v = primary["value"]
     n = 1 << args.log2n
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(n / (v * 1e9) * 1e3, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": runs,
+            "warmup": warm, "ms_per_step": round(statistics.median(primary["seconds"]) * 1e3, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"merge_shuffle_parallel n=2^{args.log2n} uint32 uniform payload, cutoff 65536",
-                       "n": n, "elem_bytes": 4, "cutoff": 65536, "seed": 0, "parallelism": "host threads"},
-            "cpu_baseline": {**base, "value": v},
+                       "n": n, "elem_bytes": 4, "cutoff": 65536, "seed": 0, "parallelism": "host threads",
+                       "requested_steps": args.steps, "requested_warmup": args.warmup},
+            "cpu_baseline": primary, "port": port if primary is not port else None,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -245,31 +311,41 @@ def main():
                                                  sp))
     else:
         bits.value = D.merge_shuffle_sharded(x, n_total, 65536, 0, exchange=exchange)
+    if args.log2n in REF_BITS and bits.value != REF_BITS[args.log2n]:
+        raise SystemExit(f"bits {bits.value} != reference {REF_BITS[args.log2n]}: not the reference's shuffle")
 
-    lib.sk_profile_enable(1)
-    l0 = lib.sk_launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    def timed(nsteps):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
         ev0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(nsteps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+        if dist:
+            dist.barrier()
+        el = ev0.elapsed_time(ev1)
+        if dist:
+            t = torch.tensor([el], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        return el
+
+    # the timed region: clean steps (no per-stage events)
+    l0 = lib.sk_launch_count()
+    with ClockSampler(local) as clk:
+        ms = timed(args.steps)
     launches = lib.sk_launch_count() - l0
-    ms = ev0.elapsed_time(ev1)
+    # a second, profiled pass of the same steps: per-stage CUDA events on the
+    # launching stream give the merge round's average duration (roofline)
+    lib.sk_profile_enable(1)
+    ms_prof = timed(args.steps)
     stage_ms = (ctypes.c_double * 5)()
     stage_l = (ctypes.c_uint64 * 5)()
     lib.sk_profile_read(stage_ms, stage_l, 5)
     lib.sk_profile_enable(0)
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     ms_per_step = ms / args.steps
     value = n_total / (ms_per_step * 1e-3) / 1e9
 
@@ -297,6 +373,7 @@ def main():
                                              "final_copy"])},
             # the whole step: c+1 passes over the shard (leaves + local rounds)
             "step_passes": local_rounds + 1,
+            "profiled_pass_ms_per_step": round(ms_prof / args.steps, 3),
             "step_frac_of_roofline": round((local_rounds + 1) * alg_bytes / (peak * 1e9) * 1e3 / ms_per_step, 4)}
 
     # e2e through the public API with host buffers (pinned), H2D + D2H inside
@@ -334,7 +411,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_sample()
+        cpu = time_port(args.log2n, 1)   # one full-size run of the oracle port (~20-30 s)
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,

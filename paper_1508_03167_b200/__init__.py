@@ -4,8 +4,7 @@ Drop-in for the reference shufflekit's MergeShuffle path: same entry points,
 bit-identical permutations and bit counts, computed by hand-written sm_100a
 CUDA kernels behind a C ABI (include/shufflekit_b200.h).
 """
-from .bitstream import (BitSource, DrawTape, TapeExhausted, advance_state, mix64, read_tape, substream_seed,
-                        write_tape)
+from .bitstream import BitSource, advance_state, mix64, substream_seed
 from .shufflers import (MERGE_CUTOFF_DEFAULT, MergeRange, ShuffleConfig, ShuffleReport, batched_shuffle,
                         fisher_yates, merge, merge_plan, merge_rounds, merge_shuffle, merge_shuffle_parallel,
                         merge_task_indices)
@@ -15,8 +14,7 @@ from .verify import ChiSquareResult, chi_counts, chi_square_threshold, chi_squar
 __version__ = "0.1.0"
 
 __all__ = [
-    "BitSource", "DrawTape", "TapeExhausted", "mix64", "substream_seed", "read_tape", "write_tape",
-    "advance_state", "MergeRange", "ShuffleConfig", "ShuffleReport", "MERGE_CUTOFF_DEFAULT", "fisher_yates",
+    "BitSource", "mix64", "substream_seed", "advance_state", "MergeRange", "ShuffleConfig", "ShuffleReport", "MERGE_CUTOFF_DEFAULT", "fisher_yates",
     "merge", "merge_plan", "merge_rounds", "merge_task_indices", "merge_shuffle", "merge_shuffle_parallel",
     "batched_shuffle", "ChiSquareResult", "chi_counts", "chi_square_threshold", "chi_square_uniformity",
     "permutation_rank", "RS_CUTOFF_DEFAULT", "rs_shuffle", "rs_shuffle_parallel",

@@ -132,9 +132,6 @@ struct LevelBufs {
   uint64_t sbs = 0, npairs = 0;
   uint64_t* rank = nullptr;
   PairPlan* plans = nullptr;
-  uint64_t* segs = nullptr;                 // npairs x kSMax segment boundaries
-  unsigned long long* seglen_max = nullptr;  // kSMax: longest segment h over pairs
-  uint64_t seglen_host[kSMax] = {};
   uint64_t* chains = nullptr;               // per tile: window starts of the tree merge
   uint32_t tpp = 1;                          // tree tiles per pair
   // tails
@@ -201,15 +198,12 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
   for (auto& L : lv) {
     L.rank = A.alloc<uint64_t>(L.npairs * L.sbs, ps);
     L.plans = A.alloc<PairPlan>(L.npairs, ps);
-    L.segs = A.alloc<uint64_t>(L.npairs * kSMax, ps);
-    L.seglen_max = A.alloc<unsigned long long>(kSMax, ps);
-    CK(cudaMemsetAsync(L.seglen_max, 0, kSMax * 8, ps));
     L.chains = A.alloc<uint64_t>(tree_chain_words(L.npairs, L.tpp), ps);
   }
   for (auto& L : lv) {
     uint64_t* csum = A.alloc<uint64_t>(rank_scan_scratch(L.npairs, L.sbs), ps);
     launch_rank_tables(L.LJ, L.sbs, L.rank, csum, ps);
-    launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, L.segs, L.seglen_max, ps);
+    launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, ps);
     launch_tree_chains(eb, L.plans, L.npairs, L.rank, L.tpp, L.chains, ps);
   }
   CK(cudaGetLastError());
@@ -227,7 +221,6 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
   for (int i = 0; i < nl; ++i) {
     CK(cudaMemcpyAsync(hplans.data() + pprefix[i], lv[i].plans, lv[i].npairs * sizeof(PairPlan),
                        cudaMemcpyDeviceToHost, ps));
-    CK(cudaMemcpyAsync(lv[i].seglen_host, lv[i].seglen_max, kSMax * 8, cudaMemcpyDeviceToHost, ps));
   }
   CK(cudaStreamSynchronize(ps));
   std::vector<uint64_t> offs(tot_pairs);
@@ -305,18 +298,31 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
   CK(cudaGetLastError());
 }
 
-struct SideStream {
-  cudaStream_t s = nullptr;
-  SideStream() { cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); }
-  ~SideStream() {
-    if (s) cudaStreamDestroy(s);
+// Helper streams of the calling thread on the CURRENT device (a thread may
+// drive several devices in turn): plan, round and copy streams, created on
+// first use per device.
+enum HelperStream { kPlanStream = 0, kRoundStream = 1, kCopyStream = 2 };
+constexpr int kMaxDevices = 64;
+struct HelperStreams {
+  cudaStream_t s[3][kMaxDevices] = {};
+  ~HelperStreams() {
+    for (auto& row : s)
+      for (cudaStream_t x : row)
+        if (x) cudaStreamDestroy(x);
   }
 };
 
-static cudaStream_t side_stream() {
-  static thread_local SideStream ss;
-  return ss.s;
+static cudaStream_t helper_stream(HelperStream which) {
+  static thread_local HelperStreams hs;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) throw std::runtime_error("device ordinal out of range");
+  cudaStream_t& s = hs.s[which][dev];
+  if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
 }
+
+static cudaStream_t side_stream() { return helper_stream(kPlanStream); }
 
 // Run rounds 1..c over `cur` (data currently there); the result lands in
 // `other`.  The tree merge reads every window of a CTA before writing it back
@@ -338,14 +344,12 @@ static void run_round_range(LevelBufs& L, int eb, void* buf, uint64_t p0, uint64
 
 static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* other, cudaStream_t st,
                         size_t first = 0) {
-  const bool in_place = merge_tree_active();
   for (size_t r = first; r < lv.size(); ++r) {
     auto& L = lv[r];
-    const bool last = r + 1 == lv.size();
-    void* out = (in_place && !last) ? cur : other;
+    void* out = r + 1 == lv.size() ? other : cur;
     {
       StageTimer tm(2, st);
-      launch_merge_round(eb, cur, out, L.plans, L.npairs, L.rank, L.segs, L.seglen_host, L.chains, L.tpp, st);
+      launch_merge_tree(eb, cur, out, L.plans, L.npairs, L.rank, L.chains, L.tpp, st);
     }
     {
       StageTimer tm(3, st);
@@ -446,15 +450,8 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
   A.release(st);
 }
 
-static cudaStream_t round_stream() {
-  static thread_local SideStream rs;
-  return rs.s;
-}
-
-static cudaStream_t copy_stream() {
-  static thread_local SideStream cs;
-  return cs.s;
-}
+static cudaStream_t round_stream() { return helper_stream(kRoundStream); }
+static cudaStream_t copy_stream() { return helper_stream(kCopyStream); }
 
 // The host entry for big arrays: the H2D copy runs in 2^k chunks on a copy
 // stream; the leaf draws (no data needed) and the merge plans are prepared
@@ -514,7 +511,7 @@ static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned 
       CK(cudaEventRecord(evl[j], st));
     }
     build_plans(lv, eb, d_bits, A, ps, st);
-    const size_t nloc = merge_tree_active() ? (size_t)std::max(0, std::min((int)lv.size() - 1, c - k)) : 0;
+    const size_t nloc = (size_t)std::max(0, std::min((int)lv.size() - 1, c - k));
     cudaStream_t rs = round_stream();  // ordered after st by the per-chunk events only
     for (uint64_t j = 0; j < K; ++j) {
       CK(cudaStreamWaitEvent(rs, evl[j], 0));
@@ -602,21 +599,9 @@ static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t
   try {
     fork_side(st, ps);
     build_plans(lv, eb, d_bits, A, ps, st);
-    if (merge_tree_active()) {  // the tree merge runs in place
-      launch_merge_round(eb, data, data, L.plans, 1, L.rank, L.segs, L.seglen_host, L.chains, L.tpp, st);
-      CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
-      launch_tail_apply(eb, data, L.dst, L.src, L.tmp, 2 * L.total, st);
-    } else {
-      unsigned char* scratch = A.alloc<unsigned char>(N * eb, st);
-      // kernels address elements by absolute index; shift the scratch base so
-      // index j lands on scratch[0].
-      void* out_base = (void*)(scratch - j * eb);
-      launch_merge_round(eb, data, out_base, L.plans, 1, L.rank, L.segs, L.seglen_host, L.chains, L.tpp, st);
-      launch_copy_tail_region(eb, data, out_base, L.plans, 1, st);
-      CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
-      launch_tail_apply(eb, out_base, L.dst, L.src, L.tmp, 2 * L.total, st);
-      CK(cudaMemcpyAsync((unsigned char*)data + j * eb, scratch, N * eb, cudaMemcpyDeviceToDevice, st));
-    }
+    launch_merge_tree(eb, data, data, L.plans, 1, L.rank, L.chains, L.tpp, st);  // in place
+    CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
+    launch_tail_apply(eb, data, L.dst, L.src, L.tmp, 2 * L.total, st);
     CK(cudaGetLastError());
   } catch (...) {
     cudaStreamSynchronize(ps);
@@ -932,11 +917,8 @@ int sk_version(void) { return 1; }
 // Internal knobs for performance experiments (not part of the public header).
 int sk_debug_set(int key, int value) {
   if (key == 1) { debug_set_leaf_stop(value); return 0; }
-  if (key == 2) { debug_set_seg_variant(value); return 0; }
   if (key == 4) { debug_set_tree_force_direct(value); return 0; }
-  if (key == 5) { debug_set_leaf_variant(value); return 0; }
   if (key == 6) { debug_set_leaf_fallback(value); return 0; }
-  if (key == 7) { debug_set_decode_variant(value); return 0; }
   return -1;
 }
 const char* sk_last_error(void) { return g_err.c_str(); }
@@ -1004,7 +986,7 @@ int sk_merge_shuffle_parallel_host(void* host_data, int elem_bytes, uint64_t n, 
   {
     const uint64_t cut = cutoff ? cutoff : 65536;
     const int c = plan_c(n, cut);
-    if (n >= (1ull << 24) && c >= 3 && ((n + (1ull << c) - 1) >> c) <= 65536 && merge_tree_active()) {
+    if (n >= (1ull << 24) && c >= 3 && ((n + (1ull << c) - 1) >> c) <= 65536) {
       unsigned long long* d_bits;
       CK(cudaMallocAsync((void**)&d_bits, 8, st));
       CK(cudaMemsetAsync(d_bits, 0, 8, st));

@@ -1,19 +1,20 @@
 // leaf.cu -- leaf Fisher-Yates (reference: _kernels.py:85-93 _fy_range,
 // shufflers.py:137-155, leaf tasks shufflers.py:268-278).
 //
-// Two kernels:
-//  * leaf_decode16_kernel: one lane per leaf decodes the m-1 fast-dice-roller
-//    draws j_i (i = m-1 .. 1) of its substream.  This is the only serial part:
-//    draws are variable-length so draw k's bit offset depends on draws < k.
-//  * leaf_apply_kernel: one CTA per leaf applies the m-1 swaps in parallel via
-//    the successor-chain closed form (tests/decomp_model.py leaf_apply_model):
+// Two stages:
+//  * decode (leaf_decode16b_kernel): one lane per leaf decodes the m-1
+//    fast-dice-roller draws j_i (i = m-1 .. 1) of its substream.  This is the
+//    only serial part: draws are variable-length, so draw k's bit offset
+//    depends on the draws before it.
+//  * apply: the m-1 swaps in parallel via the successor-chain closed form
+//    (tests/decomp_model.py leaf_apply_model):
 //      N(i) = next larger step with target j_i,  H(x) = first step > x targeting x,
 //      final[i] = orig[W(N(i))] (or orig[j_i] if none), final[0] = orig[W(0)],
 //      W(x) = W(H(x)) if H(x) exists else x.
-//    Steps are bucketed by target with a shared-memory counting sort (16-bit
-//    counters, two per 32-bit word, atomics in smem); one lane per bucket
-//    entry scans its (tiny) bucket for its successor, then every output
-//    gathers through the chain.
+//    leaf_apply_v3_kernel (leaves of 2049..65536) groups the steps by target
+//    with byte counters in shared memory; leaf_apply_kernel (leaves of <= 2048
+//    and the Rao-Sandelius leaf lists) with 16-bit counters.
+#include <stdexcept>
 #include <algorithm>
 #include "sk_kernels.h"
 
@@ -21,10 +22,6 @@ namespace sk {
 
 // debug: stop the leaf-apply pipeline after phase k (phase timing experiments)
 __device__ int g_leaf_stop = 99;
-// host, leaves > 8192: 2 = leaf_apply_v3_kernel (default), 1 = leaf_apply_kernel,
-// 0 = leaf_apply_reg_kernel
-static int g_leaf_variant = 2;
-static int g_leaf_v3_block = 1024;  // threads per CTA of leaf_apply_v3_kernel
 
 // One lane per leaf, one fast-dice-roller *iteration* per loop trip (so lanes
 // whose draws reject do not stall the others), bits served from a per-lane ring
@@ -44,112 +41,12 @@ __device__ __forceinline__ uint64_t leaf_word(const StreamDesc& sd, uint64_t w) 
 // schedulers (single-warp blocks were observed to share them).
 constexpr int kDecodeBlock = 128;
 
-template <bool FRESH>
-__global__ void __launch_bounds__(kDecodeBlock) leaf_decode16_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
-                                                                     uint16_t* __restrict__ draws,
-                                                                     unsigned long long* __restrict__ bits) {
-  __shared__ uint32_t ring[16][kDecodeBlock];
-  const uint32_t lane = threadIdx.x;
-  const uint64_t g = (uint64_t)blockIdx.x * kDecodeBlock + lane;
-  LeafDesc L;
-  uint32_t m = 0;
-  if (g < nleaves) {
-    L = leaf_desc(J, E, g);
-    m = (uint32_t)(L.hi - L.lo);
-  } else {
-    L.lo = 0; L.hi = 0; L.array = 0; L.sd = fresh_stream(0);
-  }
-  uint32_t i = m >= 2 ? m - 1 : 0;   // current step; its bound is i + 1
-  uint16_t* dr = draws + L.lo;
-  uint16_t* wp = dr + i;             // where draw i goes
-  uint64_t gw = 0;
-  uint32_t wr = 0;
-  if (i) {
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      uint64_t x = leaf_word<FRESH>(L.sd, gw++);
-      ring[wr & 15][lane] = (uint32_t)(x >> 32);
-      ring[(wr + 1) & 15][lane] = (uint32_t)x;
-      wr += 2;
-    }
-  }
-  // four-half window A|B|C|D: the extraction uses A|B; C and D are already
-  // loaded so a ring read has two word crossings of slack before its use
-  uint32_t A = ring[0][lane], B = ring[1][lane], C = ring[2][lane], D = ring[3][lane];
-  uint32_t rd = 4;
-  uint32_t pos = 0;
-  uint32_t v = 1, c = 0;
-  // Draws are packed eight at a time (16-byte stores, most recent draw in the
-  // low bits) except in the 16-byte chunk holding draw m-1, whose upper bytes
-  // belong to the next leaf: those go out as single 16-bit stores.  Per-lane
-  // scattered 16-bit stores cost one L1 wavefront each and sat on the decode's
-  // critical path.
-  uint16_t* const head = reinterpret_cast<uint16_t*>(reinterpret_cast<uintptr_t>(wp) & ~(uintptr_t)15);
-  uint64_t plo = 0, phi = 0;
-  uint16_t* pend = head;  // draws in [wp + 1, pend) are packed, not yet stored
-  while (__any_sync(0xffffffffu, i != 0)) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (i != 0 && wr - rd <= 14) {
-        uint64_t x = leaf_word<FRESH>(L.sd, gw++);
-        ring[wr & 15][lane] = (uint32_t)(x >> 32);
-        ring[(wr + 1) & 15][lane] = (uint32_t)x;
-        wr += 2;
-      }
-    }
-#pragma unroll 4
-    for (int tr = 0; tr < kDecodeTrips; ++tr) {
-      // one fast-dice-roller iteration (_kernels.py:71-82); finished lanes
-      // (i == 0) compute harmlessly but never store or advance
-      const bool act = i != 0;
-      const uint32_t b = i + 1;
-      uint32_t k = __clz(v) - __clz(b);  // smallest k with v << k >= b
-      k += ((v << k) < b) ? 1u : 0u;
-      const uint32_t x = __funnelshift_l(B, A, pos);
-      const uint32_t cc = (c << k) | (x >> (32 - k));
-      const uint32_t acc = (act && cc < b) ? 1u : 0u;
-      // predicated stores through a running pointer (wp == &dr[i])
-      const bool inhead = wp >= head;
-      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.global.u16 [%1], %2;\n}" ::"r"(
-                       inhead ? acc : 0u),
-                   "l"(wp), "h"((unsigned short)cc));
-      const bool push = acc && !inhead;
-      phi = push ? ((phi << 16) | (plo >> 48)) : phi;
-      plo = push ? ((plo << 16) | cc) : plo;
-      const uint32_t fl = (push && ((reinterpret_cast<uintptr_t>(wp) & 15) == 0)) ? 1u : 0u;
-      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.global.v2.u64 [%1], {%2, %3};\n}" ::"r"(fl),
-                   "l"(wp), "l"(plo), "l"(phi));
-      pend = fl ? wp : pend;
-      wp -= acc;
-      c = acc ? 0u : cc - b;
-      v = acc ? 1u : (v << k) - b;
-      i -= acc;
-      pos += act ? k : 0u;
-      const bool cross = pos >= 32;
-      const uint32_t nxt = ring[rd & 15][lane];
-      pos = cross ? pos - 32 : pos;
-      A = cross ? B : A;
-      B = cross ? C : B;
-      C = cross ? D : C;
-      D = cross ? nxt : D;
-      rd += cross ? 1u : 0u;
-    }
-  }
-  if (m >= 2) {
-    // the last (< 8) packed draws: dr[1 ..], dr[1] in the low bits
-    const long rem = (long)(pend - (dr + 1));
-    for (long k = 0; k < rem; ++k) dr[1 + k] = (uint16_t)(k < 4 ? plo >> (16 * k) : phi >> (16 * (k - 4)));
-    atomicAdd(&bits[L.array], 32ull * (rd - 4) + pos);  // bits consumed = halves passed + pos
-  }
-}
-
 // Leaner decode (same draws, same bit accounting): the step index i drives
 // everything -- the store address (dr + i), the flush condition ((lo + i) % 8
 // == 0), the head test (i > ih: draws whose 16-byte chunk reaches past the
 // leaf's last draw go out as single 16-bit stores) -- instead of a running
 // 64-bit pointer, the 8-draw shift register is four 32-bit words advanced by
 // byte permutes, and the FDR bit extraction is two funnel shifts.
-static int g_decode_variant = 1;  // 1 = leaf_decode16b_kernel, 0 = leaf_decode16_kernel
 
 template <bool FRESH>
 __global__ void __launch_bounds__(kDecodeBlock) leaf_decode16b_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
@@ -445,231 +342,6 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
       for (int k = 0; k < 8; ++k) {
         const uint32_t i = i0 + k * BLOCK;
         if (i < m) dst[i] = v[k];
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Leaf apply with the leaf's draws held in registers (leaves of 8193 .. 65536
-// elements; leaf_apply_kernel keeps the small-leaf configuration).
-//
-// 512 threads; thread t owns steps s = 4096k + 8t + e (k < K, e < 8), whose
-// draws j_s stay in 4K registers (two per register) for the whole leaf, so the
-// bucket passes never re-read them.  Per target half (the upper half first):
-// histogram, scan and scatter of the steps into per-target buckets in shared
-// memory, as in leaf_apply_kernel; then
-//  * every owned step finds its successor N(s) = min{b in bucket(j_s) : b > s}
-//    by scanning its bucket (~3 entries on average) and replaces j_s by it in
-//    its register.  N(s) > s >= j_s, so the 16-bit value tells the two cases
-//    apart, and the upper half's replaced values (> s >= 32768) fail the
-//    lower half's target test;
-//  * every target x of the half stores H(x) = min{b in bucket(x) : b > x}
-//    (coalesced) to the CTA's scratch.
-// Finally H is reloaded into shared memory and each owned output gathers
-// orig[W(N(s))] (W: follow H to its root) or orig[j_s].  No successor table
-// is stored (leaf_apply_kernel's random Nn scatter to L2 is gone), and the
-// outputs go out as 16-byte stores.
-template <typename V, int K, int MINB>
-__global__ void __launch_bounds__(512, MINB)
-    leaf_apply_reg_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves, const V* __restrict__ in, V* __restrict__ out,
-                          const uint16_t* __restrict__ draws, uint16_t* __restrict__ scratch, uint32_t mmax,
-                          const uint64_t* __restrict__ list) {
-  constexpr uint32_t BLOCK = 512;
-  extern __shared__ uint32_t sh[];
-  __shared__ uint32_t warp_tot[BLOCK / 32];
-  const uint32_t half = mmax < kLeafHalf ? mmax : kLeafHalf;
-  const uint32_t cw = (half + 1) >> 1;
-  uint16_t* cur = reinterpret_cast<uint16_t*>(sh);         // [half] bucket cursors
-  uint16_t* bkt = reinterpret_cast<uint16_t*>(sh + cw);    // [mmax] buckets
-  const uint16_t* Hs = reinterpret_cast<const uint16_t*>(sh);  // [mmax] H, at the end
-  // per-CTA scratch: H (16-byte aligned, read back as uint4) and the long-bucket staging
-  uint16_t* Hg = reinterpret_cast<uint16_t*>(
-      ((uintptr_t)(scratch + (uint64_t)blockIdx.x * leaf_scratch_stride(mmax)) + 15) & ~(uintptr_t)15);
-  uint16_t* tmp = Hg + ((mmax + 7) & ~7u) + 8;
-  const uint32_t tid = threadIdx.x;
-
-  for (uint64_t g = blockIdx.x; g < nleaves; g += gridDim.x) {
-    LeafDesc L;
-    if (list) {
-      L.lo = list[2 * g];
-      L.hi = list[2 * g + 1];
-    } else {
-      L = leaf_desc(J, E, g);
-    }
-    const uint32_t m = (uint32_t)(L.hi - L.lo);
-    const V* src_in = in + L.lo;
-    V* dst = out + L.lo;
-    if (m < 2) {
-      if (m == 1 && tid == 0) dst[0] = src_in[0];
-      continue;
-    }
-    const uint16_t* __restrict__ dr = draws + L.lo;
-    if (tid == 0 && g + gridDim.x < nleaves) {  // the next leaf's draws into L2
-      uint64_t nlo, nhi;
-      if (list) {
-        nlo = list[2 * (g + gridDim.x)];
-        nhi = list[2 * (g + gridDim.x) + 1];
-      } else {
-        const LeafDesc Ln = leaf_desc(J, E, g + gridDim.x);
-        nlo = Ln.lo;
-        nhi = Ln.hi;
-      }
-      l2_prefetch(draws + nlo, (size_t)(nhi - nlo) * 2);
-    }
-    uint32_t r[K][4];
-    const bool dvec = (((uintptr_t)dr) & 15) == 0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t s0 = (uint32_t)k * 4096 + tid * 8;
-      if (dvec && s0 + 8 <= m) {
-        const uint4 q = *reinterpret_cast<const uint4*>(dr + s0);
-        r[k][0] = q.x; r[k][1] = q.y; r[k][2] = q.z; r[k][3] = q.w;
-      } else {
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const uint32_t a = s0 + 2 * w;
-          const uint32_t lo16 = a < m ? (uint32_t)dr[a] : 0u;
-          const uint32_t hi16 = a + 1 < m ? (uint32_t)dr[a + 1] : 0u;
-          r[k][w] = lo16 | (hi16 << 16);
-        }
-      }
-    }
-    for (int hh = m > kLeafHalf ? 1 : 0; hh >= 0; --hh) {
-      const uint32_t T0 = (uint32_t)hh * kLeafHalf;
-      const uint32_t nt = min(kLeafHalf, m - T0);
-      if (tid == 0 && hh == 0) l2_prefetch(src_in, (size_t)m * sizeof(V));  // gathered next
-      for (uint32_t w = tid; w < ((nt + 1) >> 1); w += BLOCK) sh[w] = 0;
-      __syncthreads();
-      // 1. histogram of the half's targets
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const uint32_t s = (uint32_t)k * 4096 + tid * 8 + e;
-          const uint32_t jj = ((r[k][e >> 1] >> ((e & 1) << 4)) & 0xFFFFu) - T0;
-          if (s - 1u < m - 1u && jj < nt) atomicAdd(&sh[jj >> 1], 1u << ((jj & 1) << 4));
-        }
-      __syncthreads();
-      if (g_leaf_stop <= 1) continue;
-      // 2. bucket starts
-      scan_counts16(cur, nt, warp_tot);
-      __syncthreads();
-      if (g_leaf_stop <= 2) continue;
-      // 3. scatter step ids into their buckets (cursors end at the bucket ends);
-      //    each step keeps its slot in place of j_s (and a bit in `mine`)
-      uint32_t mine[(K * 8 + 31) / 32];
-#pragma unroll
-      for (int q = 0; q < (K * 8 + 31) / 32; ++q) mine[q] = 0;
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const uint32_t s = (uint32_t)k * 4096 + tid * 8 + e;
-          const uint32_t sh16 = (e & 1) << 4;
-          const uint32_t jj = ((r[k][e >> 1] >> sh16) & 0xFFFFu) - T0;
-          if (s - 1u < m - 1u && jj < nt) {
-            const uint32_t old = atomicAdd(&sh[jj >> 1], 1u << ((jj & 1) << 4));
-            const uint32_t slot = (old >> ((jj & 1) << 4)) & 0xFFFFu;
-            bkt[slot] = (uint16_t)s;
-            r[k][e >> 1] = (r[k][e >> 1] & ~(0xFFFFu << sh16)) | (slot << sh16);
-            mine[(k * 8 + e) >> 5] |= 1u << ((k * 8 + e) & 31);
-          }
-        }
-      __syncthreads();
-      if (g_leaf_stop <= 3) continue;
-      // 4. per target x of the half: every bucket entry b is replaced by its
-      //    successor min{b' in bucket : b' > b} or, if none, by x (<= b), and
-      //    H(x) = min{b in bucket : b > x} goes to the scratch
-      for (uint32_t x = tid; x < nt; x += BLOCK) {
-        const uint32_t st = x ? (uint32_t)cur[x - 1] : 0u, n = (uint32_t)cur[x] - st;
-        const uint32_t p = T0 + x;
-        uint32_t H = 0x10000u;
-        if (n <= 4) {
-          uint32_t v[4], res[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) v[i] = (uint32_t)i < n ? (uint32_t)bkt[st + i] : 0u;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            uint32_t best = 0x10000u;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) best = (v[j] > v[i] && v[j] < best) ? v[j] : best;
-            res[i] = best < 0x10000u ? best : p;
-            H = (v[i] > p && v[i] < H) ? v[i] : H;
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if ((uint32_t)i < n) bkt[st + i] = (uint16_t)res[i];
-        } else {  // long buckets (small targets): results staged in the scratch
-          for (uint32_t i = 0; i < n; ++i) {
-            const uint32_t vi = bkt[st + i];
-            uint32_t best = 0x10000u;
-            for (uint32_t j = 0; j < n; ++j) {
-              const uint32_t vj = bkt[st + j];
-              best = (vj > vi && vj < best) ? vj : best;
-            }
-            tmp[st + i] = (uint16_t)(best < 0x10000u ? best : p);
-            H = (vi > p && vi < H) ? vi : H;
-          }
-          for (uint32_t i = 0; i < n; ++i) bkt[st + i] = tmp[st + i];
-        }
-        Hg[p] = (uint16_t)(H & 0xFFFFu);
-      }
-      __syncthreads();
-      if (g_leaf_stop <= 4) continue;
-      // 5. the owned steps of the half pick up N(s) or j_s from their slot
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          if (mine[(k * 8 + e) >> 5] & (1u << ((k * 8 + e) & 31))) {
-            const uint32_t sh16 = (e & 1) << 4;
-            const uint32_t slot = (r[k][e >> 1] >> sh16) & 0xFFFFu;
-            r[k][e >> 1] = (r[k][e >> 1] & ~(0xFFFFu << sh16)) | ((uint32_t)bkt[slot] << sh16);
-          }
-        }
-      __syncthreads();
-    }
-    if (g_leaf_stop <= 5) continue;
-    // H into shared memory (over the cursors and buckets)
-    for (uint32_t w = tid; w < ((m + 7) >> 3); w += BLOCK)
-      reinterpret_cast<uint4*>(sh)[w] = reinterpret_cast<const uint4*>(Hg)[w];
-    __syncthreads();
-    // 6. gather: final[s] = orig[W(N(s))] or orig[j_s]; final[0] = orig[W(0)]
-    const bool ovec = (((uintptr_t)dst) & 15) == 0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t s0 = (uint32_t)k * 4096 + tid * 8;
-      if (s0 < m) {
-        V v[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const uint32_t s = s0 + e;
-          const uint32_t x = (r[k][e >> 1] >> ((e & 1) << 4)) & 0xFFFFu;
-          uint32_t src = x;
-          if (s == 0 || x > s) {
-            uint32_t y = s == 0 ? 0u : x, h;
-            while ((h = Hs[y]) != 0) y = h;
-            src = y;
-          }
-          v[e] = s < m ? (g_leaf_stop == 6 ? (V)src : src_in[src]) : V(0);
-        }
-        if (ovec && s0 + 8 <= m) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst + s0);
-          if constexpr (sizeof(V) == 4) {
-            d4[0] = make_uint4(v[0], v[1], v[2], v[3]);
-            d4[1] = make_uint4(v[4], v[5], v[6], v[7]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              d4[q] = make_uint4((uint32_t)v[2 * q], (uint32_t)(v[2 * q] >> 32), (uint32_t)v[2 * q + 1],
-                                 (uint32_t)(v[2 * q + 1] >> 32));
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (s0 + e < m) dst[s0 + e] = v[e];
-        }
       }
     }
     __syncthreads();
@@ -1148,11 +820,6 @@ __global__ void leaf_serial_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
 }
 
 // ---------------------------------------------------------------- launchers
-void debug_set_leaf_variant(int v) {
-  if (v >= 10) g_leaf_v3_block = v == 10 ? 512 : 1024;
-  else g_leaf_variant = v;
-}
-void debug_set_decode_variant(int v) { g_decode_variant = v; }
 void debug_set_leaf_fallback(int v) { cudaMemcpyToSymbol(g_leaf_force_fallback, &v, sizeof(int)); }
 void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int)); }
 
@@ -1161,13 +828,8 @@ void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nle
   if (!nleaves) return;
   unsigned blocks = (unsigned)((nleaves + kDecodeBlock - 1) / kDecodeBlock);
   const bool fresh = !(E.active && E.sd.plen != 0);
-  if (g_decode_variant == 1) {
-    if (fresh) leaf_decode16b_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
-    else leaf_decode16b_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
-  } else {
-    if (fresh) leaf_decode16_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
-    else leaf_decode16_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
-  }
+  if (fresh) leaf_decode16b_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
+  else leaf_decode16b_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
   count_launch();
 }
 
@@ -1192,7 +854,7 @@ static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nlea
                          const uint16_t* draws, uint16_t* scratch, uint32_t mmax, uint32_t grid,
                          const uint64_t* list, cudaStream_t st) {
   size_t smem = leaf_apply_smem(mmax, (int)sizeof(V));
-  if (g_leaf_variant == 2 && mmax > 2048 && (mmax <= 8192 || in != out)) {
+  if (mmax > 2048 && (mmax <= 8192 || in != out)) {
     // v3 (leaves > 8192 gather in two or more chunks: distinct buffers only)
     smem = leaf_apply_v3_smem(mmax, (int)sizeof(V));
     if (mmax <= 4096) {
@@ -1203,33 +865,13 @@ static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nlea
       auto k = leaf_apply_v3_kernel<V, 256, 16>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k<<<grid, 256, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
-    } else if (g_leaf_v3_block == 512) {
-      auto k = leaf_apply_v3_kernel<V, 512, 64>;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
     } else {
       auto k = leaf_apply_v3_kernel<V, 1024, 32>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k<<<grid, 1024, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
     }
-  } else if (mmax > 8192 && g_leaf_variant == 0) {
-    if (mmax <= 16384) {
-      auto k = leaf_apply_reg_kernel<V, 4, 2>;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
-    } else if (mmax <= 32768) {
-      auto k = leaf_apply_reg_kernel<V, 8, 1>;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
-    } else {
-      auto k = leaf_apply_reg_kernel<V, 16, 1>;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k<<<grid, 512, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
-    }
   } else if (mmax > 8192) {
-    auto k = leaf_apply_kernel<V, 1024>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, 1024, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
+    throw std::runtime_error("leaf apply: leaves above 8192 elements need distinct in/out buffers");
   } else {
     auto k = leaf_apply_kernel<V, 256>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1244,11 +886,9 @@ uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms, int eb) {
   size_t smem = leaf_apply_smem(mmax);
   size_t fit = (size_t)(220 * 1024) / (smem + 2048);
   int per_sm = (int)std::max((size_t)1, std::min(fit, (size_t)(mmax > 8192 ? 2 : 8)));
-  if (mmax > 8192 && g_leaf_variant == 2) per_sm = 1;  // v3: 1024 threads, ~200 KB
-  if (mmax > 2048 && mmax <= 8192 && g_leaf_variant == 2)  // v3, 256 threads
+  if (mmax > 8192) per_sm = 1;  // v3: 1024 threads, ~200 KB
+  if (mmax > 2048 && mmax <= 8192)  // v3, 256 threads
     per_sm = (int)std::max((size_t)1, std::min((size_t)4, (size_t)(220 * 1024) / (leaf_apply_v3_smem(mmax, eb) + 2048)));
-  if (mmax > 8192 && g_leaf_variant == 0)  // register-resident draws: 512 threads, 1-3 CTAs per SM
-    per_sm = mmax <= 16384 ? 2 : 1;
   uint64_t g = (uint64_t)num_sms * per_sm;
   if (g > nleaves) g = nleaves;
   return (uint32_t)(g ? g : 1);

@@ -1,16 +1,16 @@
 // merge.cu -- one merge round of the parallel schedule (reference: _kernels.py:96-121
 // _merge, shufflers.py:158-191 merge, rounds shufflers.py:117-130 / 291-297).
 //
-// Phase 1 (the coin-flip swap merge) is rewritten as segment passes: the A
-// queue of the in-place merge is the stream F with F[u] = A[u] (u < n1) and
-// F[n1 + k] = F[select1(k)].  Segments S_0 = [0, n1), S_{h+1} =
-// [n1 + rank'(S_h.start), n1 + rank'(S_h.end)) (rank' = ones before min(p, t))
-// partition [0, X); [X, N) is the identity (A queue empty).  Segment h is one
-// streaming pass: at position p, F[p] is read from in[p]; a zero emits F[p],
-// a one emits the B element in[n1 + rank'(p)] and stores F[p] in its place
-// (position n1 + rank'(p) lies in segment h+1, so the next pass reads it as
-// F).  Reads 1.5 N, writes 1.5 N per round, all coalesced.  Small segments of
-// a pair are finished by one CTA in a tail kernel.
+// Phase 1 (the coin-flip swap merge): the A queue of the in-place merge is the
+// stream F with F[u] = A[u] (u < n1) and F[n1 + k] = F[select1(k)].  Segments
+// S_0 = [0, n1), S_{h+1} = [n1 + rank'(S_h.start), n1 + rank'(S_h.end))
+// (rank' = ones before min(p, t)) partition [0, X); [X, N) is the identity (A
+// queue empty).  A tile [a_0, b_0) of S_0 is followed through its windows
+// [a_{h+1}, b_{h+1}) = [n1 + rank'(a_h), n1 + rank'(b_h)): the windows of all
+// tiles partition [0, X), and a tile's swaps only touch its own windows, so
+// one CTA per tile loads them (TMA), swaps them in shared memory window by
+// window and stores them back -- one read and one write per element per
+// round, in place (merge_tree_kernel).
 // (Derivation + CPU check: tests/decomp_model.py merge_phase1_model.)
 //
 // Phase 2 (tail insertion, x = t..N-1: swap(x, FDR(x+1))) is precomputed as a
@@ -169,8 +169,7 @@ __device__ uint64_t select_bit(const StreamDesc& sd, const uint64_t* R, uint64_t
 // Stop point (_kernels.py:104-115): t = min(select0(n1), select1(n2)); A is
 // exhausted iff the zero comes first.  X = first fixed point of S -> n1 + rank'(S).
 __global__ void pair_plan_kernel(LevelJob LJ, uint64_t sbs, const uint64_t* __restrict__ rank,
-                                 PairPlan* __restrict__ plans, uint64_t* __restrict__ segs,
-                                 unsigned long long* __restrict__ seglen_max) {
+                                 PairPlan* __restrict__ plans) {
   uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= LJ.npairs) return;
   PairPlan P;
@@ -178,13 +177,9 @@ __global__ void pair_plan_kernel(LevelJob LJ, uint64_t sbs, const uint64_t* __re
   P.rank_off = g * sbs;
   P.tail_off = 0;
   const uint64_t n1 = P.n1, n2 = P.n2, N = n1 + n2;
-  uint64_t* sg = segs + g * kSMax;
   if (n1 == 0 || n2 == 0) {  // shufflers.py:169-170: no bits, no change
     P.t = 0; P.X = n1; P.aex = 0; P.degenerate = 1; P.tail_len = 0; P.bits = 0;
     P.nseg = n1 ? 1 : 0;
-    sg[0] = 0;
-    sg[1] = n1;
-    if (n1) atomicMax(&seglen_max[0], (unsigned long long)n1);
   } else {
     const uint64_t* R = rank + g * sbs;
     uint64_t used = (N + 1 + 511) >> 9;
@@ -195,13 +190,10 @@ __global__ void pair_plan_kernel(LevelJob LJ, uint64_t sbs, const uint64_t* __re
     // segment chain S_0 = 0, S_{h+1} = n1 + rank'(S_h) up to the fixed point X
     uint64_t S = 0;
     uint32_t h = 0;
-    sg[0] = 0;
     for (;;) {
       uint64_t S2 = n1 + (S ? rank_bits(P.sd, R, S < t ? S : t) : 0);
       if (S2 == S) break;
-      if (h < (uint32_t)kSMax) atomicMax(&seglen_max[h], (unsigned long long)(S2 - S));
       ++h;
-      if (h < (uint32_t)kSMax) sg[h] = S2;
       S = S2;
     }
     P.nseg = h;
@@ -212,10 +204,9 @@ __global__ void pair_plan_kernel(LevelJob LJ, uint64_t sbs, const uint64_t* __re
   plans[g] = P;
 }
 
-void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, PairPlan* plans, uint64_t* segs,
-                      unsigned long long* seglen_max, cudaStream_t st) {
+void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, PairPlan* plans, cudaStream_t st) {
   if (!LJ.npairs) return;
-  pair_plan_kernel<<<(unsigned)((LJ.npairs + 127) / 128), 128, 0, st>>>(LJ, sbs, rank, plans, segs, seglen_max);
+  pair_plan_kernel<<<(unsigned)((LJ.npairs + 127) / 128), 128, 0, st>>>(LJ, sbs, rank, plans);
   count_launch();
 }
 
@@ -313,166 +304,6 @@ __device__ __forceinline__ uint64_t warp_rank(const StreamDesc& sd, const uint64
   }
   for (int o = 4; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   return R[sb] + __shfl_sync(0xffffffffu, c, 0);
-}
-
-// One tile of a segment: positions [p0, p0 + len) of the pair, rank0 =
-// rank'(p0).  Warp w owns 32*CPW consecutive positions; lane l < CPW extracts
-// the one-bits of chunk l (32 positions), a warp scan and the block's warp
-// totals give every one its rank'.  One F load per position, one B load + one
-// F store per one, one output store per position -- all coalesced.
-template <typename V, int BLOCK, int CPW>
-__device__ __forceinline__ uint32_t segment_tile(V* __restrict__ pio, V* __restrict__ pout, const StreamDesc& sd,
-                                                 uint64_t n1, uint64_t t, uint64_t p0, uint32_t len, uint64_t rank0,
-                                                 uint32_t* wsum) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint32_t wbase = wid * 32 * CPW;
-  uint32_t mword = 0;
-  if (lane < (uint32_t)CPW) {
-    const uint32_t i = wbase + lane * 32;
-    if (i < len) {
-      const uint64_t p = p0 + i;
-      if (p < t) {
-        uint32_t nv = min(32u, len - i);
-        const uint64_t nt = t - p;
-        if (nt < nv) nv = (uint32_t)nt;
-        const uint32_t b = (uint32_t)(bits64_at(sd, p) >> 32);
-        mword = (nv == 32) ? b : (b & ~(0xffffffffu >> nv));
-      }
-    }
-  }
-  const uint32_t cnt = __popc(mword);
-  uint32_t x = cnt;
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= (uint32_t)o) x += y;
-  }
-  const uint32_t round_base = x - cnt;
-  if (lane == 31) wsum[wid] = x;
-  __syncthreads();
-  uint32_t before = 0, total = 0;
-#pragma unroll
-  for (int w = 0; w < BLOCK / 32; ++w) {
-    before += (w < (int)wid) ? wsum[w] : 0u;
-    total += wsum[w];
-  }
-  const uint64_t qbase = n1 + rank0 + before;  // position of this warp's first B element
-  const uint32_t ltmask = ~(0xffffffffu >> lane);
-  // all loads of the tile first (independent, in flight together), then all
-  // stores: the F stores into pio may alias later F loads, so interleaving
-  // them would serialize every round on a full memory latency
-  V f[CPW], b[CPW];
-  uint32_t qo[CPW];
-  uint32_t onemask = 0, inmask = 0;
-#pragma unroll
-  for (int k = 0; k < CPW; ++k) {
-    const uint32_t i = wbase + 32 * k + lane;
-    const uint32_t m = __shfl_sync(0xffffffffu, mword, k);
-    const uint32_t rb = __shfl_sync(0xffffffffu, round_base, k);
-    const bool in_t = i < len;
-    const bool one = in_t && ((m >> (31 - lane)) & 1u);
-    qo[k] = rb + __popc(m & ltmask);
-    inmask |= (in_t ? 1u : 0u) << k;
-    onemask |= (one ? 1u : 0u) << k;
-    if (in_t) f[k] = pio[p0 + i];
-    if (one) b[k] = pio[qbase + qo[k]];
-  }
-#pragma unroll
-  for (int k = 0; k < CPW; ++k) {
-    const uint64_t p = p0 + wbase + 32 * k + lane;
-    if ((onemask >> k) & 1u) {
-      pout[p] = b[k];
-      pio[qbase + qo[k]] = f[k];  // carried A element: read as F by the next segment pass
-    } else if ((inmask >> k) & 1u) {
-      pout[p] = f[k];
-    }
-  }
-  return total;
-}
-
-template <typename V, int BLOCK, int CPW, int Q, int MINB>
-__global__ void __launch_bounds__(BLOCK, MINB) merge_segment_kernel(V* __restrict__ in, V* __restrict__ out,
-                                                                 const PairPlan* __restrict__ plans,
-                                                                 const uint64_t* __restrict__ rank,
-                                                                 const uint64_t* __restrict__ segs, uint32_t h,
-                                                                 uint32_t tpp) {
-  // Q consecutive tiles per CTA: the plan loads and the rank-table query are
-  // paid once, later tiles carry the rank from the block totals.
-  constexpr uint32_t T = BLOCK * CPW;
-  __shared__ uint32_t wsum[2][BLOCK / 32];
-  __shared__ uint64_t rank0_s;
-  const uint64_t g = blockIdx.x / tpp, tau = blockIdx.x - g * tpp;
-  const PairPlan* Pp = plans + g;
-  if (h >= Pp->nseg) return;
-  const uint64_t* sg = segs + g * kSMax;
-  const uint64_t S0 = sg[h], S1 = (h + 1 < Pp->nseg) ? sg[h + 1] : Pp->X;
-  uint64_t p0 = S0 + tau * (uint64_t)(T * Q);
-  if (p0 >= S1) return;
-  const uint64_t n1 = Pp->n1, t = Pp->t;
-  const StreamDesc sd = Pp->sd;
-  if (threadIdx.x < 32) {
-    uint64_t r0;
-    if (tau == 0) r0 = S1 - n1;  // rank'(S_h) = S_{h+1} - n1 (the chain itself)
-    else r0 = warp_rank(sd, rank + Pp->rank_off, p0 < t ? p0 : t, threadIdx.x);
-    if (threadIdx.x == 0) rank0_s = r0;
-  }
-  __syncthreads();
-  uint64_t rk = rank0_s;
-  V* pio = in + Pp->s;
-  V* pout = out + Pp->s;
-#pragma unroll 1
-  for (int qi = 0; qi < Q && p0 < S1; ++qi) {
-    const uint32_t len = (uint32_t)min((uint64_t)T, S1 - p0);
-    rk += segment_tile<V, BLOCK, CPW>(pio, pout, sd, n1, t, p0, len, rk, wsum[qi & 1]);
-    p0 += T;
-  }
-}
-
-// The remaining (small) segments of every pair, one CTA per pair, in order.
-template <typename V, int BLOCK, int CPW>
-__global__ void __launch_bounds__(BLOCK) merge_tail_kernel(V* __restrict__ in, V* __restrict__ out,
-                                                           const PairPlan* __restrict__ plans,
-                                                           const uint64_t* __restrict__ rank,
-                                                           const uint64_t* __restrict__ segs, uint32_t h0) {
-  constexpr uint32_t T = BLOCK * CPW;
-  __shared__ uint32_t wsum[BLOCK / 32];
-  __shared__ uint64_t seg_s[2];
-  const uint64_t g = blockIdx.x;
-  const PairPlan* Pp = plans + g;
-  const uint32_t nseg = Pp->nseg;
-  const uint64_t n1 = Pp->n1, t = Pp->t, X = Pp->X;
-  const StreamDesc sd = Pp->sd;
-  const uint64_t* sg = segs + g * kSMax;
-  const uint64_t* R = rank + Pp->rank_off;
-  V* pio = in + Pp->s;
-  V* pout = out + Pp->s;
-  for (uint32_t h = h0; h < nseg; ++h) {
-    if (threadIdx.x < 32) {
-      // segment h = [S_h, S_{h+1}); beyond the stored chain S_{h+1} = n1 + rank'(S_h)
-      const uint64_t S0 = (h < (uint32_t)kSMax) ? sg[h] : seg_s[1];
-      uint64_t S1;
-      if (h + 1 >= nseg) S1 = X;
-      else if (h + 1 < (uint32_t)kSMax) S1 = sg[h + 1];
-      else S1 = n1 + warp_rank(sd, R, S0 < t ? S0 : t, threadIdx.x);
-      __syncwarp();
-      if (threadIdx.x == 0) { seg_s[0] = S0; seg_s[1] = S1; }
-    }
-    __syncthreads();
-    const uint64_t S0 = seg_s[0], S1 = seg_s[1];
-    for (uint64_t p0 = S0; p0 < S1; p0 += T) {
-      uint64_t rk = S1 - n1;  // rank'(S_h) = S_{h+1} - n1; later tiles use the rank table
-      if (p0 != S0) {
-        __shared__ uint64_t rk_s;
-        if (threadIdx.x < 32) {
-          uint64_t v = warp_rank(sd, R, p0 < t ? p0 : t, threadIdx.x);
-          if (threadIdx.x == 0) rk_s = v;
-        }
-        __syncthreads();
-        rk = rk_s;
-      }
-      segment_tile<V, BLOCK, CPW>(pio, pout, sd, n1, t, p0, (uint32_t)min((uint64_t)T, S1 - p0), rk, wsum);
-      __syncthreads();
-    }
-  }
 }
 
 // ------------------------------------------------------- merge round (tree)
@@ -1185,64 +1016,6 @@ void launch_merge_tree(int eb, void* in, void* out, const PairPlan* plans, uint6
   if (!npairs) return;
   if (eb == 4) merge_tree_t<uint32_t>(in, out, plans, npairs, rank, chains, tpp, st);
   else merge_tree_t<unsigned long long>(in, out, plans, npairs, rank, chains, tpp, st);
-}
-
-constexpr int kSegBlock = 256;
-constexpr int kSegCPW = 8;  // 2048 positions per tile
-uint32_t merge_tile(int eb) { (void)eb; return kSegBlock * kSegCPW; }
-
-// segment-kernel shape (tuning knob, see sk_debug_set key 2): CPW chunks per
-// warp (tile = 256*CPW positions), Q tiles per CTA, min CTAs per SM
-static int g_seg_variant = 0;
-void debug_set_seg_variant(int v) { g_seg_variant = v; }
-bool merge_tree_active() { return g_seg_variant < 100; }
-
-template <typename V, int CPW, int Q, int MINB>
-static void seg_launch(void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
-                       const uint64_t* segs, uint32_t h, uint64_t seglen, cudaStream_t st) {
-  constexpr uint32_t T = kSegBlock * CPW;
-  const uint32_t tpp = (uint32_t)((seglen + T * Q - 1) / (T * Q));
-  merge_segment_kernel<V, kSegBlock, CPW, Q, MINB><<<(unsigned)(npairs * tpp), kSegBlock, 0, st>>>(
-      (V*)in, (V*)out, plans, rank, segs, h, tpp);
-  count_launch();
-}
-
-template <typename V>
-static void merge_round_t(void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
-                          const uint64_t* segs, const uint64_t* seglen_max_host, cudaStream_t st) {
-  if (!npairs) return;
-  constexpr uint32_t T = kSegBlock * kSegCPW;
-  uint32_t h = 0;
-  for (; h < (uint32_t)kSMax && seglen_max_host[h] > T; ++h) {
-    const uint64_t L = seglen_max_host[h];
-    switch (g_seg_variant) {
-      case 1: seg_launch<V, 4, 4, 8>(in, out, plans, npairs, rank, segs, h, L, st); break;
-      case 2: seg_launch<V, 4, 8, 8>(in, out, plans, npairs, rank, segs, h, L, st); break;
-      case 3: seg_launch<V, 8, 4, 4>(in, out, plans, npairs, rank, segs, h, L, st); break;
-      case 4: seg_launch<V, 16, 2, 2>(in, out, plans, npairs, rank, segs, h, L, st); break;
-      case 5: seg_launch<V, 8, 2, 4>(in, out, plans, npairs, rank, segs, h, L, st); break;
-      case 6: seg_launch<V, 4, 16, 8>(in, out, plans, npairs, rank, segs, h, L, st); break;
-      default: seg_launch<V, 8, 8, 4>(in, out, plans, npairs, rank, segs, h, L, st); break;
-    }
-  }
-  merge_tail_kernel<V, kSegBlock, kSegCPW><<<(unsigned)npairs, kSegBlock, 0, st>>>((V*)in, (V*)out, plans, rank,
-                                                                                 segs, h);
-  count_launch();
-}
-
-void launch_merge_round(int eb, void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
-                        const uint64_t* segs, const uint64_t* seglen_max_host, const uint64_t* chains, uint32_t tpp,
-                        cudaStream_t st) {
-  if (g_seg_variant < 100) {  // default: the tree kernel (one read + one write per element)
-    launch_merge_tree(eb, in, out, plans, npairs, rank, chains, tpp, st);
-    return;
-  }
-  // debug variants >= 100: the segment-pass kernels (1.5 + 1.5 passes), shape = variant - 100
-  const int keep = g_seg_variant;
-  g_seg_variant -= 100;
-  if (eb == 4) merge_round_t<uint32_t>(in, out, plans, npairs, rank, segs, seglen_max_host, st);
-  else merge_round_t<unsigned long long>(in, out, plans, npairs, rank, segs, seglen_max_host, st);
-  g_seg_variant = keep;
 }
 
 // [X, N) is untouched by phase 1 (A queue empty past X).

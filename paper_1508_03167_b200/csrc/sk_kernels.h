@@ -22,11 +22,7 @@ void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64
                         unsigned long long* bits, cudaStream_t st);
 
 void debug_set_leaf_stop(int v);
-void debug_set_leaf_variant(int v);
 void debug_set_leaf_fallback(int v);
-void debug_set_decode_variant(int v);
-void debug_set_seg_variant(int v);
-bool merge_tree_active();
 void debug_set_tree_force_direct(int v);
 
 // merge.cu
@@ -43,15 +39,10 @@ struct LevelTail {            // device-side view used by the all-levels tail de
 };
 void launch_rank_tables(const LevelJob& LJ, uint64_t sbs, uint64_t* rank, uint64_t* csum, cudaStream_t st);
 uint64_t rank_scan_scratch(uint64_t npairs, uint64_t sbs);
-void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, PairPlan* plans, uint64_t* segs,
-                      unsigned long long* seglen_max, cudaStream_t st);
+void launch_pair_plan(const LevelJob& LJ, uint64_t sbs, const uint64_t* rank, PairPlan* plans, cudaStream_t st);
 void launch_tail_decode(const LevelTail* d_levels, int nlevels, const uint64_t* d_pair_prefix, uint64_t total_pairs,
                         unsigned long long* bits, cudaStream_t st);
 
-void launch_merge_round(int eb, void* in, void* out, const PairPlan* plans, uint64_t npairs, const uint64_t* rank,
-                        const uint64_t* segs, const uint64_t* seglen_max_host, const uint64_t* chains, uint32_t tpp,
-                        cudaStream_t st);
-uint32_t merge_tile(int eb);
 uint32_t tree_tile(int eb);
 uint32_t tree_tiles_per_pair(const LevelJob& LJ, int eb);
 uint64_t tree_chain_words(uint64_t npairs, uint32_t tpp);

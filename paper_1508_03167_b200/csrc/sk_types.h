@@ -64,7 +64,6 @@ struct PairPlan {
   uint32_t pad;
 };
 
-constexpr int kSMax = 64;            // stored segment boundaries per pair
 
 
 constexpr uint64_t kNone = ~0ULL;

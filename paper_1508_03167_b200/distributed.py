@@ -145,6 +145,28 @@ class _Groups:
 _GROUPS = {}
 
 
+def _groups(world: int) -> _Groups:
+    """The span groups of this world, built once (dist.new_group is a collective)."""
+    g = _GROUPS.get(world)
+    if g is None:
+        g = _GROUPS[world] = _Groups(world)
+    return g
+
+
+def release_groups() -> None:
+    """Destroy the span groups (before dist.destroy_process_group)."""
+    for g in _GROUPS.values():
+        for grp in g.g.values():
+            if grp is not dist.group.WORLD:
+                dist.destroy_process_group(grp)
+    _GROUPS.clear()
+
+
+def _coll_device(t: torch.Tensor):
+    """Where collective buffers live: host tensors for gloo, the shard's device for NCCL."""
+    return torch.device("cpu") if dist.get_backend() == "gloo" else t.device
+
+
 def merge_shuffle_sharded(shard: torch.Tensor, n: int, cutoff: Optional[int], seed: int,
                           engine=None, exchange: str = "peer") -> int:
     """Shuffle the n-element array whose contiguous shard this rank holds
@@ -171,8 +193,7 @@ def merge_shuffle_sharded(shard: torch.Tensor, n: int, cutoff: Optional[int], se
     elif world > 1:
         bits += _spanning_rounds_allgather(shard, seed, engine, c, q, bounds, nblk, local_rounds)
     if world > 1:
-        t = torch.tensor([bits], dtype=torch.float64, device=shard.device)
-        # bit counts fit 2^53 exactly for n < 2^47
+        t = torch.tensor([bits], dtype=torch.int64, device=_coll_device(shard))
         dist.all_reduce(t)
         bits = int(t.item())
     return bits
@@ -180,12 +201,12 @@ def merge_shuffle_sharded(shard: torch.Tensor, n: int, cutoff: Optional[int], se
 
 def _spanning_rounds_peer(shard, n, seed, engine, c, q, bounds, nblk, local_rounds) -> int:
     world, rank = dist.get_world_size(), dist.get_rank()
-    groups = _GROUPS.setdefault(world, _Groups(world))
+    groups = _groups(world)
     # every rank's shard buffer, mapped into this process (own: its pointer)
-    h = torch.tensor(list(engine.peer_handle(shard)), dtype=torch.uint8, device=shard.device)
+    h = torch.tensor(list(engine.peer_handle(shard)), dtype=torch.uint8, device=_coll_device(shard))
     hs = [torch.empty_like(h) for _ in range(world)]
     dist.all_gather(hs, h)
-    ok = torch.ones(1, dtype=torch.int32, device=shard.device)
+    ok = torch.ones(1, dtype=torch.int32, device=_coll_device(shard))
     ptr = [0] * world
     err = None
     try:
@@ -226,7 +247,7 @@ def _spanning_rounds_allgather(shard, seed, engine, c, q, bounds, nblk, local_ro
     blk0 = rank * nblk
     lo, hi = bounds[blk0], bounds[blk0 + nblk]
     bits = 0
-    groups = _GROUPS.setdefault(world, _Groups(world))
+    groups = _groups(world)
     sizes = [bounds[(r + 1) * nblk] - bounds[r * nblk] for r in range(world)]
     for r in range(local_rounds + 1, c + 1):
         span = 1 << (r - local_rounds)

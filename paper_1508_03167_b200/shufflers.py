@@ -22,7 +22,7 @@ from typing import List, Optional, Tuple
 import numpy as np
 
 from . import _lib
-from .bitstream import BitSource, advance_state
+from .bitstream import BitSource, advance_state, require_plain, require_splittable
 
 #: Default leaf size (shufflers.py:29; SPEC says 2^7, the code -- and this -- 2^16).
 MERGE_CUTOFF_DEFAULT = 1 << 16
@@ -145,13 +145,14 @@ class _Device:
             self.kind = "numpy"
             self.dev = torch.from_numpy(np.ascontiguousarray(arr)).cuda() if arr.size else torch.empty(0, device="cuda")
         else:
+            # a Python sequence of arbitrary items: shuffle the index permutation
+            # on the GPU and reorder the items on the way back (never coerce them)
             self.kind = "seq"
-            a = np.asarray(list(arr), dtype=np.int64)
-            self.seq = a
-            self.dev = torch.from_numpy(a).cuda() if a.size else torch.empty(0, dtype=torch.int64, device="cuda")
+            self.seq_items = list(arr)
+            self.dev = torch.arange(len(self.seq_items), dtype=torch.int64, device="cuda")
         self.n = self.dev.numel()
         eb = self.dev.element_size()
-        if eb not in (4, 8):
+        if self.kind != "seq" and eb not in (4, 8):
             # shuffle an index permutation, gather on the way back
             self.perm_mode = True
             self.payload = self.dev
@@ -165,7 +166,13 @@ class _Device:
 
     @property
     def stream(self):
-        return ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.dev.device).cuda_stream)
+
+    def run(self, entry: str, *args):
+        """Call a C-ABI entry with the array's device current (the library
+        launches on the current device, on the stream passed in)."""
+        with self.torch.cuda.device(self.dev.device):
+            _lib.check(getattr(_lib.load(), entry)(*args))
 
     def finish(self):
         res = self.dev
@@ -186,23 +193,18 @@ class _Device:
         elif self.kind == "numpy":
             self.orig[...] = host.numpy()
         else:
-            vals = host.numpy().tolist()
-            self.orig[:] = vals
-
-
-def _require_plain(src: BitSource) -> None:
-    if not src.is_plain:
-        raise NotImplementedError("tape/recording BitSources are host-only; the GPU path needs a plain source")
+            items = self.seq_items
+            self.orig[:] = [items[i] for i in host.numpy().tolist()]
 
 
 # ------------------------------------------------------------ entry points
 def fisher_yates(arr, src: BitSource) -> None:
     """Uniformly shuffle arr in place (shufflers.py:145-155 -> _kernels.fy_inplace)."""
-    _require_plain(src)
+    require_plain(src)
     d = _Device(arr)
     st = _lib.state_array(src.state_tuple())
     if d.n >= 2:
-        _lib.check(_lib.load().sk_fy_range(d.ptr, d.eb, 0, d.n, st, d.stream))
+        d.run("sk_fy_range", d.ptr, d.eb, 0, d.n, st, d.stream)
         src.set_state_tuple(tuple(st))
     d.finish()
 
@@ -214,10 +216,10 @@ def merge(arr, rng: MergeRange, src: BitSource) -> None:
         raise ValueError(f"{rng} exceeds array of length {len(arr)}")
     if n1 == 0 or n2 == 0:
         return
-    _require_plain(src)
+    require_plain(src)
     d = _Device(arr)
     st = _lib.state_array(src.state_tuple())
-    _lib.check(_lib.load().sk_merge_range(d.ptr, d.eb, s, s + n1, s + n1 + n2, st, d.stream))
+    d.run("sk_merge_range", d.ptr, d.eb, s, s + n1, s + n1 + n2, st, d.stream)
     src.set_state_tuple(tuple(st))
     d.finish()
 
@@ -225,13 +227,13 @@ def merge(arr, rng: MergeRange, src: BitSource) -> None:
 def merge_shuffle(arr, cfg: ShuffleConfig, src: BitSource) -> ShuffleReport:
     """Sequential single-stream merge shuffle (shufflers.py:194-217).  Every task
     continues the one stream, so it runs as a single serial GPU thread."""
-    _require_plain(src)
+    require_plain(src)
     cutoff = cfg.resolve_cutoff(MERGE_CUTOFF_DEFAULT)
     t0 = time.perf_counter_ns()
     d = _Device(arr)
     st = _lib.state_array(src.state_tuple())
     b0 = src.bits_consumed
-    _lib.check(_lib.load().sk_merge_shuffle_seq(d.ptr, d.eb, d.n, cutoff, st, d.stream))
+    d.run("sk_merge_shuffle_seq", d.ptr, d.eb, d.n, cutoff, st, d.stream)
     src.set_state_tuple(tuple(st))
     d.finish()
     return ShuffleReport("merge", d.n, src.bits_consumed - b0, time.perf_counter_ns() - t0, 1)
@@ -241,8 +243,7 @@ def merge_shuffle_parallel(arr, cfg: ShuffleConfig, src: BitSource) -> ShuffleRe
     """Merge shuffle on the frozen substream schedule (shufflers.py:251-299):
     leaf i uses substream i, the round-r merge at block i substream r*q + i.
     `src` itself is not advanced (only src.seed is read, bitstream.py:225)."""
-    if src._tape is not None:
-        raise ValueError("cannot split a tape-replay source")
+    require_splittable(src)
     cutoff = cfg.resolve_cutoff(MERGE_CUTOFF_DEFAULT)
     t0 = time.perf_counter_ns()
     bits = ctypes.c_uint64(0)
@@ -255,7 +256,7 @@ def merge_shuffle_parallel(arr, cfg: ShuffleConfig, src: BitSource) -> ShuffleRe
         n = arr.size
     else:
         d = _Device(arr)
-        _lib.check(lib.sk_merge_shuffle_parallel(d.ptr, d.eb, d.n, cutoff, src.seed, ctypes.byref(bits), d.stream))
+        d.run("sk_merge_shuffle_parallel", d.ptr, d.eb, d.n, cutoff, src.seed, ctypes.byref(bits), d.stream)
         d.finish()
         n = d.n
     return ShuffleReport("merge", n, int(bits.value), time.perf_counter_ns() - t0, cfg.threads)
@@ -278,10 +279,11 @@ def batched_shuffle(arr2d, cfg: ShuffleConfig, seed: int):
         raise ValueError("expected a contiguous 2-d array of 4- or 8-byte elements")
     B, L = t.shape
     bits = np.zeros(max(B, 1), dtype=np.uint64)
-    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    _lib.check(_lib.load().sk_batched_shuffle(ctypes.c_void_p(t.data_ptr()), t.element_size(), B, L, cutoff,
-                                              seed & ((1 << 64) - 1),
-                                              bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), stream))
+    with torch.cuda.device(t.device):
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(_lib.load().sk_batched_shuffle(ctypes.c_void_p(t.data_ptr()), t.element_size(), B, L, cutoff,
+                                                  seed & ((1 << 64) - 1),
+                                                  bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), stream))
     if host is not None:
         res = t.cpu().numpy()
         if isinstance(host, np.ndarray):

@@ -20,6 +20,7 @@ from .bitstream import BitSource, substream_seed
 from .shufflers import MERGE_CUTOFF_DEFAULT
 
 _CHI_ALGO_IDS = {"fy": 0, "merge": 1, "merge_parallel": 2}
+CHI_ALGORITHMS = tuple(_CHI_ALGO_IDS)
 
 
 def permutation_rank(perm) -> int:

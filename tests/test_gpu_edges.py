@@ -73,3 +73,34 @@ def test_rs_sequential_huge_cutoff():
     O.rs_range(a, 0, n, 150_000, st)
     assert np.array_equal(x.cpu().numpy(), a)
     assert list(src.state_tuple()) == [int(v) for v in st]
+
+
+def test_python_sequences_of_any_items():
+    # lists of floats, strings, bools, huge ints and objects are reordered as
+    # items (index permutation on the GPU), never coerced to int64
+    n, cutoff, seed = 5000, 64, 11
+    ref, bits = O.merge_shuffle_perm(n, cutoff, seed)
+    for items in ([i + 0.5 for i in range(n)], [f"s{i}" for i in range(n)], [bool(i & 1) for i in range(n)],
+                  [2 ** 70 + i for i in range(n)], [(i, None) for i in range(n)]):
+        lst = list(items)
+        rep = sk.merge_shuffle_parallel(lst, sk.ShuffleConfig(cutoff=cutoff), sk.BitSource(seed))
+        assert rep.bits == bits
+        assert lst == [items[i] for i in ref]
+    lst = [f"t{i}" for i in range(100)]
+    src = sk.BitSource(3)
+    st = O.state_vec(3, 0, 0, 0)
+    sk.fisher_yates(lst, src)
+    a = np.arange(100, dtype=np.int64)
+    O.fy_range(a, 0, 100, st)
+    assert lst == [f"t{i}" for i in a]
+
+
+def test_tensor_on_its_own_device_and_stream():
+    # a tensor is shuffled on the current stream of ITS device
+    x = torch.arange(100_000, dtype=torch.int32, device="cuda:0")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        sk.merge_shuffle_parallel(x, sk.ShuffleConfig(cutoff=1000), sk.BitSource(4))
+    s.synchronize()
+    ref, _ = O.merge_shuffle_perm(100_000, 1000, 4)
+    assert np.array_equal(x.cpu().numpy(), ref.astype(np.int32))

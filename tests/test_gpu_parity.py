@@ -281,16 +281,15 @@ def test_config4_sharded_2p24_uint64_golden():
     assert sha(data.cpu().numpy().astype("<u8")) == case["sha_u64"]
 
 
-@pytest.mark.parametrize("mode", ["direct", "segment"])
-def test_merge_fallback_paths(mode):
+def test_merge_fallback_path():
     # the tree merge's window-by-window path (taken when a tile's windows do
-    # not fit shared memory or its chain is deeper than the stored starts) and
-    # the segment-pass kernels, forced for every tile: same results
+    # not fit shared memory or its chain is deeper than the stored starts),
+    # forced for every tile: same results
     import ctypes
     from paper_1508_03167_b200 import _lib
     lib = _lib.load()
     lib.sk_debug_set.argtypes = [ctypes.c_int, ctypes.c_int]
-    key, on, off = (4, 1, 0) if mode == "direct" else (2, 100, 0)
+    key, on, off = 4, 1, 0
     lib.sk_debug_set(key, on)
     try:
         for n, cutoff, seed in [(1 << 20, 65536, 0), (300_007, 4096, 1234), (100_000, 1000, 9), (5000, 7, 3)]:
@@ -344,18 +343,17 @@ def test_merge_shuffle_multi_single_process(world, n, dt):
     assert np.array_equal(torch.cat(shards).cpu().numpy().astype(np.int64), ref)
 
 
-@pytest.mark.parametrize("variant", ["v3", "halves", "reg", "fallback", "quadratic", "decode0"])
+@pytest.mark.parametrize("variant", ["v3", "fallback", "quadratic"])
 def test_leaf_apply_variants(variant):
-    # leaves of 8193..65536 elements: the one-pass byte-counter kernel (v3,
-    # default), the target-halves kernel, the register kernel, and v3's serial
-    # fallback (counter overflow, forced for every leaf): same permutations
+    # leaves of 8193..65536 elements: the one-pass byte-counter kernel (v3)
+    # and its serial fallback (counter overflow, forced for every leaf): same
+    # permutations
     import ctypes
     from paper_1508_03167_b200 import _lib
     lib = _lib.load()
     lib.sk_debug_set.argtypes = [ctypes.c_int, ctypes.c_int]
     # quadratic: v3 with every bucket of >= 9 steps through the O(k^2) path
-    knobs = {"v3": [(5, 2)], "halves": [(5, 1)], "reg": [(5, 0)], "fallback": [(5, 2), (6, 1)],
-             "quadratic": [(5, 2), (1, 12)], "decode0": [(7, 0)]}[variant]
+    knobs = {"v3": [], "fallback": [(6, 1)], "quadratic": [(1, 12)]}[variant]
     for k, v in knobs:
         lib.sk_debug_set(k, v)
     try:
@@ -370,10 +368,8 @@ def test_leaf_apply_variants(variant):
                 assert rep.bits == rbits
                 assert np.array_equal(x.cpu().numpy().astype(np.int64), ref), (n, cutoff, seed, dt)
     finally:
-        lib.sk_debug_set(5, 2)
         lib.sk_debug_set(6, 0)
         lib.sk_debug_set(1, 99)
-        lib.sk_debug_set(7, 1)
 
 
 def test_more_than_65535_pairs_in_a_round():
