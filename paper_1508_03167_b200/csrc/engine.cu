@@ -19,7 +19,7 @@
 #include <thread>
 #include <vector>
 
-#include <cub/cub.cuh>
+#include <cmath>
 
 #include "../../include/shufflekit_b200.h"
 #include "sk_kernels.h"
@@ -134,25 +134,43 @@ struct LevelBufs {
   PairPlan* plans = nullptr;
   uint64_t* chains = nullptr;               // per tile: window starts of the tree merge
   uint32_t tpp = 1;                          // tree tiles per pair
-  // tails
-  uint64_t total = 0;
-  std::vector<uint64_t> tail_prefix;         // host: first tail record of pair g (g = 0..npairs)
+  // tails: `cap` record slots (host bound), *used of them filled (device)
+  uint64_t cap = 0;
+  uint64_t* used = nullptr;
   uint64_t* rec_key = nullptr;
   uint32_t* rec_pair = nullptr;
-  uint64_t* skey = nullptr;
-  uint32_t* sval = nullptr;
-  uint32_t* ival = nullptr;
   uint64_t* predx = nullptr;
   uint8_t* keyed = nullptr;
-  uint64_t* dst = nullptr;
+  uint64_t* hkey = nullptr;                  // target -> chain of its records
+  uint32_t* hhead = nullptr;
+  uint32_t* next = nullptr;
+  uint32_t* slot_of = nullptr;
+  uint32_t hmask = 0;
+  uint64_t* dst = nullptr;                   // 2 * cap (dst, src) slots
   uint64_t* src = nullptr;
   void* tmp = nullptr;
-  cudaEvent_t ev_tail{};
+  cudaEvent_t ev_chain{};                    // plans + window chains of this round done (plan stream)
+  cudaEvent_t ev_tail{};                     // tail (dst, src) done
 };
 
-__global__ void tail_len_kernel(const PairPlan* __restrict__ plans, uint64_t n, uint64_t* __restrict__ out) {
-  uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < n) out[g] = plans[g].tail_len;
+// Record capacity of a round's tail buffers, from the pair geometry alone (no
+// device data, no host synchronization): the tail of a pair of N elements has
+// L = N - t insertions with mean 0.80 sqrt(N) and variance 0.37 N (|random
+// walk| at the stop point; measured: tests/test_host_logic.py).  Mean + 9
+// standard deviations of the round's sum, + 4096: a pair beyond it (never
+// seen) falls back to the serial tail (PairPlan.tail_slow), still exact.
+static uint64_t tail_capacity(const LevelJob& LJ) {
+  double mean = 0, var = 0;
+  for (uint64_t g = 0; g < LJ.npairs; ++g) {
+    uint64_t s, n1, n2, array;
+    StreamDesc sd;
+    pair_geom(LJ, g, s, n1, n2, sd, array);
+    if (!n1 || !n2) continue;
+    const double N = (double)(n1 + n2);
+    mean += 0.80 * std::sqrt(N);
+    var += 0.37 * N;
+  }
+  return (uint64_t)(mean + 9.0 * std::sqrt(var)) + 4096;
 }
 
 // Small host->device uploads as kernel parameters (no copy engine).
@@ -172,11 +190,6 @@ static void poke(void* dst, const void* src, size_t n, cudaStream_t st) {
   }
 }
 
-__global__ void set_tail_off_kernel(PairPlan* plans, const uint64_t* offs, uint64_t n) {
-  uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < n) plans[g].tail_off = offs[g];
-}
-
 // Order `ps` after everything queued on `st` so far (allocations, bit counters).
 static void fork_side(cudaStream_t st, cudaStream_t ps) {
   cudaEvent_t ev;
@@ -186,116 +199,79 @@ static void fork_side(cudaStream_t st, cudaStream_t ps) {
   cudaEventDestroy(ev);
 }
 
-// Build every round's plan on `ps`; on return the window chains are queued
-// (ev_windows) and the tail plans are queued per round (lv[r].ev_tail).
-// Host-synchronizes once on the stop points (tail buffer sizing) -- the data
-// stream keeps running the leaf stage meanwhile.
-static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* d_bits, Arena& A, cudaStream_t ps,
-                        cudaStream_t st) {
+// Build every round's plan on `ps`, all on the device (no host
+// synchronization, no host->device copies: on the host entry those would queue
+// behind the big H2D transfer): per round the rank tables, stop points and
+// window chains (then lv[r].ev_chain), the tail offsets; one launch decodes
+// every pair's tail draws; per round the (dst, src) tail plan (then
+// lv[r].ev_tail).
+static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* d_bits, Arena& A, cudaStream_t ps) {
   const int nl = (int)lv.size();
-  (void)st;
-  (void)eb;
   for (auto& L : lv) {
     L.rank = A.alloc<uint64_t>(L.npairs * L.sbs, ps);
     L.plans = A.alloc<PairPlan>(L.npairs, ps);
     L.chains = A.alloc<uint64_t>(tree_chain_words(L.npairs, L.tpp), ps);
+    L.used = A.alloc<uint64_t>(1, ps);
+    CK(cudaEventCreateWithFlags(&L.ev_chain, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&L.ev_tail, cudaEventDisableTiming));
   }
   for (auto& L : lv) {
     uint64_t* csum = A.alloc<uint64_t>(rank_scan_scratch(L.npairs, L.sbs), ps);
     launch_rank_tables(L.LJ, L.sbs, L.rank, csum, ps);
     launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, ps);
     launch_tree_chains(eb, L.plans, L.npairs, L.rank, L.tpp, L.chains, ps);
+    CK(cudaEventRecord(L.ev_chain, ps));
   }
-  CK(cudaGetLastError());
-  // (the host synchronization below also orders the data stream's merge
-  // kernels after these window chains)
-  // tail sizes -> host
   uint64_t tot_pairs = 0;
   std::vector<uint64_t> pprefix(nl + 1, 0);
-  for (int i = 0; i < nl; ++i) {
-    pprefix[i] = tot_pairs;
-    tot_pairs += lv[i].npairs;
-  }
-  pprefix[nl] = tot_pairs;
-  std::vector<PairPlan> hplans(tot_pairs);
-  for (int i = 0; i < nl; ++i) {
-    CK(cudaMemcpyAsync(hplans.data() + pprefix[i], lv[i].plans, lv[i].npairs * sizeof(PairPlan),
-                       cudaMemcpyDeviceToHost, ps));
-  }
-  CK(cudaStreamSynchronize(ps));
-  std::vector<uint64_t> offs(tot_pairs);
-  for (int i = 0; i < nl; ++i) {
-    uint64_t acc = 0;
-    lv[i].tail_prefix.resize(lv[i].npairs + 1);
-    for (uint64_t g = 0; g < lv[i].npairs; ++g) {
-      offs[pprefix[i] + g] = acc;
-      lv[i].tail_prefix[g] = acc;
-      acc += hplans[pprefix[i] + g].tail_len;
-    }
-    lv[i].tail_prefix[lv[i].npairs] = acc;
-    lv[i].total = acc;
-  }
-  // (no host->device copies here: on the host entry they would queue behind
-  // the big H2D transfer on the copy engine.  The tail offsets are scanned on
-  // the device; the small level tables go up as kernel parameters.)
-  uint64_t* d_offs = A.alloc<uint64_t>(tot_pairs, ps);
   std::vector<LevelTail> ht(nl);
   for (int i = 0; i < nl; ++i) {
     auto& L = lv[i];
-    uint64_t* lens = A.alloc<uint64_t>(L.npairs, ps);
-    tail_len_kernel<<<(unsigned)((L.npairs + 255) / 256), 256, 0, ps>>>(L.plans, L.npairs, lens);
-    count_launch();
-    size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, lens, d_offs + pprefix[i], (int)L.npairs, ps));
-    void* ts = A.alloc<unsigned char>(tb, ps);
-    CK(cub::DeviceScan::ExclusiveSum(ts, tb, lens, d_offs + pprefix[i], (int)L.npairs, ps));
-    count_launch();
-    set_tail_off_kernel<<<(unsigned)((L.npairs + 255) / 256), 256, 0, ps>>>(L.plans, d_offs + pprefix[i], L.npairs);
-    count_launch();
-    L.rec_key = A.alloc<uint64_t>(L.total, ps);
-    L.rec_pair = A.alloc<uint32_t>(L.total, ps);
+    pprefix[i] = tot_pairs;
+    tot_pairs += L.npairs;
+    L.cap = tail_capacity(L.LJ);
+    launch_tail_offsets(L.plans, L.npairs, L.cap, L.used, ps);
+    L.rec_key = A.alloc<uint64_t>(L.cap, ps);
+    L.rec_pair = A.alloc<uint32_t>(L.cap, ps);
     ht[i] = LevelTail{L.plans, L.npairs, L.rec_key, L.rec_pair};
   }
+  pprefix[nl] = tot_pairs;
   LevelTail* d_lt = A.alloc<LevelTail>(nl, ps);
   uint64_t* d_pp = A.alloc<uint64_t>(nl + 1, ps);
   poke(d_lt, ht.data(), nl * sizeof(LevelTail), ps);
   poke(d_pp, pprefix.data(), (nl + 1) * 8, ps);
   launch_tail_decode(d_lt, nl, d_pp, tot_pairs, d_bits, ps);
-  // per round: sort tail targets, build (dst, src)
-  uint64_t nbits_key = 1;
-  {
-    uint64_t mx = 0;
-    for (auto& L : lv) mx = std::max(mx, (uint64_t)L.LJ.J.batch * L.LJ.J.len);  // global positions < this
-    if (lv[0].LJ.E.active) mx = lv[0].LJ.E.lo + lv[0].LJ.E.n1 + lv[0].LJ.E.n2;
-    while ((1ULL << nbits_key) <= mx && nbits_key < 64) ++nbits_key;
-  }
   for (auto& L : lv) {
-    CK(cudaEventCreateWithFlags(&L.ev_tail, cudaEventDisableTiming));
-    if (L.total) {
-      L.skey = A.alloc<uint64_t>(L.total, ps);
-      L.sval = A.alloc<uint32_t>(L.total, ps);
-      L.ival = A.alloc<uint32_t>(L.total, ps);
-      L.predx = A.alloc<uint64_t>(L.total, ps);
-      L.keyed = A.alloc<uint8_t>(L.total, ps);
-      L.dst = A.alloc<uint64_t>(2 * L.total, ps);
-      L.src = A.alloc<uint64_t>(2 * L.total, ps);
-      L.tmp = A.alloc<uint64_t>(2 * L.total, ps);
-      launch_iota32(L.ival, L.total, ps);
-      size_t tb = 0;
-      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, L.rec_key, L.skey, L.ival, L.sval, (int)L.total, 0,
-                                         (int)nbits_key, ps));
-      void* tstore = A.alloc<unsigned char>(tb, ps);
-      CK(cub::DeviceRadixSort::SortPairs(tstore, tb, L.rec_key, L.skey, L.ival, L.sval, (int)L.total, 0,
-                                         (int)nbits_key, ps));
-      count_launch();
-      CK(cudaMemsetAsync(L.keyed, 0, L.total, ps));
-      CK(cudaMemsetAsync(L.dst, 0xFF, 2 * L.total * 8, ps));
-      launch_tail_plan(L.plans, L.rec_key, L.rec_pair, L.skey, L.sval, L.total, L.predx, L.keyed, L.dst, L.src, ps);
-      launch_tail_chase(L.plans, L.rec_key, L.rec_pair, L.predx, L.keyed, L.total, L.dst, L.src, ps);
-    }
+    uint32_t hb = 1;
+    while ((1ull << hb) < 2 * L.cap) ++hb;
+    L.hmask = (uint32_t)((1ull << hb) - 1);
+    L.hkey = A.alloc<uint64_t>(1ull << hb, ps);
+    L.hhead = A.alloc<uint32_t>(1ull << hb, ps);
+    L.next = A.alloc<uint32_t>(L.cap, ps);
+    L.slot_of = A.alloc<uint32_t>(L.cap, ps);
+    L.predx = A.alloc<uint64_t>(L.cap, ps);
+    L.keyed = A.alloc<uint8_t>(L.cap, ps);
+    L.dst = A.alloc<uint64_t>(2 * L.cap, ps);
+    L.src = A.alloc<uint64_t>(2 * L.cap, ps);
+    L.tmp = A.alloc<uint64_t>(2 * L.cap, ps);
+    CK(cudaMemsetAsync(L.hkey, 0xFF, (8ull << hb), ps));
+    CK(cudaMemsetAsync(L.hhead, 0xFF, (4ull << hb), ps));
+    CK(cudaMemsetAsync(L.keyed, 0, L.cap, ps));
+    CK(cudaMemsetAsync(L.dst, 0xFF, 2 * L.cap * 8, ps));
+    launch_tail_plan(L.plans, L.rec_key, L.rec_pair, L.used, L.cap, L.hkey, L.hhead, L.next, L.slot_of, L.hmask,
+                     L.predx, L.keyed, L.dst, L.src, ps);
+    launch_tail_chase(L.plans, L.rec_key, L.rec_pair, L.predx, L.keyed, L.used, L.cap, L.dst, L.src, ps);
     CK(cudaEventRecord(L.ev_tail, ps));
   }
   CK(cudaGetLastError());
+}
+
+static void destroy_events(std::vector<LevelBufs>& lv) {
+  for (auto& L : lv) {
+    if (L.ev_chain) cudaEventDestroy(L.ev_chain);
+    if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+    L.ev_chain = L.ev_tail = nullptr;
+  }
 }
 
 // Helper streams of the calling thread on the CURRENT device (a thread may
@@ -331,15 +307,17 @@ static cudaStream_t side_stream() { return helper_stream(kPlanStream); }
 // The segment-pass debug kernels park elements in their input and need the
 // ping-pong.  Returns the buffer holding the result.
 // Pairs [p0, p1) of one round, in place (tree merge), with their tail insertions.
-static void run_round_range(LevelBufs& L, int eb, void* buf, uint64_t p0, uint64_t p1, cudaStream_t st) {
+// (positions [lo, hi) = the pairs' elements: the tail slots are filtered by it)
+static void run_round_range(LevelBufs& L, int eb, void* buf, uint64_t p0, uint64_t p1, uint64_t lo, uint64_t hi,
+                            cudaStream_t st) {
   {
     StageTimer tm(2, st);
+    CK(cudaStreamWaitEvent(st, L.ev_chain, 0));
     launch_merge_tree_range(eb, buf, buf, L.plans, p0, p1, L.rank, L.chains, L.tpp, st);
   }
   StageTimer tm(3, st);
   CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
-  const uint64_t s0 = 2 * L.tail_prefix[p0], s1 = 2 * L.tail_prefix[p1];
-  launch_tail_apply(eb, buf, L.dst + s0, L.src + s0, (unsigned char*)L.tmp + s0 * eb, s1 - s0, st);
+  launch_tail_apply(eb, buf, L.dst, L.src, L.tmp, 2 * L.cap, L.plans, L.npairs, lo, hi, st);
 }
 
 static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* other, cudaStream_t st,
@@ -349,13 +327,14 @@ static void* run_rounds(std::vector<LevelBufs>& lv, int eb, void* cur, void* oth
     void* out = r + 1 == lv.size() ? other : cur;
     {
       StageTimer tm(2, st);
+      CK(cudaStreamWaitEvent(st, L.ev_chain, 0));
       launch_merge_tree(eb, cur, out, L.plans, L.npairs, L.rank, L.chains, L.tpp, st);
     }
     {
       StageTimer tm(3, st);
       if (out != cur) launch_copy_tail_region(eb, cur, out, L.plans, L.npairs, st);
       CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
-      launch_tail_apply(eb, out, L.dst, L.src, L.tmp, 2 * L.total, st);
+      launch_tail_apply(eb, out, L.dst, L.src, L.tmp, 2 * L.cap, L.plans, L.npairs, 0, ~0ull, st);
     }
     if (out != cur) std::swap(cur, other);
   }
@@ -426,7 +405,7 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
     }
     CK(cudaGetLastError());
     // plans run on the side stream while the leaf stage runs
-    if (!lv.empty()) build_plans(lv, eb, d_bits, A, ps, st);
+    if (!lv.empty()) build_plans(lv, eb, d_bits, A, ps);
     void* res = run_rounds(lv, eb, cur, data, st);
     if (res != data) {
       StageTimer tm(4, st);
@@ -435,8 +414,7 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
   } catch (...) {
     cudaStreamSynchronize(ps);
     cudaStreamSynchronize(st);
-    for (auto& L : lv)
-      if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+    destroy_events(lv);
     A.release(st);
     throw;
   }
@@ -445,8 +423,7 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
   CK(cudaEventRecord(done, ps));
   CK(cudaStreamWaitEvent(st, done, 0));
   cudaEventDestroy(done);
-  for (auto& L : lv)
-    if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+  destroy_events(lv);
   A.release(st);
 }
 
@@ -510,14 +487,14 @@ static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned 
       CK(cudaEventCreateWithFlags(&evl[j], cudaEventDisableTiming));
       CK(cudaEventRecord(evl[j], st));
     }
-    build_plans(lv, eb, d_bits, A, ps, st);
+    build_plans(lv, eb, d_bits, A, ps);
     const size_t nloc = (size_t)std::max(0, std::min((int)lv.size() - 1, c - k));
     cudaStream_t rs = round_stream();  // ordered after st by the per-chunk events only
     for (uint64_t j = 0; j < K; ++j) {
       CK(cudaStreamWaitEvent(rs, evl[j], 0));
       for (size_t r = 0; r < nloc; ++r) {
         const uint64_t pp = B >> (r + 1);  // pairs of round r+1 per chunk
-        run_round_range(lv[r], eb, scr, j * pp, (j + 1) * pp, rs);
+        run_round_range(lv[r], eb, scr, j * pp, (j + 1) * pp, bound_at(n, j * B, c), bound_at(n, (j + 1) * B, c), rs);
       }
     }
     for (auto e : evl) cudaEventDestroy(e);
@@ -537,8 +514,7 @@ static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned 
     cudaStreamSynchronize(st);
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
-    for (auto& L : lv)
-      if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+    destroy_events(lv);
     A.release(st);
     throw;
   }
@@ -549,8 +525,7 @@ static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned 
   cudaEventDestroy(done);
   for (auto e : ev)
     if (e) cudaEventDestroy(e);
-  for (auto& L : lv)
-    if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+  destroy_events(lv);
   A.release(st);
 }
 
@@ -598,15 +573,16 @@ static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t
   L.tpp = tree_tiles_per_pair(L.LJ, eb);
   try {
     fork_side(st, ps);
-    build_plans(lv, eb, d_bits, A, ps, st);
+    build_plans(lv, eb, d_bits, A, ps);
+    CK(cudaStreamWaitEvent(st, L.ev_chain, 0));
     launch_merge_tree(eb, data, data, L.plans, 1, L.rank, L.chains, L.tpp, st);  // in place
     CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
-    launch_tail_apply(eb, data, L.dst, L.src, L.tmp, 2 * L.total, st);
+    launch_tail_apply(eb, data, L.dst, L.src, L.tmp, 2 * L.cap, L.plans, 1, 0, ~0ull, st);
     CK(cudaGetLastError());
   } catch (...) {
     cudaStreamSynchronize(ps);
     cudaStreamSynchronize(st);
-    if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+    destroy_events(lv);
     A.release(st);
     throw;
   }
@@ -615,7 +591,7 @@ static void run_single_pair(int eb, void* data, uint64_t j, uint64_t k, uint64_t
   CK(cudaEventRecord(done, ps));
   CK(cudaStreamWaitEvent(st, done, 0));
   cudaEventDestroy(done);
-  if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+  destroy_events(lv);
   A.release(st);
 }
 
@@ -640,18 +616,19 @@ static void run_pair_peers(int eb, const PeerSpan& span, uint64_t n1, uint64_t n
   L.tpp = tree_tiles_per_pair(L.LJ, eb);
   try {
     fork_side(st, ps);
-    build_plans(lv, eb, d_bits, A, ps, st);
+    build_plans(lv, eb, d_bits, A, ps);
     if (phase == 1) {
+      CK(cudaStreamWaitEvent(st, L.ev_chain, 0));
       launch_merge_tree_peer(eb, span, L.plans, L.rank, L.chains, L.tpp, (uint32_t)part, st);
     } else {
       CK(cudaStreamWaitEvent(st, L.ev_tail, 0));
-      launch_tail_apply_peer(eb, span, L.dst, L.src, L.tmp, 2 * L.total, st);
+      launch_tail_apply_peer(eb, span, L.dst, L.src, L.tmp, 2 * L.cap, L.plans, st);
     }
     CK(cudaGetLastError());
   } catch (...) {
     cudaStreamSynchronize(ps);
     cudaStreamSynchronize(st);
-    if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+    destroy_events(lv);
     A.release(st);
     throw;
   }
@@ -660,7 +637,7 @@ static void run_pair_peers(int eb, const PeerSpan& span, uint64_t n1, uint64_t n
   CK(cudaEventRecord(done, ps));
   CK(cudaStreamWaitEvent(st, done, 0));
   cudaEventDestroy(done);
-  if (L.ev_tail) cudaEventDestroy(L.ev_tail);
+  destroy_events(lv);
   A.release(st);
 }
 
@@ -919,6 +896,7 @@ int sk_debug_set(int key, int value) {
   if (key == 1) { debug_set_leaf_stop(value); return 0; }
   if (key == 4) { debug_set_tree_force_direct(value); return 0; }
   if (key == 6) { debug_set_leaf_fallback(value); return 0; }
+  if (key == 7) { debug_set_warp_decode_max(value); return 0; }
   return -1;
 }
 const char* sk_last_error(void) { return g_err.c_str(); }

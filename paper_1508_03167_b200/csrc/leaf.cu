@@ -41,6 +41,108 @@ __device__ __forceinline__ uint64_t leaf_word(const StreamDesc& sd, uint64_t w) 
 // schedulers (single-warp blocks were observed to share them).
 constexpr int kDecodeBlock = 128;
 
+// One WARP per leaf, for jobs with few leaves (the lane-per-leaf kernel below
+// then leaves most of the GPU idle for the ~6 ms its per-lane chain of 65535
+// draws takes).  Batches of 32 consecutive steps: lane l takes step s = i - l
+// and first assumes that every earlier step of the batch accepts its first
+// FDR iteration (k0 = bit length of s), so its bit offset is o + the sum of
+// the earlier k0 -- a closed form, k0 takes at most two values in a batch.  A
+// ballot finds the first lane f whose first iteration rejects: the lanes
+// before f are final, lane f finishes its draw with the full FDR loop (e extra
+// bits), the lanes after f re-test at offsets shifted by e, and so on: one
+// phase per rejection (about a quarter of the draws).  Bit-identical to the
+// serial loop (_kernels.py:64-93).  Bits come from a per-warp ring of 64
+// words in shared memory, topped up 32 words at a time (one per lane).
+constexpr int kWarpDecodeWarps = 4;
+constexpr uint32_t kRingHalves = 128;    // 64 words = 4096 bits per warp
+constexpr uint64_t kRingAhead = 1536;    // bits kept available past the batch start
+static uint64_t g_warp_decode_max = 4096;  // jobs with at most this many leaves use the warp decode
+
+template <bool FRESH>
+__global__ void __launch_bounds__(32 * kWarpDecodeWarps)
+    leaf_decode_warp_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves, uint16_t* __restrict__ draws,
+                            unsigned long long* __restrict__ bits) {
+  __shared__ uint32_t ring_all[kWarpDecodeWarps][kRingHalves];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t g = (uint64_t)blockIdx.x * kWarpDecodeWarps + wid;
+  if (g >= nleaves) return;  // whole warp
+  uint32_t* const ring = ring_all[wid];
+  const LeafDesc L = leaf_desc(J, E, g);
+  const uint32_t m = (uint32_t)(L.hi - L.lo);
+  if (m < 2) return;
+  uint16_t* const dr = draws + L.lo;
+  uint64_t wgen = 0;  // words [wgen - 64, wgen) are in the ring
+  auto refill = [&]() {
+    const uint64_t x = leaf_word<FRESH>(L.sd, wgen + lane);
+    const uint32_t h = (uint32_t)((wgen + lane) * 2) & (kRingHalves - 1);
+    ring[h] = (uint32_t)(x >> 32);
+    ring[h + 1] = (uint32_t)x;
+    wgen += 32;
+    __syncwarp();
+  };
+  refill();
+  refill();
+  // 32 stream bits from bit p on (MSB first); outside the ring (a very long
+  // rejection chain) the words are generated directly
+  auto bits32 = [&](uint64_t p) -> uint32_t {
+    if (p + 32 > 64 * wgen) return (uint32_t)(bits64_at(L.sd, p) >> 32);
+    const uint32_t h = (uint32_t)(p >> 5);
+    return __funnelshift_l(ring[(h + 1) & (kRingHalves - 1)], ring[h & (kRingHalves - 1)], (uint32_t)p & 31);
+  };
+  uint64_t o = 0;      // bit offset of the batch's first draw
+  uint32_t i = m - 1;  // the batch's first step (bound i + 1)
+  while (i >= 1) {
+    while (o + kRingAhead > 64 * wgen) refill();
+    const uint32_t n = min(32u, i);
+    const bool valid = lane < n;
+    const uint32_t s = i - lane, b = s + 1;
+    const uint32_t k0 = valid ? 32 - __clz(s) : 0u;
+    // sum of k0 over the lanes before: K for the steps >= 2^(K-1), K-1 below
+    const uint32_t K = 32 - __clz(i), lb = i + 1 - (1u << (K - 1));
+    const uint32_t pre = lane * K - (lane > lb ? lane - lb : 0u);
+    const uint32_t total_k0 = n * K - (n > lb ? n - lb : 0u);
+    uint64_t off = o + pre;
+    uint32_t start = 0, ext = 0;
+    for (;;) {
+      const bool live = valid && lane >= start;
+      uint32_t c = 0;
+      bool acc = true;
+      if (live) {
+        c = bits32(off) >> (32 - k0);
+        acc = c < b;
+      }
+      const uint32_t rej = __ballot_sync(0xffffffffu, live && !acc);
+      const uint32_t f = rej ? (uint32_t)__ffs(rej) - 1 : 32u;
+      if (live && lane < f) dr[s] = (uint16_t)c;
+      if (f == 32) break;
+      uint32_t e = 0;
+      if (lane == f) {  // the rest of this draw's FDR loop (_kernels.py:71-82)
+        uint32_t v = (1u << k0) - b, cc = c - b;
+        uint64_t p = off + k0;
+        for (;;) {
+          uint32_t k = __clz(v) - __clz(s);  // smallest k with v << k >= b  (s = b - 1)
+          k += ((v << k) <= s) ? 1u : 0u;
+          cc = (cc << k) | (bits32(p) >> (32 - k));
+          v <<= k;
+          p += k;
+          if (cc < b) break;
+          cc -= b;
+          v -= b;
+        }
+        dr[s] = (uint16_t)cc;
+        e = (uint32_t)(p - off - k0);
+      }
+      e = __shfl_sync(0xffffffffu, e, f);
+      ext += e;
+      if (lane > f) off += e;
+      start = f + 1;
+    }
+    o += total_k0 + ext;
+    i -= n;
+  }
+  if (lane == 0) atomicAdd(&bits[L.array], (unsigned long long)o);
+}
+
 // Leaner decode (same draws, same bit accounting): the step index i drives
 // everything -- the store address (dr + i), the flush condition ((lo + i) % 8
 // == 0), the head test (i > ih: draws whose 16-byte chunk reaches past the
@@ -820,6 +922,7 @@ __global__ void leaf_serial_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
 }
 
 // ---------------------------------------------------------------- launchers
+void debug_set_warp_decode_max(int v) { g_warp_decode_max = v < 0 ? 0 : (uint64_t)v; }
 void debug_set_leaf_fallback(int v) { cudaMemcpyToSymbol(g_leaf_force_fallback, &v, sizeof(int)); }
 void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int)); }
 
@@ -828,8 +931,15 @@ void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nle
   if (!nleaves) return;
   unsigned blocks = (unsigned)((nleaves + kDecodeBlock - 1) / kDecodeBlock);
   const bool fresh = !(E.active && E.sd.plen != 0);
-  if (fresh) leaf_decode16b_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
-  else leaf_decode16b_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
+  if (nleaves <= g_warp_decode_max) {
+    const unsigned wb = (unsigned)((nleaves + kWarpDecodeWarps - 1) / kWarpDecodeWarps);
+    if (fresh) leaf_decode_warp_kernel<true><<<wb, 32 * kWarpDecodeWarps, 0, st>>>(J, E, nleaves, draws, bits);
+    else leaf_decode_warp_kernel<false><<<wb, 32 * kWarpDecodeWarps, 0, st>>>(J, E, nleaves, draws, bits);
+  } else if (fresh) {
+    leaf_decode16b_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
+  } else {
+    leaf_decode16b_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
+  }
   count_launch();
 }
 

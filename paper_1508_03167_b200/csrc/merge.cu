@@ -176,6 +176,7 @@ __global__ void pair_plan_kernel(LevelJob LJ, uint64_t sbs, const uint64_t* __re
   pair_geom(LJ, g, P.s, P.n1, P.n2, P.sd, P.array);
   P.rank_off = g * sbs;
   P.tail_off = 0;
+  P.tail_slow = 0;
   const uint64_t n1 = P.n1, n2 = P.n2, N = n1 + n2;
   if (n1 == 0 || n2 == 0) {  // shufflers.py:169-170: no bits, no change
     P.t = 0; P.X = n1; P.aex = 0; P.degenerate = 1; P.tail_len = 0; P.bits = 0;
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(128) tail_decode_kernel(const LevelTail* __res
   PairPlan* Pp = lv.plans + g;
   if (Pp->degenerate) return;
   const uint64_t t = Pp->t, N = Pp->n1 + Pp->n2, s = Pp->s, off = Pp->tail_off;
+  const bool store = !Pp->tail_slow;  // slow pairs: bits only (their tail runs serially)
   const StreamDesc sd = Pp->sd;
   uint64_t o = t + 1;  // bit offset of the next draw
   uint64_t x = t;      // next insertion step
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(128) tail_decode_kernel(const LevelTail* __res
     }
     const uint32_t fail = __ballot_sync(0xffffffffu, valid && !acc);
     const uint32_t f = fail ? (uint32_t)(__ffs(fail) - 1) : 32u;  // first rejecting lane
-    if (valid && lane < f) {
+    if (store && valid && lane < f) {
       lv.rec_key[off + (xl - t)] = s + c;
       lv.rec_pair[off + (xl - t)] = (uint32_t)g;
     }
@@ -265,8 +267,10 @@ __global__ void __launch_bounds__(128) tail_decode_kernel(const LevelTail* __res
         Reader64 rd;
         rd.init(sd, ol);
         m = fdr64(rd, b, used);
-        lv.rec_key[off + (xl - t)] = s + m;
-        lv.rec_pair[off + (xl - t)] = (uint32_t)g;
+        if (store) {
+          lv.rec_key[off + (xl - t)] = s + m;
+          lv.rec_pair[off + (xl - t)] = (uint32_t)g;
+        }
       }
       used = __shfl_sync(0xffffffffu, used, f);
       const uint64_t of = __shfl_sync(0xffffffffu, ol, f);
@@ -1036,49 +1040,133 @@ void launch_copy_tail_region(int eb, const void* in, void* out, const PairPlan* 
 }
 
 // -------------------------------------------------------------- tail plan
-__global__ void iota32_kernel(uint32_t* v, uint64_t n) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (uint32_t)i;
-}
-void launch_iota32(uint32_t* v, uint64_t n, cudaStream_t st) {
-  if (!n) return;
-  iota32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n);
-  count_launch();
-}
 
 // Over records sorted by target (stable in x): predecessor in the target's
 // group, and for each group's last step x_last > q the output (q <- x_last).
+// ------------------------------------------------------------ tail plans
+// The records of a round live at [tail_off, tail_off + tail_len) per pair,
+// tail_off the exclusive prefix of tail_len over the round's pairs (one CTA
+// scans them).  The buffers hold `cap` records (a bound sized on the host
+// from the pair geometry, tail_capacity): the pairs from the first one that
+// does not fit on are marked tail_slow and keep no records; their tail runs
+// serially (tail_slow_apply).  *used = records kept.
+__global__ void __launch_bounds__(1024) tail_offsets_kernel(PairPlan* __restrict__ plans, uint64_t npairs,
+                                                            uint64_t cap, uint64_t* __restrict__ used) {
+  __shared__ uint64_t wsum[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t per = (npairs + 1023) / 1024, g0 = tid * per, g1 = min(npairs, g0 + per);
+  uint64_t sum = 0;
+  for (uint64_t g = g0; g < g1; ++g) sum += plans[g].tail_len;
+  uint64_t x = sum;  // inclusive block scan of the per-thread sums
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  uint64_t before = 0;
+  for (uint32_t w = 0; w < wid; ++w) before += wsum[w];
+  uint64_t acc = before + x - sum;
+  uint64_t first_slow = kNone;
+  for (uint64_t g = g0; g < g1; ++g) {
+    const uint64_t len = plans[g].tail_len;
+    const bool slow = acc + len > cap;
+    plans[g].tail_off = slow ? 0 : acc;
+    plans[g].tail_slow = slow ? 1u : 0u;
+    if (slow && first_slow == kNone) first_slow = acc;
+    acc += len;
+  }
+  // records kept = the prefix at the first slow pair (prefixes grow with g), else the total
+  __shared__ unsigned long long s_used;
+  if (tid == 0) s_used = ~0ULL;
+  __syncthreads();
+  if (first_slow != kNone) atomicMin(&s_used, (unsigned long long)first_slow);
+  __syncthreads();
+  if (tid == 1023) *used = (s_used != ~0ULL) ? s_used : acc;
+}
+
+void launch_tail_offsets(PairPlan* plans, uint64_t npairs, uint64_t cap, uint64_t* used, cudaStream_t st) {
+  tail_offsets_kernel<<<1, 1024, 0, st>>>(plans, npairs, cap, used);
+  count_launch();
+}
+
+// Records with the same target (a global position; equal targets lie in one
+// pair) are chained through an open-addressing table keyed by the target:
+// the slot's head is pushed atomically, so each chain lists every record of
+// its target (equal targets are rare: ~L^2/2N per pair).
+__device__ __forceinline__ uint32_t tail_hash(uint64_t key, uint32_t mask) {
+  return (uint32_t)((key * GOLDEN) >> 32) & mask;
+}
+
+__global__ void tail_hash_kernel(const uint64_t* __restrict__ rec_key, const uint64_t* __restrict__ used,
+                                 uint64_t* __restrict__ hkey, uint32_t* __restrict__ hhead,
+                                 uint32_t* __restrict__ next, uint32_t* __restrict__ slot_of, uint32_t mask) {
+  const uint64_t rec = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rec >= *used) return;
+  const uint64_t key = rec_key[rec];
+  uint32_t h = tail_hash(key, mask);
+  for (;;) {
+    const unsigned long long prev =
+        atomicCAS(reinterpret_cast<unsigned long long*>(hkey + h), ~0ULL, (unsigned long long)key);
+    if (prev == ~0ULL || prev == key) break;
+    h = (h + 1) & mask;
+  }
+  slot_of[rec] = h;
+  next[rec] = atomicExch(hhead + h, (uint32_t)rec);
+}
+
+// Per record x (target q = m_x): predx = the latest earlier step with the same
+// target; the LAST step targeting q moves P1[x] into q for good (when x > q)
+// -- a (dst, src) pair; a tail position q >= t written that way is "keyed"
+// (tests/decomp_model.py tail_plan_model).
 __global__ void tail_plan_kernel(const PairPlan* __restrict__ plans, const uint64_t* __restrict__ rec_key,
-                                 const uint32_t* __restrict__ rec_pair, const uint64_t* __restrict__ skey,
-                                 const uint32_t* __restrict__ sval, uint64_t total, uint64_t* __restrict__ predx,
-                                 uint8_t* __restrict__ keyed, uint64_t* __restrict__ dst, uint64_t* __restrict__ src) {
-  uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= total) return;
-  uint32_t rec = sval[k];
-  uint64_t key = skey[k];
+                                 const uint32_t* __restrict__ rec_pair, const uint64_t* __restrict__ used,
+                                 const uint32_t* __restrict__ hhead, const uint32_t* __restrict__ next,
+                                 const uint32_t* __restrict__ slot_of, uint64_t* __restrict__ predx,
+                                 uint8_t* __restrict__ keyed, uint64_t* __restrict__ dst,
+                                 uint64_t* __restrict__ src) {
+  const uint64_t rec = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rec >= *used) return;
+  const uint64_t key = rec_key[rec];
   const PairPlan* P = plans + rec_pair[rec];
-  uint64_t loc = rec - P->tail_off, x = P->t + loc;
-  predx[rec] = (k > 0 && skey[k - 1] == key) ? (P->t + (sval[k - 1] - P->tail_off)) : kNone;
-  bool last = (k + 1 == total) || skey[k + 1] != key;
+  const uint64_t off = P->tail_off, loc = rec - off, x = P->t + loc;
+  // records of one pair are consecutive: step order == record order
+  uint64_t pred = kNone;
+  bool last = true;
+  for (uint32_t r = hhead[slot_of[rec]]; r != 0xffffffffu; r = next[r]) {
+    if (r == rec || rec_key[r] != key) continue;
+    if (r < rec) pred = (pred == kNone || r > pred) ? r : pred;
+    else last = false;
+  }
+  predx[rec] = pred == kNone ? kNone : P->t + (pred - off);
   if (last) {
-    uint64_t q = key - P->s;
+    const uint64_t q = key - P->s;
     if (x > q) {
-      uint64_t slot = 2 * P->tail_off + P->tail_len + loc;
+      const uint64_t slot = 2 * off + P->tail_len + loc;
       dst[slot] = key;
       src[slot] = P->s + x;
-      if (q >= P->t) keyed[P->tail_off + (q - P->t)] = 1;
+      if (q >= P->t) keyed[off + (q - P->t)] = 1;
     }
   }
-  (void)rec_key;
+}
+
+void launch_tail_plan(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair, const uint64_t* used,
+                      uint64_t cap, uint64_t* hkey, uint32_t* hhead, uint32_t* next, uint32_t* slot_of, uint32_t hmask,
+                      uint64_t* predx, uint8_t* keyed, uint64_t* dst, uint64_t* src, cudaStream_t st) {
+  const unsigned b = (unsigned)((cap + 255) / 256);
+  tail_hash_kernel<<<b, 256, 0, st>>>(rec_key, used, hkey, hhead, next, slot_of, hmask);
+  tail_plan_kernel<<<b, 256, 0, st>>>(plans, rec_key, rec_pair, used, hhead, next, slot_of, predx, keyed, dst, src);
+  count_launch();
+  count_launch();
 }
 
 // For every insertion position x not overwritten later: chase V(m_x, x).
 __global__ void tail_chase_kernel(const PairPlan* __restrict__ plans, const uint64_t* __restrict__ rec_key,
                                   const uint32_t* __restrict__ rec_pair, const uint64_t* __restrict__ predx,
-                                  const uint8_t* __restrict__ keyed, uint64_t total, uint64_t* __restrict__ dst,
-                                  uint64_t* __restrict__ src) {
+                                  const uint8_t* __restrict__ keyed, const uint64_t* __restrict__ used,
+                                  uint64_t* __restrict__ dst, uint64_t* __restrict__ src) {
   uint64_t rec = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (rec >= total) return;
+  if (rec >= *used) return;
   if (keyed[rec]) return;
   const PairPlan* P = plans + rec_pair[rec];
   const uint64_t t = P->t, s = P->s, off = P->tail_off;
@@ -1098,46 +1186,69 @@ __global__ void tail_chase_kernel(const PairPlan* __restrict__ plans, const uint
   src[slot] = s + sr;
 }
 
-void launch_tail_plan(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair,
-                      const uint64_t* skey, const uint32_t* sval, uint64_t total, uint64_t* predx,
-                      uint8_t* keyed, uint64_t* dst, uint64_t* src, cudaStream_t st) {
-  if (!total) return;
-  tail_plan_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(plans, rec_key, rec_pair, skey, sval, total,
-                                                                    predx, keyed, dst, src);
-  count_launch();
-}
-
 void launch_tail_chase(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair,
-                       const uint64_t* predx, const uint8_t* keyed, uint64_t total, uint64_t* dst, uint64_t* src,
-                       cudaStream_t st) {
-  if (!total) return;
-  tail_chase_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(plans, rec_key, rec_pair, predx, keyed, total,
-                                                                     dst, src);
+                       const uint64_t* predx, const uint8_t* keyed, const uint64_t* used, uint64_t cap, uint64_t* dst,
+                       uint64_t* src, cudaStream_t st) {
+  tail_chase_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, st>>>(plans, rec_key, rec_pair, predx, keyed, used, dst,
+                                                                   src);
   count_launch();
 }
 
 // ------------------------------------------------------------ tail apply
+// The (dst, src) slots of a round: gather every source, then scatter (dst =
+// kNone: unused slot).  Only slots whose dst lies in [lo, hi) (the host
+// entry applies a round chunk by chunk).  The last CTA of the gather also
+// runs the tail of every tail_slow pair of the range serially, in place --
+// the reference loop itself (shufflers.py:188-191), never taken in practice.
+template <typename V, class Acc>
+__device__ void tail_serial_pairs(const Acc& acc, const PairPlan* __restrict__ plans, uint64_t npairs, uint64_t lo,
+                                  uint64_t hi) {
+  for (uint64_t g = threadIdx.x; g < npairs; g += blockDim.x) {
+    const PairPlan P = plans[g];
+    if (!P.tail_slow || P.s < lo || P.s >= hi) continue;
+    Reader64 rd;
+    rd.init(P.sd, P.t + 1);
+    uint64_t nb = 0;
+    for (uint64_t x = P.t; x < P.n1 + P.n2; ++x) {  // x >= t >= 1: bound >= 2
+      const uint64_t m = fdr64(rd, x + 1, nb);
+      const V a = acc.ld(P.s + x), b = acc.ld(P.s + m);
+      acc.st(P.s + x, b);
+      acc.st(P.s + m, a);
+    }
+  }
+}
+
 template <typename V>
-__global__ void tail_gather_kernel(const V* __restrict__ buf, const uint64_t* __restrict__ dst,
-                                   const uint64_t* __restrict__ src, V* __restrict__ tmp, uint64_t n) {
+__global__ void tail_gather_kernel(V* __restrict__ buf, const uint64_t* __restrict__ dst,
+                                   const uint64_t* __restrict__ src, V* __restrict__ tmp, uint64_t n, uint64_t lo,
+                                   uint64_t hi, const PairPlan* __restrict__ plans, uint64_t npairs) {
   uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n && dst[k] != kNone) tmp[k] = buf[src[k]];
+  if (k < n) {
+    const uint64_t d = dst[k];
+    if (d != kNone && d >= lo && d < hi) tmp[k] = buf[src[k]];
+  }
+  if (blockIdx.x == gridDim.x - 1) tail_serial_pairs<V>(FlatAcc<V>{buf, buf}, plans, npairs, lo, hi);
 }
 template <typename V>
 __global__ void tail_scatter_kernel(V* __restrict__ buf, const uint64_t* __restrict__ dst,
-                                    const V* __restrict__ tmp, uint64_t n) {
+                                    const V* __restrict__ tmp, uint64_t n, uint64_t lo, uint64_t hi) {
   uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n && dst[k] != kNone) buf[dst[k]] = tmp[k];
+  if (k < n) {
+    const uint64_t d = dst[k];
+    if (d != kNone && d >= lo && d < hi) buf[d] = tmp[k];
+  }
 }
 
 // Tail insertion over a pair split across peer buffers (positions are pair
 // relative: the (dst, src) plan of an explicit pair with lo = 0).
 template <typename V>
 __global__ void tail_gather_peer_kernel(const PeerParts<V> P, const uint64_t* __restrict__ dst,
-                                        const uint64_t* __restrict__ src, V* __restrict__ tmp, uint64_t n) {
+                                        const uint64_t* __restrict__ src, V* __restrict__ tmp, uint64_t n,
+                                        const PairPlan* __restrict__ plans) {
   uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const PeerAcc<V> acc{P};
   if (k < n && dst[k] != kNone) tmp[k] = acc.ld(src[k]);
+  if (blockIdx.x == gridDim.x - 1) tail_serial_pairs<V>(acc, plans, 1, 0, ~0ULL);
 }
 template <typename V>
 __global__ void tail_scatter_peer_kernel(const PeerParts<V> P, const uint64_t* __restrict__ dst,
@@ -1149,7 +1260,7 @@ __global__ void tail_scatter_peer_kernel(const PeerParts<V> P, const uint64_t* _
 
 template <typename V>
 static void tail_apply_peer_t(const PeerSpan& ps, const uint64_t* dst, const uint64_t* src, void* tmp,
-                              uint64_t nslots, cudaStream_t st) {
+                              uint64_t nslots, const PairPlan* plans, cudaStream_t st) {
   PeerParts<V> P{};
   P.n = ps.n;
   for (int k = 0; k < ps.n; ++k) {
@@ -1158,34 +1269,34 @@ static void tail_apply_peer_t(const PeerSpan& ps, const uint64_t* dst, const uin
   }
   P.start[ps.n] = ps.start[ps.n];
   unsigned b = (unsigned)((nslots + 255) / 256);
-  tail_gather_peer_kernel<V><<<b, 256, 0, st>>>(P, dst, src, (V*)tmp, nslots);
+  tail_gather_peer_kernel<V><<<b, 256, 0, st>>>(P, dst, src, (V*)tmp, nslots, plans);
   tail_scatter_peer_kernel<V><<<b, 256, 0, st>>>(P, dst, (const V*)tmp, nslots);
   count_launch();
   count_launch();
 }
 
 void launch_tail_apply_peer(int eb, const PeerSpan& ps, const uint64_t* dst, const uint64_t* src, void* tmp,
-                            uint64_t nslots, cudaStream_t st) {
+                            uint64_t nslots, const PairPlan* plans, cudaStream_t st) {
   if (!nslots) return;
-  if (eb == 4) tail_apply_peer_t<uint32_t>(ps, dst, src, tmp, nslots, st);
-  else tail_apply_peer_t<unsigned long long>(ps, dst, src, tmp, nslots, st);
+  if (eb == 4) tail_apply_peer_t<uint32_t>(ps, dst, src, tmp, nslots, plans, st);
+  else tail_apply_peer_t<unsigned long long>(ps, dst, src, tmp, nslots, plans, st);
+}
+
+template <typename V>
+static void tail_apply_t(void* buf, const uint64_t* dst, const uint64_t* src, void* tmp, uint64_t nslots,
+                         const PairPlan* plans, uint64_t npairs, uint64_t lo, uint64_t hi, cudaStream_t st) {
+  const unsigned b = (unsigned)((nslots + 255) / 256);
+  tail_gather_kernel<V><<<b, 256, 0, st>>>((V*)buf, dst, src, (V*)tmp, nslots, lo, hi, plans, npairs);
+  tail_scatter_kernel<V><<<b, 256, 0, st>>>((V*)buf, dst, (const V*)tmp, nslots, lo, hi);
+  count_launch();
+  count_launch();
 }
 
 void launch_tail_apply(int eb, void* buf, const uint64_t* dst, const uint64_t* src, void* tmp, uint64_t nslots,
-                       cudaStream_t st) {
+                       const PairPlan* plans, uint64_t npairs, uint64_t lo, uint64_t hi, cudaStream_t st) {
   if (!nslots) return;
-  unsigned b = (unsigned)((nslots + 255) / 256);
-  if (eb == 4) {
-    tail_gather_kernel<uint32_t><<<b, 256, 0, st>>>((const uint32_t*)buf, dst, src, (uint32_t*)tmp, nslots);
-    tail_scatter_kernel<uint32_t><<<b, 256, 0, st>>>((uint32_t*)buf, dst, (const uint32_t*)tmp, nslots);
-  } else {
-    tail_gather_kernel<unsigned long long><<<b, 256, 0, st>>>((const unsigned long long*)buf, dst, src,
-                                                              (unsigned long long*)tmp, nslots);
-    tail_scatter_kernel<unsigned long long><<<b, 256, 0, st>>>((unsigned long long*)buf, dst,
-                                                               (const unsigned long long*)tmp, nslots);
-  }
-  count_launch();
-  count_launch();
+  if (eb == 4) tail_apply_t<uint32_t>(buf, dst, src, tmp, nslots, plans, npairs, lo, hi, st);
+  else tail_apply_t<unsigned long long>(buf, dst, src, tmp, nslots, plans, npairs, lo, hi, st);
 }
 
 }  // namespace sk

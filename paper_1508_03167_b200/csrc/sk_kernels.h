@@ -23,6 +23,7 @@ void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64
 
 void debug_set_leaf_stop(int v);
 void debug_set_leaf_fallback(int v);
+void debug_set_warp_decode_max(int v);
 void debug_set_tree_force_direct(int v);
 
 // merge.cu
@@ -54,19 +55,19 @@ void launch_merge_tree(int eb, void* in, void* out, const PairPlan* plans, uint6
                        const uint64_t* chains, uint32_t tpp, cudaStream_t st);
 void launch_copy_tail_region(int eb, const void* in, void* out, const PairPlan* plans, uint64_t npairs,
                              cudaStream_t st);
-void launch_iota32(uint32_t* v, uint64_t n, cudaStream_t st);
-void launch_tail_plan(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair,
-                      const uint64_t* skey, const uint32_t* sval, uint64_t total, uint64_t* predx,
-                      uint8_t* keyed, uint64_t* dst, uint64_t* src, cudaStream_t st);
+void launch_tail_offsets(PairPlan* plans, uint64_t npairs, uint64_t cap, uint64_t* used, cudaStream_t st);
+void launch_tail_plan(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair, const uint64_t* used,
+                      uint64_t cap, uint64_t* hkey, uint32_t* hhead, uint32_t* next, uint32_t* slot_of, uint32_t hmask,
+                      uint64_t* predx, uint8_t* keyed, uint64_t* dst, uint64_t* src, cudaStream_t st);
 void launch_tail_chase(const PairPlan* plans, const uint64_t* rec_key, const uint32_t* rec_pair,
-                       const uint64_t* predx, const uint8_t* keyed, uint64_t total, uint64_t* dst, uint64_t* src,
-                       cudaStream_t st);
+                       const uint64_t* predx, const uint8_t* keyed, const uint64_t* used, uint64_t cap, uint64_t* dst,
+                       uint64_t* src, cudaStream_t st);
 void launch_merge_tree_peer(int eb, const PeerSpan& ps, const PairPlan* plans, const uint64_t* rank,
                             const uint64_t* chains, uint32_t tpp, uint32_t part, cudaStream_t st);
 void launch_tail_apply_peer(int eb, const PeerSpan& ps, const uint64_t* dst, const uint64_t* src, void* tmp,
-                            uint64_t nslots, cudaStream_t st);
+                            uint64_t nslots, const PairPlan* plans, cudaStream_t st);
 void launch_tail_apply(int eb, void* buf, const uint64_t* dst, const uint64_t* src, void* tmp, uint64_t nslots,
-                       cudaStream_t st);
+                       const PairPlan* plans, uint64_t npairs, uint64_t lo, uint64_t hi, cudaStream_t st);
 
 // rs.cu (Rao-Sandelius, §8 row F2)
 struct RsRange {              // a big range of one frontier level

@@ -61,7 +61,7 @@ struct PairPlan {
   uint32_t aex;         // 1: A exhausted (zero stop), 0: B exhausted
   uint32_t degenerate;  // n1 == 0 || n2 == 0: no bits, identity
   uint32_t nseg;        // segments [S_h, S_{h+1}) of the A queue, h < nseg; X = S_nseg
-  uint32_t pad;
+  uint32_t tail_slow;   // 1: the tail records did not fit the round's capacity -> serial tail
 };
 
 

@@ -83,3 +83,23 @@ def test_oracle_tasked_equals_sequential_pure_python_schedule():
             O.merge(b, j, k, l, st)
             tot += int(st[3])
     assert np.array_equal(a, b) and bits == tot
+
+
+def test_tail_length_statistics_behind_the_capacity_bound():
+    # csrc/engine.cu tail_capacity sizes a round's tail buffers as
+    # sum 0.80 sqrt(N) + 9 sqrt(sum 0.37 N): the tail of a pair of N elements
+    # has L = N - t insertions, t = min(select0(n1), select1(n2)) on its bit
+    # stream (_kernels.py:104-121).  Check the constants on pair streams.
+    rng = np.random.default_rng(3)
+    for N in (1 << 10, 1 << 14):
+        n1 = N // 2
+        L = []
+        for _ in range(3000):
+            b = rng.integers(0, 2, 2 * N + 10)
+            tz = np.searchsorted(np.cumsum(1 - b), n1 + 1)
+            to = np.searchsorted(np.cumsum(b), N - n1 + 1)
+            L.append(N - min(tz, to))
+        L = np.asarray(L, dtype=np.float64)
+        assert abs(L.mean() / np.sqrt(N) - 0.80) < 0.04
+        assert abs(L.var() / N - 0.37) < 0.05
+        assert L.max() < 0.80 * np.sqrt(N) + 9 * np.sqrt(0.37 * N)
