@@ -130,9 +130,16 @@ int sk_ipc_close(void *base);
 int sk_merge_shuffle_seq(void *data, int elem_bytes, uint64_t n, uint64_t cutoff, uint64_t state_io[4],
                          void *stream);
 
+/* Replaces _kernels.balanced_small_inplace (_kernels.py:546-553) and
+ * balanced.balanced_shuffle (balanced.py:219-245) for n <= 32 (SURVEY.md §8
+ * row F1): singleton leaves merged bottom-up, each pair interleaved along a
+ * word drawn as ONE fast dice roll below C(n1+n2, n1) from the source's
+ * stream and unranked lexicographically.  state_io as sk_fy_range. */
+int sk_balanced_small(void *data, int elem_bytes, uint64_t n, uint64_t state_io[4], void *stream);
+
 /* Replaces _kernels.chi_counts (_kernels.py:489-526) for algo "fy" (0),
- * "merge" (1) and "merge_parallel" (2); 2 <= n <= 20 ... counts_out: host
- * array of n! int64 bins.  Synchronizes. */
+ * "merge" (1), "merge_parallel" (2) and "balanced" (3); 2 <= n <= 20 ...
+ * counts_out: host array of n! int64 bins.  Synchronizes. */
 int sk_chi_counts(int algo, int n, uint64_t trials, uint64_t seed, uint64_t cutoff, int64_t *counts_out,
                   void *stream);
 

@@ -58,6 +58,8 @@ def lib():
         L.ora_fdr.argtypes = [ip, u64]
         L.ora_batched.restype = None
         L.ora_batched.argtypes = [ip, u64, u64, u64, u64, ip, ctypes.c_int]
+        L.ora_bs_small.restype = None
+        L.ora_bs_small.argtypes = [ip, ctypes.c_int, ip]
         L.ora_chi_counts.restype = None
         L.ora_chi_counts.argtypes = [ctypes.c_int, ctypes.c_int, u64, u64, u64, ip,
                                      ctypes.c_int]
@@ -114,6 +116,12 @@ def fdr(st: np.ndarray, bound: int) -> int:
     return int(lib().ora_fdr(_ptr(st), bound))
 
 
+def bs_small(arr: np.ndarray, st: np.ndarray) -> None:
+    """BalancedShuffle, n <= 32 (_kernels.py:292-341) on int64 arr, state in place."""
+    assert arr.dtype == np.int64 and arr.size <= 32
+    lib().ora_bs_small(_ptr(arr), arr.size, _ptr(st))
+
+
 def batched(batch: int, length: int, cutoff: int, seed: int, threads: int = 1):
     a = np.tile(np.arange(length, dtype=np.int64), batch)
     bits = np.zeros(batch, dtype=np.uint64)
@@ -121,7 +129,7 @@ def batched(batch: int, length: int, cutoff: int, seed: int, threads: int = 1):
     return a.reshape(batch, length), bits
 
 
-_CHI_ALGO = {"fy": 0, "merge": 1, "merge_parallel": 2}
+_CHI_ALGO = {"fy": 0, "merge": 1, "merge_parallel": 2, "balanced": 3}
 
 
 def chi_counts(algo: str, n: int, trials: int, seed: int, cutoff: int,

@@ -8,6 +8,7 @@ from .bitstream import BitSource, advance_state, mix64, substream_seed
 from .shufflers import (MERGE_CUTOFF_DEFAULT, MergeRange, ShuffleConfig, ShuffleReport, batched_shuffle,
                         fisher_yates, merge, merge_plan, merge_rounds, merge_shuffle, merge_shuffle_parallel,
                         merge_task_indices)
+from .balanced import balanced_shuffle
 from .splitshuffle import RS_CUTOFF_DEFAULT, rs_shuffle, rs_shuffle_parallel
 from .verify import ChiSquareResult, chi_counts, chi_square_threshold, chi_square_uniformity, permutation_rank
 
@@ -17,5 +18,5 @@ __all__ = [
     "BitSource", "mix64", "substream_seed", "advance_state", "MergeRange", "ShuffleConfig", "ShuffleReport", "MERGE_CUTOFF_DEFAULT", "fisher_yates",
     "merge", "merge_plan", "merge_rounds", "merge_task_indices", "merge_shuffle", "merge_shuffle_parallel",
     "batched_shuffle", "ChiSquareResult", "chi_counts", "chi_square_threshold", "chi_square_uniformity",
-    "permutation_rank", "RS_CUTOFF_DEFAULT", "rs_shuffle", "rs_shuffle_parallel",
+    "permutation_rank", "balanced_shuffle", "RS_CUTOFF_DEFAULT", "rs_shuffle", "rs_shuffle_parallel",
 ]

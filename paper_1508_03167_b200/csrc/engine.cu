@@ -1371,10 +1371,30 @@ int sk_merge_shuffle_seq(void* data, int elem_bytes, uint64_t n, uint64_t cutoff
   SK_CATCH
 }
 
+int sk_balanced_small(void* data, int elem_bytes, uint64_t n, uint64_t state_io[4], void* stream) {
+  if (int e = check_eb(elem_bytes)) return e;
+  if (!state_io || n > 32 || (n && !data)) { set_err("balanced_small: n <= 32 and a state"); return SK_EINVAL; }
+  if (state_io[2] > 63) { set_err("buffered_bits must be < 64"); return SK_EINVAL; }
+  if (n < 2) return SK_OK;
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  unsigned long long* d_bits;
+  CK(cudaMallocAsync((void**)&d_bits, 8, st));
+  CK(cudaMemsetAsync(d_bits, 0, 8, st));
+  uint64_t bits = 0;
+  launch_bs_small(elem_bytes, data, (int)n, desc_from_state(state_io), d_bits, st);
+  CK(cudaGetLastError());
+  fetch_bits(d_bits, &bits, 1, st);
+  CK(cudaFreeAsync(d_bits, st));
+  advance_state(state_io, bits);
+  SK_CATCH
+}
+
 int sk_chi_counts(int algo, int n, uint64_t trials, uint64_t seed, uint64_t cutoff, int64_t* counts_out,
                   void* stream) {
-  if (algo < 0 || algo > 2 || n < 1 || n > 20 || !counts_out) {
-    set_err("chi_counts: algo in {0,1,2}, 1 <= n <= 20");
+  if (algo < 0 || algo > 3 || n < 1 || n > 20 || !counts_out) {
+    set_err("chi_counts: algo in {0,1,2,3}, 1 <= n <= 20");
     return SK_EINVAL;
   }
   if (cutoff == 0) cutoff = 65536;

@@ -97,10 +97,23 @@ __global__ void __launch_bounds__(32 * kWarpDecodeWarps)
     const bool valid = lane < n;
     const uint32_t s = i - lane, b = s + 1;
     const uint32_t k0 = valid ? 32 - __clz(s) : 0u;
-    // sum of k0 over the lanes before: K for the steps >= 2^(K-1), K-1 below
-    const uint32_t K = 32 - __clz(i), lb = i + 1 - (1u << (K - 1));
-    const uint32_t pre = lane * K - (lane > lb ? lane - lb : 0u);
-    const uint32_t total_k0 = n * K - (n > lb ? n - lb : 0u);
+    // sum of k0 over the lanes before: for i >= 64 the batch's steps cross at
+    // most one power of two (K for the steps >= 2^(K-1), K-1 below), a closed
+    // form; the last batches by a warp scan
+    uint32_t pre, total_k0;
+    if (i >= 64) {
+      const uint32_t K = 32 - __clz(i), lb = i + 1 - (1u << (K - 1));
+      pre = lane * K - (lane > lb ? lane - lb : 0u);
+      total_k0 = n * K - (n > lb ? n - lb : 0u);
+    } else {
+      uint32_t x = k0;
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= (uint32_t)d) x += y;
+      }
+      pre = x - k0;
+      total_k0 = __shfl_sync(0xffffffffu, x, 31);
+    }
     uint64_t off = o + pre;
     uint32_t start = 0, ext = 0;
     for (;;) {

@@ -100,6 +100,7 @@ void launch_rs_copy_ranges(int eb, const uint64_t* list, uint32_t count, const v
 // misc.cu
 void launch_chi(int algo, int n, uint64_t trials, uint64_t seed, uint64_t cutoff, unsigned long long* counts,
                 cudaStream_t st);
+void launch_bs_small(int eb, void* data, int n, StreamDesc sd, unsigned long long* bits, cudaStream_t st);
 void launch_seq(int eb, void* data, uint64_t n, uint64_t cutoff, StreamDesc sd, unsigned long long* bits,
                 cudaStream_t st);
 

@@ -256,11 +256,11 @@ def _spanning_rounds_allgather(shard, seed, engine, c, q, bounds, nblk, local_ro
         i = (blk0 // (2 * p)) * (2 * p)  # first block of the spanning pair
         j, k, l = bounds[i], bounds[i + p], bounds[i + 2 * p]
         mx = max(sizes[g0:g0 + span])
-        send = torch.empty(mx, dtype=shard.dtype, device=shard.device)
+        send = torch.empty(mx, dtype=shard.dtype, device=_coll_device(shard))
         send[:shard.numel()] = shard
         parts = [torch.empty_like(send) for _ in range(span)]
         dist.all_gather(parts, send, group=groups.get(span, g0))
-        pair = torch.cat([parts[m][:sizes[g0 + m]] for m in range(span)])
+        pair = torch.cat([parts[m][:sizes[g0 + m]] for m in range(span)]).to(shard.device)
         pb = engine.merge(pair, 0, k - j, l - j, substream_seed(seed, r * q + i))
         shard.copy_(pair[lo - j:hi - j])
         if rank == g0:

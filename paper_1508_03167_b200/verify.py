@@ -19,7 +19,7 @@ from . import _lib
 from .bitstream import BitSource, substream_seed
 from .shufflers import MERGE_CUTOFF_DEFAULT
 
-_CHI_ALGO_IDS = {"fy": 0, "merge": 1, "merge_parallel": 2}
+_CHI_ALGO_IDS = {"fy": 0, "merge": 1, "merge_parallel": 2, "balanced": 3}
 CHI_ALGORITHMS = tuple(_CHI_ALGO_IDS)
 
 
