@@ -7,8 +7,8 @@ Run in the build container only (the reference is not on the GPU box):
 
 Writes tests/golden/cli.json: for each command line, the reference's exit
 code, stdout and stderr (wall-clock columns of `bench` are blanked).  The
-commands only use algorithms the B200 backend serves (fy, merge, rs; chisq
-for fy / merge / merge_parallel).
+commands only use algorithms the B200 backend serves (fy, merge, rs,
+balanced for n <= 32; chisq for fy / merge / merge_parallel / balanced).
 """
 from __future__ import annotations
 
@@ -39,6 +39,12 @@ CASES = [
     {"argv": ["verify", "--mode", "chisq", "--algo", "merge_parallel", "--n", "5", "--trials", "20000", "--seed",
               "2", "--cutoff", "1"]},
     {"argv": ["verify", "--mode", "chisq", "--algo", "fy", "--n", "4", "--trials", "5000", "--seed", "3"]},
+    # BalancedShuffle, the n <= 32 slice the B200 backend serves
+    {"argv": ["shuffle", "--algo", "balanced", "--n", "20", "--seed", "3", "--report"]},
+    {"argv": ["shuffle", "--algo", "balanced", "--seed", "13", "--report"], "stdin": "\n".join(f"w{i}" for i in range(29)) + "\n"},
+    {"argv": ["bench", "--algos", "balanced,merge", "--sizes", "5,17,32", "--trials", "4", "--seed", "2",
+              "--threads", "2"]},
+    {"argv": ["verify", "--mode", "chisq", "--algo", "balanced", "--n", "4", "--trials", "5000", "--seed", "3"]},
 ]
 
 
