@@ -2,7 +2,7 @@
 // shufflers.py:137-155, leaf tasks shufflers.py:268-278).
 //
 // Two stages:
-//  * decode (leaf_decode16b_kernel): one lane per leaf decodes the m-1
+//  * decode (leaf_decode_lane_kernel): one lane per leaf decodes the m-1
 //    fast-dice-roller draws j_i (i = m-1 .. 1) of its substream.  This is the
 //    only serial part: draws are variable-length, so draw k's bit offset
 //    depends on the draws before it.
@@ -23,11 +23,8 @@ namespace sk {
 // debug: stop the leaf-apply pipeline after phase k (phase timing experiments)
 __device__ int g_leaf_stop = 99;
 
-// One lane per leaf, one fast-dice-roller *iteration* per loop trip (so lanes
-// whose draws reject do not stall the others), bits served from a per-lane ring
-// of 32-bit half-words in shared memory that the warp tops up in bulk (uniform
-// mix64 work, no per-lane divergent word generation).  Bounds <= 65536, so one
-// iteration takes k <= 16 bits and TRIPS=16 iterations take at most 9 halves.
+// Bounds <= 65536: one FDR iteration takes k <= 16 bits, so TRIPS=16
+// iterations take at most 9 ring halves.
 constexpr int kDecodeTrips = 16;
 
 template <bool FRESH>
@@ -41,225 +38,11 @@ __device__ __forceinline__ uint64_t leaf_word(const StreamDesc& sd, uint64_t w) 
 // schedulers (single-warp blocks were observed to share them).
 constexpr int kDecodeBlock = 128;
 
-// One WARP per leaf, for jobs with few leaves (the lane-per-leaf kernel below
-// then leaves most of the GPU idle for the ~6 ms its per-lane chain of 65535
-// draws takes).  Batches of 32 consecutive steps: lane l takes step s = i - l
-// and first assumes that every earlier step of the batch accepts its first
-// FDR iteration (k0 = bit length of s), so its bit offset is o + the sum of
-// the earlier k0 -- a closed form, k0 takes at most two values in a batch.  A
-// ballot finds the first lane f whose first iteration rejects: the lanes
-// before f are final, lane f finishes its draw with the full FDR loop (e extra
-// bits), the lanes after f re-test at offsets shifted by e, and so on: one
-// phase per rejection (about a quarter of the draws).  Bit-identical to the
-// serial loop (_kernels.py:64-93).  Bits come from a per-warp ring of 64
-// words in shared memory, topped up 32 words at a time (one per lane).
-constexpr int kWarpDecodeWarps = 4;
-constexpr uint32_t kRingHalves = 128;    // 64 words = 4096 bits per warp
-constexpr uint64_t kRingAhead = 1536;    // bits kept available past the batch start
-static uint64_t g_warp_decode_max = 4096;  // jobs with at most this many leaves use the warp decode
-
-template <bool FRESH>
-__global__ void __launch_bounds__(32 * kWarpDecodeWarps)
-    leaf_decode_warp_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves, uint16_t* __restrict__ draws,
-                            unsigned long long* __restrict__ bits) {
-  __shared__ uint32_t ring_all[kWarpDecodeWarps][kRingHalves];
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint64_t g = (uint64_t)blockIdx.x * kWarpDecodeWarps + wid;
-  if (g >= nleaves) return;  // whole warp
-  uint32_t* const ring = ring_all[wid];
-  const LeafDesc L = leaf_desc(J, E, g);
-  const uint32_t m = (uint32_t)(L.hi - L.lo);
-  if (m < 2) return;
-  uint16_t* const dr = draws + L.lo;
-  uint64_t wgen = 0;  // words [wgen - 64, wgen) are in the ring
-  auto refill = [&]() {
-    const uint64_t x = leaf_word<FRESH>(L.sd, wgen + lane);
-    const uint32_t h = (uint32_t)((wgen + lane) * 2) & (kRingHalves - 1);
-    ring[h] = (uint32_t)(x >> 32);
-    ring[h + 1] = (uint32_t)x;
-    wgen += 32;
-    __syncwarp();
-  };
-  refill();
-  refill();
-  // 32 stream bits from bit p on (MSB first); outside the ring (a very long
-  // rejection chain) the words are generated directly
-  auto bits32 = [&](uint64_t p) -> uint32_t {
-    if (p + 32 > 64 * wgen) return (uint32_t)(bits64_at(L.sd, p) >> 32);
-    const uint32_t h = (uint32_t)(p >> 5);
-    return __funnelshift_l(ring[(h + 1) & (kRingHalves - 1)], ring[h & (kRingHalves - 1)], (uint32_t)p & 31);
-  };
-  uint64_t o = 0;      // bit offset of the batch's first draw
-  uint32_t i = m - 1;  // the batch's first step (bound i + 1)
-  while (i >= 1) {
-    while (o + kRingAhead > 64 * wgen) refill();
-    const uint32_t n = min(32u, i);
-    const bool valid = lane < n;
-    const uint32_t s = i - lane, b = s + 1;
-    const uint32_t k0 = valid ? 32 - __clz(s) : 0u;
-    // sum of k0 over the lanes before: for i >= 64 the batch's steps cross at
-    // most one power of two (K for the steps >= 2^(K-1), K-1 below), a closed
-    // form; the last batches by a warp scan
-    uint32_t pre, total_k0;
-    if (i >= 64) {
-      const uint32_t K = 32 - __clz(i), lb = i + 1 - (1u << (K - 1));
-      pre = lane * K - (lane > lb ? lane - lb : 0u);
-      total_k0 = n * K - (n > lb ? n - lb : 0u);
-    } else {
-      uint32_t x = k0;
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-        if (lane >= (uint32_t)d) x += y;
-      }
-      pre = x - k0;
-      total_k0 = __shfl_sync(0xffffffffu, x, 31);
-    }
-    uint64_t off = o + pre;
-    uint32_t start = 0, ext = 0;
-    for (;;) {
-      const bool live = valid && lane >= start;
-      uint32_t c = 0;
-      bool acc = true;
-      if (live) {
-        c = bits32(off) >> (32 - k0);
-        acc = c < b;
-      }
-      const uint32_t rej = __ballot_sync(0xffffffffu, live && !acc);
-      const uint32_t f = rej ? (uint32_t)__ffs(rej) - 1 : 32u;
-      if (live && lane < f) dr[s] = (uint16_t)c;
-      if (f == 32) break;
-      uint32_t e = 0;
-      if (lane == f) {  // the rest of this draw's FDR loop (_kernels.py:71-82)
-        uint32_t v = (1u << k0) - b, cc = c - b;
-        uint64_t p = off + k0;
-        for (;;) {
-          uint32_t k = __clz(v) - __clz(s);  // smallest k with v << k >= b  (s = b - 1)
-          k += ((v << k) <= s) ? 1u : 0u;
-          cc = (cc << k) | (bits32(p) >> (32 - k));
-          v <<= k;
-          p += k;
-          if (cc < b) break;
-          cc -= b;
-          v -= b;
-        }
-        dr[s] = (uint16_t)cc;
-        e = (uint32_t)(p - off - k0);
-      }
-      e = __shfl_sync(0xffffffffu, e, f);
-      ext += e;
-      if (lane > f) off += e;
-      start = f + 1;
-    }
-    o += total_k0 + ext;
-    i -= n;
-  }
-  if (lane == 0) atomicAdd(&bits[L.array], (unsigned long long)o);
-}
-
-// Leaner decode (same draws, same bit accounting): the step index i drives
-// everything -- the store address (dr + i), the flush condition ((lo + i) % 8
-// == 0), the head test (i > ih: draws whose 16-byte chunk reaches past the
-// leaf's last draw go out as single 16-bit stores) -- instead of a running
-// 64-bit pointer, the 8-draw shift register is four 32-bit words advanced by
-// byte permutes, and the FDR bit extraction is two funnel shifts.
-
-template <bool FRESH>
-__global__ void __launch_bounds__(kDecodeBlock) leaf_decode16b_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
-                                                                      uint16_t* __restrict__ draws,
-                                                                      unsigned long long* __restrict__ bits) {
-  __shared__ uint32_t ring[16][kDecodeBlock];
-  const uint32_t lane = threadIdx.x;
-  const uint64_t g = (uint64_t)blockIdx.x * kDecodeBlock + lane;
-  LeafDesc L;
-  uint32_t m = 0;
-  if (g < nleaves) {
-    L = leaf_desc(J, E, g);
-    m = (uint32_t)(L.hi - L.lo);
-  } else {
-    L.lo = 0; L.hi = 0; L.array = 0; L.sd = fresh_stream(0);
-  }
-  uint32_t i = m >= 2 ? m - 1 : 0;  // current step; its bound is i + 1
-  uint16_t* const dr = draws + L.lo;
-  const uint32_t al = (uint32_t)(L.lo & 7);
-  // draws i > ih are stored singly; chunks [i, i+7] with (lo + i) % 8 == 0 and i <= ih - 7 are flushed
-  const int32_t ih = (int32_t)m - 1 - (int32_t)((al + m) & 7);
-  uint64_t gw = 0;
-  uint32_t wr = 0;
-  if (i) {
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      uint64_t x = leaf_word<FRESH>(L.sd, gw++);
-      ring[wr & 15][lane] = (uint32_t)(x >> 32);
-      ring[(wr + 1) & 15][lane] = (uint32_t)x;
-      wr += 2;
-    }
-  }
-  uint32_t A = ring[0][lane], B = ring[1][lane], C = ring[2][lane], D = ring[3][lane];
-  uint32_t rd = 4;
-  uint32_t pos = 0;
-  uint32_t v = 1, c = 0;
-  uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;  // last 8 packed draws, newest in w0's low half
-  while (__any_sync(0xffffffffu, i != 0)) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (i != 0 && wr - rd <= 14) {
-        uint64_t x = leaf_word<FRESH>(L.sd, gw++);
-        ring[wr & 15][lane] = (uint32_t)(x >> 32);
-        ring[(wr + 1) & 15][lane] = (uint32_t)x;
-        wr += 2;
-      }
-    }
-#pragma unroll 4
-    for (int tr = 0; tr < kDecodeTrips; ++tr) {
-      const bool act = i != 0;
-      const uint32_t b = i + 1;
-      uint32_t k = __clz(v) - __clz(b);  // smallest k with v << k >= b
-      k += ((v << k) < b) ? 1u : 0u;
-      const uint32_t x = __funnelshift_l(B, A, pos);
-      const uint32_t cc = __funnelshift_l(x, c, k);  // (c << k) | top k bits of x
-      const bool acc = act && cc < b;
-      const bool single = acc && (int32_t)i > ih;
-      const bool push = acc && (int32_t)i <= ih;
-      uint16_t* const a = dr + i;
-      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.global.u16 [%1], %2;\n}" ::"r"(
-                       single ? 1u : 0u),
-                   "l"(a), "h"((unsigned short)cc));
-      if (push) {
-        w3 = __byte_perm(w2, w3, 0x5432);
-        w2 = __byte_perm(w1, w2, 0x5432);
-        w1 = __byte_perm(w0, w1, 0x5432);
-        w0 = __byte_perm(cc, w0, 0x5410);
-      }
-      const bool fl = push && ((al + i) & 7) == 0;
-      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.global.v4.u32 [%1], {%2, %3, %4, %5};\n}" ::"r"(
-                       fl ? 1u : 0u),
-                   "l"(a), "r"(w0), "r"(w1), "r"(w2), "r"(w3));
-      c = acc ? 0u : cc - b;
-      v = acc ? 1u : (v << k) - b;
-      i -= acc ? 1u : 0u;
-      pos += act ? k : 0u;
-      const bool cross = pos >= 32;
-      const uint32_t nxt = ring[rd & 15][lane];
-      pos = cross ? pos - 32 : pos;
-      A = cross ? B : A;
-      B = cross ? C : B;
-      C = cross ? D : C;
-      D = cross ? nxt : D;
-      rd += cross ? 1u : 0u;
-    }
-  }
-  if (m >= 2) {
-    // the pending (< 8) packed draws: dr[1 ..], draw 1 in w0's low half
-    const uint32_t f = 8 - ((al + 1) & 7) == 8 ? 1u : 8 - ((al + 1) & 7) + 1;  // first flush point >= 1
-    const uint32_t pend = (ih >= 8 && (int32_t)f + 7 <= ih) ? f - 1 : (ih > 0 ? (uint32_t)ih : 0u);
-    const uint32_t wv[4] = {w0, w1, w2, w3};
-    for (uint32_t k = 0; k < pend; ++k) dr[1 + k] = (uint16_t)(wv[k >> 1] >> (16 * (k & 1)));
-    atomicAdd(&bits[L.array], 32ull * (rd - 4) + pos);  // bits consumed = halves passed + pos
-  }
-}
-
-// Lean lane-per-leaf decode (same draws, same bit accounting as
-// leaf_decode16b_kernel), fewer instructions per FDR trip:
+// The decode: one lane per leaf, one fast-dice-roller ITERATION per loop trip
+// (lanes whose draw rejects do not stall the warp), bits served from a
+// per-lane ring of 32-bit half-words in shared memory that the warp tops up in
+// bulk (uniform mix64 work), extracted from a 4-half register window by two
+// funnel shifts.  Per trip:
 //  * the store address is a running 64-bit pointer (one 64-bit decrement per
 //    accepted draw instead of an address built from lo + i every trip);
 //  * every draw goes into the 8-draw shift register, and a full 16-byte
@@ -1053,30 +836,16 @@ __global__ void leaf_serial_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
 }
 
 // ---------------------------------------------------------------- launchers
-void debug_set_warp_decode_max(int v) { g_warp_decode_max = v < 0 ? 0 : (uint64_t)v; }
 void debug_set_leaf_fallback(int v) { cudaMemcpyToSymbol(g_leaf_force_fallback, &v, sizeof(int)); }
 void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int)); }
 
-static int g_lane_decode_lean = 1;  // lane-per-leaf jobs: 1 = leaf_decode_lane_kernel, 0 = leaf_decode16b_kernel
-void debug_set_lane_decode(int v) { g_lane_decode_lean = v; }
-
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
-                          unsigned long long* bits, cudaStream_t st, uint4* stash) {
+                          unsigned long long* bits, uint4* stash, cudaStream_t st) {
   if (!nleaves) return;
   unsigned blocks = (unsigned)((nleaves + kDecodeBlock - 1) / kDecodeBlock);
   const bool fresh = !(E.active && E.sd.plen != 0);
-  if (nleaves <= g_warp_decode_max) {
-    const unsigned wb = (unsigned)((nleaves + kWarpDecodeWarps - 1) / kWarpDecodeWarps);
-    if (fresh) leaf_decode_warp_kernel<true><<<wb, 32 * kWarpDecodeWarps, 0, st>>>(J, E, nleaves, draws, bits);
-    else leaf_decode_warp_kernel<false><<<wb, 32 * kWarpDecodeWarps, 0, st>>>(J, E, nleaves, draws, bits);
-  } else if (g_lane_decode_lean && stash) {
-    if (fresh) leaf_decode_lane_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, stash, bits);
-    else leaf_decode_lane_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, stash, bits);
-  } else if (fresh) {
-    leaf_decode16b_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
-  } else {
-    leaf_decode16b_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, bits);
-  }
+  if (fresh) leaf_decode_lane_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, stash, bits);
+  else leaf_decode_lane_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, stash, bits);
   count_launch();
 }
 

@@ -129,9 +129,9 @@ def test_config4_2p33_uint64_one_gpu_equals_8_shards():
     from paper_1508_03167_b200 import distributed as D
     shards = []
     for r in range(8):
-        lo, hi = D.shard_range(n, None, 8, r)
+        lo, hi = D.shard_range(n, 65536, 8, r)
         shards.append(torch.arange(lo, hi, dtype=torch.int64, device="cuda"))
-    bits8 = D.merge_shuffle_multi(shards, n, None, seed)
+    bits8 = D.merge_shuffle_multi(shards, n, 65536, seed)
     assert bits8 == bits1
     fp8, off = 0, 0
     for t in shards:

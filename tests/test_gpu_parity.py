@@ -343,7 +343,7 @@ def test_merge_shuffle_multi_single_process(world, n, dt):
     assert np.array_equal(torch.cat(shards).cpu().numpy().astype(np.int64), ref)
 
 
-@pytest.mark.parametrize("variant", ["v3", "fallback", "quadratic", "lane_decode", "lane_decode_16b", "warp_decode"])
+@pytest.mark.parametrize("variant", ["v3", "fallback", "quadratic"])
 def test_leaf_apply_variants(variant):
     # leaves of 8193..65536 elements: the one-pass byte-counter kernel (v3)
     # and its serial fallback (counter overflow, forced for every leaf): same
@@ -353,10 +353,7 @@ def test_leaf_apply_variants(variant):
     lib = _lib.load()
     lib.sk_debug_set.argtypes = [ctypes.c_int, ctypes.c_int]
     # quadratic: v3 with every bucket of >= 9 steps through the O(k^2) path
-    # lane_decode / warp_decode: every job's leaf draws by the lane-per-leaf
-    # kernel / by the warp-per-leaf speculative kernel
-    knobs = {"v3": [], "fallback": [(6, 1)], "quadratic": [(1, 12)], "lane_decode": [(7, 0)],
-             "lane_decode_16b": [(7, 0), (8, 0)], "warp_decode": [(7, 1 << 30)]}[variant]
+    knobs = {"v3": [], "fallback": [(6, 1)], "quadratic": [(1, 12)]}[variant]
     for k, v in knobs:
         lib.sk_debug_set(k, v)
     try:
@@ -373,8 +370,6 @@ def test_leaf_apply_variants(variant):
     finally:
         lib.sk_debug_set(6, 0)
         lib.sk_debug_set(1, 99)
-        lib.sk_debug_set(7, 4096)
-        lib.sk_debug_set(8, 1)
 
 
 def test_more_than_65535_pairs_in_a_round():
