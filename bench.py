@@ -216,6 +216,35 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def pcie_roofline(host, dev, step_s, reps=3):
+    """The e2e step's transfer floor: the pinned host<->device copy rates of
+    this box measured here (the step's own buffers, one direction at a time,
+    CUDA events, best of `reps`), the floor = H2D bytes / H2D rate + D2H
+    bytes / D2H rate (the shuffle needs all its input before its last round
+    and produces its output only after it, so the two transfers cannot
+    overlap each other), and the fraction floor / measured e2e step time."""
+    import torch
+    nbytes = host.numel() * host.element_size()
+    st = torch.cuda.current_stream()
+    rates = {}
+    for name, fn in (("h2d", lambda: dev.copy_(host, non_blocking=True)),
+                     ("d2h", lambda: host.copy_(dev, non_blocking=True))):
+        best = None
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        rates[name] = nbytes / (best * 1e-3) / 1e9
+    floor_s = nbytes / (rates["h2d"] * 1e9) + nbytes / (rates["d2h"] * 1e9)
+    return {"bound": "pcie", "h2d_gbs": round(rates["h2d"], 2), "d2h_gbs": round(rates["d2h"], 2),
+            "floor_ms": round(floor_s * 1e3, 2), "step_ms": round(step_s * 1e3, 2),
+            "frac": round(floor_s / step_s, 4)}
+
+
 def traffic_from_profile():
     p = os.path.join(ROOT, "profiles", "merge_kernel_traffic.json")
     try:
@@ -408,6 +437,7 @@ def main():
                "h2d_bytes_per_step": 4 * n_total, "d2h_bytes_per_step": 4 * n_total + 8 * world,
                "path": ("sk_merge_shuffle_parallel_host (C ABI), pinned host buffer" if world == 1 else
                         "per rank: pinned host shard -> device, merge_shuffle_sharded, device -> host")}
+        e2e["roofline"] = pcie_roofline(host, x, el / args.e2e_steps)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -896,6 +896,7 @@ int sk_debug_set(int key, int value) {
   if (key == 1) { debug_set_leaf_stop(value); return 0; }
   if (key == 4) { debug_set_tree_force_direct(value); return 0; }
   if (key == 6) { debug_set_leaf_fallback(value); return 0; }
+  if (key == 7) { debug_set_leaf_l2pol(value); return 0; }
   return -1;
 }
 const char* sk_last_error(void) { return g_err.c_str(); }

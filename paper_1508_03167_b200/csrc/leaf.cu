@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(BLOCK) leaf_apply_kernel(ArrayJob J, ExplicitT
 //  7. H into shared memory (over the buckets), then every output gathers
 //     orig[W(N(s))] (W: follow H to its root) or orig[j_s]; 16-byte stores.
 __device__ int g_leaf_force_fallback = 0;
+static int g_leaf_l2pol_host = 1;  // debug knob (host side): 0 = no L2 eviction hints (A/B timing)
 
 __device__ __forceinline__ void cx(uint32_t& a, uint32_t& b) {
   const uint32_t lo = min(a, b), hi = max(a, b);
@@ -426,7 +427,7 @@ __device__ __forceinline__ void sort_net16(uint32_t* k) {
 // gather stages `chunk` elements per pass; when one chunk holds the whole
 // leaf every source is read before any output is written, so in == out is
 // allowed (the pure Fisher-Yates jobs run in place).
-template <typename V, int BLOCK, int NP>
+template <typename V, int BLOCK, int NP, bool POL = true>
 __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
     leaf_apply_v3_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves, const V* __restrict__ in, V* __restrict__ out,
                          const uint16_t* __restrict__ draws, uint16_t* scratch, uint32_t mmax,
@@ -460,6 +461,11 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
     s_stop = g_leaf_stop;
   }
   __syncthreads();
+// L2 policies: scratch and half-written output lines stay (evict_last), the
+// leaf's input and its final output lines stream (evict_first); created at the
+// use (uniform registers)
+#define POL_LAST (POL ? l2_policy_last() : l2_policy_normal())
+#define POL_FIRST (POL ? l2_policy_first() : l2_policy_normal())
 #define Hg (s_hg)
 #define lst (s_hg + mr)
 #define tmp (s_hg + 2 * mr)
@@ -630,9 +636,9 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
         const uint32_t v1 = k >= 2 ? (uint32_t)bkt[st + 1] : 0u;
         uint32_t H = 0;
         if (k >= 9) {  // queued from the top of the list area
-          lst[mr - 1 - atomicAdd(&s_nhuge, 1u)] = (uint16_t)p;
+          st_pol(lst + (mr - 1 - atomicAdd(&s_nhuge, 1u)), (uint16_t)p, POL_LAST);
         } else if (k >= 3) {
-          lst[atomicAdd(&s_nlong, 1u)] = (uint16_t)p;
+          st_pol(lst + atomicAdd(&s_nlong, 1u), (uint16_t)p, POL_LAST);
         } else if (k == 1) {
           bkt[st] = (uint16_t)p;
           H = v0 > p ? v0 : 0u;
@@ -644,7 +650,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
         }
         Hq[q] = H;
       }
-      *reinterpret_cast<uint2*>(Hg + 4 * w) = make_uint2(Hq[0] | (Hq[1] << 16), Hq[2] | (Hq[3] << 16));
+      st_pol2(reinterpret_cast<uint32_t*>(Hg + 4 * w), Hq[0] | (Hq[1] << 16), Hq[2] | (Hq[3] << 16), POL_LAST);
     }
     __syncthreads();
     if (s_stop <= 4) continue;
@@ -652,7 +658,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
     //    through a sorting network; the entry at sorted position a gets the
     //    step at a + 1 (or the target itself at the end)
     for (uint32_t i = tid; i < s_nlong; i += BLOCK) {
-      const uint32_t p = lst[i];
+      const uint32_t p = ld_pol(lst + i, POL_LAST);
       const uint32_t w = p >> 2, q = p & 3;
       const uint32_t cw = cnt[w];
       const uint32_t en = (cw >> (8 * q)) & 0xFFu;
@@ -667,12 +673,12 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
       for (int a = 0; a < 8; ++a)
         if ((uint32_t)a < k)
           bkt[key[a] & 0xFFFFu] = (uint16_t)((uint32_t)(a + 1) < k ? (key[a < 7 ? a + 1 : 7] >> 16) : p);
-      Hg[p] = (uint16_t)((key[0] >> 16) > p ? (key[0] >> 16) : (key[1] >> 16));
+      st_pol(Hg + p, (uint16_t)((key[0] >> 16) > p ? (key[0] >> 16) : (key[1] >> 16)), POL_LAST);
     }
     //    buckets of >= 9 steps (the first few hundred targets), one per warp:
     //    a warp bitonic sort of the keys (<= 32 entries)
     for (uint32_t i = wid; i < s_nhuge; i += BLOCK / 32) {
-      const uint32_t p = lst[mr - 1 - i];
+      const uint32_t p = ld_pol(lst + (mr - 1 - i), POL_LAST);
       const uint32_t w = p >> 2, q = p & 3;
       const uint32_t cw = cnt[w];
       const uint32_t en = (cw >> (8 * q)) & 0xFFu;
@@ -691,7 +697,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
         const uint32_t nxt = __shfl_down_sync(0xffffffffu, key, 1);
         const uint32_t k1 = __shfl_sync(0xffffffffu, key, 1);
         if (lane < k) bkt[key & 0xFFFFu] = (uint16_t)(lane + 1 < k ? (nxt >> 16) : p);
-        if (lane == 0) Hg[p] = (uint16_t)((key >> 16) > p ? (key >> 16) : (k1 >> 16));
+        if (lane == 0) st_pol(Hg + p, (uint16_t)((key >> 16) > p ? (key >> 16) : (k1 >> 16)), POL_LAST);
       } else if (lane == 0) {  // > 32 steps on one target: O(k^2) through the scratch
         uint32_t H = 0x10000u;
         for (uint32_t a = 0; a < k; ++a) {
@@ -726,7 +732,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
     // 7. H into shared memory (over the buckets); every output's source:
     //    W(N(s)) (follow H to its root) or j_s; W(0) for output 0
     for (uint32_t w = tid; w < ((m + 7) >> 3); w += BLOCK)
-      reinterpret_cast<uint4*>(bkt)[w] = reinterpret_cast<const uint4*>(Hg)[w];
+      reinterpret_cast<uint4*>(bkt)[w] = ld_pol4(Hg + 8 * w, POL_LAST);
     __syncthreads();
     if (s_stop <= 6) continue;
     {
@@ -759,8 +765,8 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
           if (s_stop != 11) {
             mbar_arrive_expect_tx(&s_bar, cn * (uint32_t)sizeof(V));
             for (uint32_t o = 0; o < cn * (uint32_t)sizeof(V); o += 65536u)
-              bulk_g2s(reinterpret_cast<char*>(sdata) + o, reinterpret_cast<const char*>(src_in + c0) + o,
-                       min(65536u, cn * (uint32_t)sizeof(V) - o), &s_bar);
+              bulk_g2s_pol(reinterpret_cast<char*>(sdata) + o, reinterpret_cast<const char*>(src_in + c0) + o,
+                           min(65536u, cn * (uint32_t)sizeof(V) - o), &s_bar, POL_FIRST);
           } else {
             mbar_arrive_expect_tx(&s_bar, 0u);  // timing: no staging
           }
@@ -776,26 +782,28 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
       V* dpass;
       asm volatile("mov.b64 %0, %1;" : "=l"(dpass) : "l"(dst + 2 * tid));
       const bool pair8 = ((((uintptr_t)dst) & (2 * sizeof(V) - 1)) == 0) && s_stop < 8;
+      // lines completed by a later pass stay in L2 until then
+      const bool olast = c0 + cn < m;
       // ... and the per-output source extraction from being hoisted likewise
 #pragma unroll
       for (int i = 0; i < (int)NP; ++i) asm volatile("" : "+r"(r[i]));
-      if (pair8) {
-        // a step pair whose two sources are in this chunk goes out as one
-        // 2-element store, otherwise the one present element singly
-#pragma unroll
-        for (int i = 0; i < (int)NP; ++i) {
-          const uint32_t s0 = (r[i] & 0xFFFFu) - c0, s1 = (r[i] >> 16) - c0;
-          const bool i0 = s0 < cn, i1 = s1 < cn;
-          if (i0 && i1) {
-            if constexpr (sizeof(V) == 4) {
-              *reinterpret_cast<uint2*>(dpass + 2 * BLOCK * i) = make_uint2(sdata[s0], sdata[s1]);
-            } else {
-              *reinterpret_cast<ulonglong2*>(dpass + 2 * BLOCK * i) = make_ulonglong2(sdata[s0], sdata[s1]);
-            }
-          } else if (i0 || i1) {
-            dpass[2 * BLOCK * i + (i1 ? 1 : 0)] = sdata[i1 ? s1 : s0];
-          }
-        }
+      // a step pair whose two sources are in this chunk goes out as one
+      // 2-element store, otherwise the one present element singly (one copy of
+      // the loop per policy: the policy stays a uniform constant)
+#define SK_GATHER_PAIRS(PLC)                                                      \
+  _Pragma("unroll") for (int i = 0; i < (int)NP; ++i) {                           \
+    const uint32_t s0 = (r[i] & 0xFFFFu) - c0, s1 = (r[i] >> 16) - c0;            \
+    const bool i0 = s0 < cn, i1 = s1 < cn;                                        \
+    if (i0 && i1) {                                                               \
+      st_pol2(dpass + 2 * BLOCK * i, sdata[s0], sdata[s1], PLC);                  \
+    } else if (i0 || i1) {                                                        \
+      st_pol(dpass + 2 * BLOCK * i + (i1 ? 1 : 0), sdata[i1 ? s1 : s0], PLC);     \
+    }                                                                             \
+  }
+      if (pair8 && olast) {
+        SK_GATHER_PAIRS(POL_LAST)
+      } else if (pair8) {
+        SK_GATHER_PAIRS(POL_FIRST)
       } else {
 #pragma unroll
       for (int i = 0; i < (int)NP; ++i)
@@ -809,6 +817,9 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? 4 : 1)
     }
   }
 }
+#undef SK_GATHER_PAIRS
+#undef POL_LAST
+#undef POL_FIRST
 #undef Hg
 #undef lst
 #undef tmp
@@ -837,6 +848,7 @@ __global__ void leaf_serial_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
 
 // ---------------------------------------------------------------- launchers
 void debug_set_leaf_fallback(int v) { cudaMemcpyToSymbol(g_leaf_force_fallback, &v, sizeof(int)); }
+void debug_set_leaf_l2pol(int v) { g_leaf_l2pol_host = v; }
 void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int)); }
 
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
@@ -882,7 +894,7 @@ static void leaf_apply_t(const ArrayJob& J, const ExplicitTask& E, uint64_t nlea
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k<<<grid, 256, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
     } else {
-      auto k = leaf_apply_v3_kernel<V, 1024, 32>;
+      auto k = g_leaf_l2pol_host ? leaf_apply_v3_kernel<V, 1024, 32, true> : leaf_apply_v3_kernel<V, 1024, 32, false>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k<<<grid, 1024, smem, st>>>(J, E, nleaves, (const V*)in, (V*)out, draws, scratch, mmax, list);
     }

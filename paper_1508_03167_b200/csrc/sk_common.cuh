@@ -74,6 +74,54 @@ __device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
 }
 
+// L2 eviction policies (createpolicy) and global accesses carrying them: the
+// leaf apply keeps its per-CTA scratch and half-written output lines resident
+// (evict_last) and streams the data it reads once (evict_first).
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_normal() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_pol(uint16_t* a, uint16_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(a), "h"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_pol(uint32_t* a, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_pol(unsigned long long* a, unsigned long long v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(a), "l"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_pol2(uint32_t* a, uint32_t x, uint32_t y, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(a), "r"(x), "r"(y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_pol2(unsigned long long* a, unsigned long long x, unsigned long long y,
+                                        uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(a), "l"(x), "l"(y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint16_t ld_pol(const uint16_t* a, uint64_t pol) {
+  uint16_t v;
+  asm volatile("ld.global.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(pol) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint4 ld_pol4(const void* a, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(a), "l"(pol)
+               : "memory");
+  return v;
+}
+
 // Number of one-bits in [0, pos) of a stream whose superblock prefix table R
 // holds ones in [0, 512k) at R[k].
 __device__ __forceinline__ uint64_t rank_bits(const StreamDesc& d, const uint64_t* R, uint64_t pos) {
@@ -235,6 +283,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_pol(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 // shared -> global bulk copy (bulk-group completion), its commit and the wait
 // until the shared source may be reused; generic-proxy smem writes must be

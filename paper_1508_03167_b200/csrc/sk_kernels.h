@@ -24,6 +24,7 @@ void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64
 
 void debug_set_leaf_stop(int v);
 void debug_set_leaf_fallback(int v);
+void debug_set_leaf_l2pol(int v);
 void debug_set_tree_force_direct(int v);
 
 // merge.cu
