@@ -37,6 +37,7 @@ SIGNATURES = {
     "sk_merge_range": (_int, [_vp, _int, _u64, _u64, _u64, _u64p, _vp]),
     "sk_merge_shuffle_seq": (_int, [_vp, _int, _u64, _u64, _u64p, _vp]),
     "sk_balanced_small": (_int, [_vp, _int, _u64, _u64p, _vp]),
+    "sk_balanced_shuffle": (_int, [_vp, _int, _u64, _u64p, _vp]),
     "sk_chi_counts": (_int, [_int, _int, _u64, _u64, _u64, ctypes.POINTER(ctypes.c_int64), _vp]),
     "sk_last_error": (ctypes.c_char_p, []),
     "sk_version": (_int, []),

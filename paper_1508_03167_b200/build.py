@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libshufflekit_b200.so")
-SOURCES = ["engine.cu", "leaf.cu", "merge.cu", "misc.cu", "rs.cu"]
+SOURCES = ["engine.cu", "leaf.cu", "merge.cu", "misc.cu", "rs.cu", "balanced.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr"]

@@ -1391,6 +1391,31 @@ int sk_balanced_small(void* data, int elem_bytes, uint64_t n, uint64_t state_io[
   SK_CATCH
 }
 
+int sk_balanced_shuffle(void* data, int elem_bytes, uint64_t n, uint64_t state_io[4], void* stream) {
+  if (n <= 32) return sk_balanced_small(data, elem_bytes, n, state_io, stream);
+  if (int e = check_eb(elem_bytes)) return e;
+  if (!state_io || !data) { set_err("balanced_shuffle: data and a state"); return SK_EINVAL; }
+  if (state_io[2] > 63) { set_err("buffered_bits must be < 64"); return SK_EINVAL; }
+  if (n > balanced_max_n()) { set_err("balanced_shuffle: n above the supported 2^17"); return SK_EINVAL; }
+  SK_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  setup_pool_once();
+  unsigned long long* d_bits;
+  CK(cudaMallocAsync((void**)&d_bits, 8, st));
+  CK(cudaMemsetAsync(d_bits, 0, 8, st));
+  uint64_t bits = 0;
+  try {
+    run_balanced(elem_bytes, data, n, desc_from_state(state_io), d_bits, st);
+    fetch_bits(d_bits, &bits, 1, st);
+  } catch (...) {
+    cudaFreeAsync(d_bits, st);
+    throw;
+  }
+  CK(cudaFreeAsync(d_bits, st));
+  advance_state(state_io, bits);
+  SK_CATCH
+}
+
 int sk_chi_counts(int algo, int n, uint64_t trials, uint64_t seed, uint64_t cutoff, int64_t* counts_out,
                   void* stream) {
   if (algo < 0 || algo > 3 || n < 1 || n > 20 || !counts_out) {

@@ -98,6 +98,10 @@ void launch_rs_leaf_serial(int eb, const RsLeaf* L, uint32_t count, const RsTask
 void launch_rs_copy_ranges(int eb, const uint64_t* list, uint32_t count, const void* from, void* to,
                            cudaStream_t st);
 
+// balanced.cu (BalancedShuffle beyond n <= 32, §8 row F1)
+uint64_t balanced_max_n();
+void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long long* d_bits, cudaStream_t st);
+
 // misc.cu
 void launch_chi(int algo, int n, uint64_t trials, uint64_t seed, uint64_t cutoff, unsigned long long* counts,
                 cudaStream_t st);
