@@ -12,12 +12,15 @@
 // Every pair draws from the caller's ONE stream in schedule order, so the
 // stream offset of pair p depends on the consumption of every earlier pair;
 // the word of a pair, though, depends only on its rank.  Three stages:
-//   A. ranks (one thread, schedule order): per pair the exact class size
-//      C(m, n1), the fast dice roll below it on multi-limb integers, the rank
+//   A. ranks (one warp, schedule order): per pair the exact class size
+//      C(m, n1) and the fast dice roll below it -- machine words for m <= 64
+//      (one lane), multi-limb integers on the whole warp above; the rank
 //      stored; the stream position at the end gives the bits consumed;
-//   B. words (one thread per pair, all pairs at once): the recursive-halving
-//      unranking on multi-limb integers, m <= 32 pieces by the lexicographic
-//      walk; one byte per position;
+//   B. words: the recursive-halving unranking.  Pairs above kBsTop positions
+//      get a warp each for their splits above kBsTop (bs_split on WarpOps);
+//      the sub-problems of <= kBsTop positions they leave, and the pairs of <=
+//      kBsTop positions, are tasks of one thread each (bs_split on
+//      SerialOps, m <= 32 by the lexicographic walk); one byte per position;
 //   C. interleave (one launch per level, one thread per pair).
 // Big naturals are little-endian 32-bit limbs with tracked lengths.  Exact
 // class sizes are products of prime powers (Legendre), divisions in the split
@@ -28,25 +31,207 @@
 #include <vector>
 #include "sk_kernels.h"
 #include "bs_core.cuh"
+#include "bs_warp.cuh"
 
 namespace sk {
 // (the multi-limb naturals and the per-pair stages: bs_core.cuh)
 
-__global__ void bs_ranks_kernel(const BsPair* __restrict__ pairs, uint32_t npairs, StreamDesc sd,
-                                const uint32_t* __restrict__ primes, uint32_t nprimes, uint32_t* pool,
-                                uint32_t* work, uint32_t wl, unsigned long long* bits) {
-  if (blockIdx.x || threadIdx.x) return;
-  bits[0] = bs_ranks(pairs, npairs, sd, primes, nprimes, pool, work, wl);
+
+constexpr uint32_t kBsTop = 1024;  // pairs / sub-problems above this many positions: a warp
+
+// A sub-problem of stage B: the word of m positions with k zeros and rank at
+// pool + rank_off ([limb count, limbs]), into words + word_off; its serial
+// scratch at scratch + scr_off (m > 32).
+struct BsJob {
+  uint32_t m, k;
+  uint64_t word_off, rank_off, scr_off;
+};
+// device-side bump counters of stage B
+struct BsCounters {
+  unsigned long long njobs, pool_top, scr_top;
+};
+
+// bits [o, o + k) of the stream, k <= 64
+__device__ __forceinline__ uint64_t bs_bits64(const StreamDesc& sd, uint64_t o, uint32_t k) {
+  const uint64_t w = o >> 6;
+  const uint32_t s = (uint32_t)(o & 63);
+  uint64_t x = bs_word(sd, w);
+  if (s) x = (x << s) | (bs_word(sd, w + 1) >> (64 - s));
+  return k == 64 ? x : (x >> (64 - k));
 }
 
-__global__ void bs_words_kernel(const BsPair* __restrict__ pairs, uint32_t npairs, const uint32_t* __restrict__ pool,
-                                uint32_t* __restrict__ scratch, const uint32_t* __restrict__ primes, uint32_t nprimes,
-                                uint8_t* __restrict__ words) {
+// A. (one warp)
+constexpr uint32_t kBsWord = 64;  // C(m, n1) < 2^62 for m <= 64
+__global__ void __launch_bounds__(32) bs_ranks_kernel(const BsPair* __restrict__ pairs, uint32_t npairs,
+                                                      StreamDesc sd, const uint32_t* __restrict__ primes,
+                                                      uint32_t nprimes, uint32_t* pool, uint32_t wl,
+                                                      unsigned long long* bits) {
+  __shared__ uint64_t Cw[(kBsWord + 1) * (kBsWord + 1)];  // C(a, b), a, b <= 64 (Pascal)
+  extern __shared__ uint32_t work[];                     // B, v, c and a spare: wl limbs each
+  const uint32_t lane = threadIdx.x;
+  for (uint32_t a = 0; a <= kBsWord; ++a) {
+    for (uint32_t b = lane; b <= kBsWord; b += 32)
+      Cw[a * (kBsWord + 1) + b] =
+          b > a ? 0ull : (b == 0 || b == a ? 1ull : Cw[(a - 1) * (kBsWord + 1) + b - 1] + Cw[(a - 1) * (kBsWord + 1) + b]);
+    __syncwarp();
+  }
+  uint32_t* B = work;
+  uint32_t* v = work + wl;
+  uint32_t* c = work + 2 * wl;
+  uint32_t* t = work + 3 * wl;
+  uint32_t nB = 0, cm = 0, cn1 = 0;
+  uint64_t o = 0;  // stream offset (uniform)
+  uint32_t bn1 = 0, bn2 = 0;
+  uint64_t broff = 0;
+  for (uint32_t p = 0; p < npairs; ++p) {
+    if ((p & 31) == 0 && p + lane < npairs) {  // the next 32 pairs' sizes, one per lane (coalesced)
+      const BsPair Q = pairs[p + lane];
+      bn1 = Q.n1;
+      bn2 = Q.n2;
+      broff = Q.rank_off;
+    }
+    BsPair P;
+    P.n1 = __shfl_sync(wb::kFull, bn1, p & 31);
+    P.n2 = __shfl_sync(wb::kFull, bn2, p & 31);
+    P.rank_off = __shfl_sync(wb::kFull, broff, p & 31);
+    const uint32_t m = P.n1 + P.n2;
+    uint32_t* R = pool + P.rank_off;
+    if (m <= kBsWord) {  // bitstream.py:187-210 in machine words (one lane)
+      if (lane == 0) {
+        const uint64_t bound = Cw[m * (kBsWord + 1) + P.n1];
+        const uint32_t lb = 64 - __clzll(bound - 1);  // bits of bound - 1
+        uint64_t vv = 1, cc = 0;
+        for (;;) {
+          uint32_t k = lb - (64 - __clzll(vv));  // smallest k with vv << k >= bound
+          if ((vv << k) < bound) ++k;
+          cc = (cc << k) | (k ? bs_bits64(sd, o, k) : 0ull);
+          o += k;
+          vv <<= k;
+          if (cc < bound) break;
+          cc -= bound;
+          vv -= bound;
+        }
+        R[0] = cc ? (cc >> 32 ? 2u : 1u) : 0u;
+        R[1] = (uint32_t)cc;
+        R[2] = (uint32_t)(cc >> 32);
+      }
+      o = __shfl_sync(wb::kFull, o, 0);
+      continue;
+    }
+    if (m != cm || P.n1 != cn1) {  // pairs of a level repeat a handful of sizes
+      nB = wb::binom(B, m, P.n1, primes, nprimes);
+      cm = m;
+      cn1 = P.n1;
+    }
+    // fast dice roller below B (>= 2): v = 1, c = 0
+    if (lane == 0) v[0] = 1;
+    __syncwarp();
+    uint32_t nv = 1, nc = 0;
+    const uint32_t lb = wb::bitlen(B, nB);
+    for (;;) {
+      uint32_t k = lb - wb::bitlen(v, nv);  // smallest k with v << k >= B
+      if (wb::cmp_shl(v, nv, k, B, nB) < 0) ++k;
+      // c = (c << k) | the next k bits: limb i of them is stream bits
+      // [o + k - 32(i+1), o + k - 32 i)
+      nc = wb::shl(t, c, nc, k);
+      const uint32_t full = k >> 5, part = k & 31, nk = full + (part ? 1u : 0u);
+      for (uint32_t i = nc + lane; i < nk; i += 32) t[i] = 0;
+      __syncwarp();
+      for (uint32_t i = lane; i < full; i += 32) t[i] |= bs_bits(sd, o + k - 32 * (i + 1), 32);
+      if (part && lane == 0) t[full] |= bs_bits(sd, o, part);
+      __syncwarp();
+      nc = wb::trim(t, nc > nk ? nc : nk);
+      { uint32_t* x = c; c = t; t = x; }
+      o += k;
+      nv = wb::shl(t, v, nv, k);
+      { uint32_t* x = v; v = t; t = x; }
+      if (wb::cmp(c, nc, B, nB) < 0) break;
+      nc = wb::sub(c, c, nc, B, nB);
+      nv = wb::sub(v, v, nv, B, nB);
+    }
+    if (lane == 0) R[0] = nc;
+    wb::copy(R + 1, c, nc);
+  }
+  if (lane == 0) bits[0] = o;
+}
+
+// B1. the splits above kBsTop of the pairs above kBsTop: one warp (and one
+// block) per pair, its numbers in shared memory: the pending sub-ranks
+// (W + 64 limbs), the current rank (W) and bs_split's working numbers.
+struct BsWarpTask {
+  uint32_t m, k, off, rlen;
+  uint64_t rank;
+};
+__host__ __device__ inline uint64_t bs_top_smem_limbs(uint32_t M) {
+  const uint32_t W = bs_limbs(M), H = W / 2 + 3;
+  return (uint64_t)W + 64 + W + BsWork::limbs(W, H);
+}
+__global__ void __launch_bounds__(32) bs_top_kernel(const BsPair* __restrict__ pairs, const uint32_t* __restrict__ big,
+                                                    const uint32_t* __restrict__ primes, uint32_t nprimes, BsJob* jobs,
+                                                    uint32_t* pool, uint64_t pool_cap, uint64_t scr_base,
+                                                    BsCounters* cnt) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t lane = threadIdx.x;
+  const BsPair P = pairs[big[blockIdx.x]];
+  const uint32_t M = P.n1 + P.n2, W = bs_limbs(M);
+  uint32_t* S = sm;                  // pending sub-ranks
+  uint32_t* rk = sm + W + 64;
+  const BsWork bw = BsWork::carve(rk + W, W, W / 2 + 3);
+  const uint32_t* pool_in = pool;
+  const uint32_t* R0 = pool_in + P.rank_off;
+  BsWarpTask st[kBsStack];
+  int sp = 0;
+  uint64_t top = 0;
+  st[sp++] = BsWarpTask{M, P.n1, 0, R0[0], top};
+  wb::copy(S, R0 + 1, R0[0]);
+  top += R0[0];
+  while (sp) {
+    const BsWarpTask T = st[--sp];
+    uint32_t nr = T.rlen;
+    wb::copy(rk, S + T.rank, nr);
+    top = T.rank;
+    uint32_t m = T.m, k = T.k, off = T.off;
+    while (m > kBsTop) {
+      const uint32_t mL = m >> 1, mR = m - mL;
+      uint32_t t, nq, nrr;
+      bs_split<WarpOps>(m, k, rk, nr, bw, primes, nprimes, t, nq, nrr);
+      const uint32_t* q = bw.q;
+      const uint32_t* rr = bw.rr;
+      if (sp < kBsStack) st[sp++] = BsWarpTask{mL, t, off, nq, top};
+      wb::copy(S + top, q, nq);
+      top += nq;
+      wb::copy(rk, rr, nrr);
+      nr = nrr;
+      off += mL;
+      m = mR;
+      k -= t;
+    }
+    // a job for B2: its rank into the pool, its serial scratch
+    uint64_t j = 0, ro = 0, so = 0;
+    if (lane == 0) {
+      j = atomicAdd(&cnt->njobs, 1ull);
+      ro = atomicAdd(&cnt->pool_top, (unsigned long long)(nr + 1));
+      so = m > (uint32_t)kBsSmall ? atomicAdd(&cnt->scr_top, (unsigned long long)bs_scratch_limbs(m)) : 0ull;
+      if (ro + nr + 1 > pool_cap) __trap();  // (the pool is sized for every job's rank)
+      jobs[j] = BsJob{m, k, P.word_off + off, ro, scr_base + so};
+      pool[ro] = nr;
+    }
+    ro = __shfl_sync(wb::kFull, ro, 0);
+    wb::copy(pool + ro + 1, rk, nr);
+  }
+}
+
+// B2. one thread per job (pairs of <= kBsTop positions and B1's sub-problems)
+__global__ void bs_jobs_kernel(const BsJob* __restrict__ jobs, const BsCounters* __restrict__ cnt, const uint32_t* pool,
+                               uint32_t* scratch, const uint32_t* __restrict__ primes, uint32_t nprimes,
+                               uint8_t* __restrict__ words) {
   __shared__ uint64_t C[(kBsSmall + 1) * (kBsSmall + 1)];
   bs_small_table(C, threadIdx.x, blockDim.x);
   __syncthreads();
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < npairs) bs_word_pair(pairs[p], pool, scratch, primes, nprimes, words, C);
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cnt->njobs) return;
+  const BsJob J = jobs[j];
+  bs_word_task(J.m, J.k, pool + J.rank_off, words + J.word_off, scratch + J.scr_off, primes, nprimes, C);
 }
 
 // C. one level's interleaves (balanced.py:198-216): position t takes the next
@@ -66,6 +251,58 @@ __global__ void bs_interleave_kernel(const BsPair* __restrict__ pairs, uint32_t 
   for (uint32_t t = 0; t < m; ++t) x[t] = w[t] ? s[ib++] : s[ia++];
 }
 
+// The same for the levels of large pairs: a block per pair; position t takes
+// right[#ones before t] or left[#zeros before t], the ones counted by a block
+// scan over tiles of 8 positions per thread.
+constexpr int kBsIlBlock = 256;
+template <typename V>
+__global__ void __launch_bounds__(kBsIlBlock) bs_interleave_block_kernel(const BsPair* __restrict__ pairs,
+                                                                         uint32_t p0, V* a, V* tmp,
+                                                                         const uint8_t* __restrict__ words) {
+  __shared__ uint32_t wsum[kBsIlBlock / 32];
+  const BsPair P = pairs[p0 + blockIdx.x];
+  const uint32_t m = P.n1 + P.n2, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint8_t* w = words + P.word_off;
+  V* x = a + P.j;
+  V* s = tmp + P.j;
+  for (uint32_t t = tid; t < m; t += kBsIlBlock) s[t] = x[t];
+  __syncthreads();
+  uint32_t ones0 = 0;  // ones before the tile
+  for (uint32_t t0 = 0; t0 < m; t0 += 8 * kBsIlBlock) {
+    const uint32_t b = t0 + 8 * tid;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (b + e < m && w[b + e]) bits |= 1u << e;
+    const uint32_t c = __popc(bits);
+    uint32_t xs = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, xs, o);
+      if (lane >= (uint32_t)o) xs += y;
+    }
+    if (lane == 31) wsum[wid] = xs;
+    __syncthreads();
+    uint32_t before = ones0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < kBsIlBlock / 32; ++k) {
+      before += k < (int)wid ? wsum[k] : 0u;
+      tot += wsum[k];
+    }
+    before += xs - c;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t t = b + e;
+      if (t < m) {
+        const uint32_t ob = before + __popc(bits & ((1u << e) - 1));  // ones before t
+        x[t] = (bits >> e) & 1u ? s[P.n1 + ob] : s[t - ob];
+      }
+    }
+    ones0 += tot;
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------ host
 static std::vector<uint32_t> primes_upto(uint32_t n) {
   std::vector<uint8_t> comp(n + 1, 0);
@@ -79,11 +316,14 @@ static std::vector<uint32_t> primes_upto(uint32_t n) {
 }
 
 // The pairs of singleton_rounds(n) (shufflers.py:108-130) that draw, in
-// schedule order, with their pools laid out.
+// schedule order, with their pools laid out, and stage B's jobs.
 struct BsPlan {
   std::vector<BsPair> pairs;
   std::vector<uint32_t> level_start;  // pairs of level L: [level_start[L], level_start[L+1])
-  uint64_t rank_limbs = 0, scratch_limbs = 0, word_bytes = 0;
+  std::vector<BsJob> jobs;            // pairs of <= kBsTop positions
+  std::vector<uint32_t> big;          // pairs above kBsTop
+  uint64_t rank_limbs = 0, scratch_limbs = 0, word_bytes = 0, job_cap = 0, pool_cap = 0;
+  uint32_t max_big = 0;
 };
 
 static BsPlan bs_plan(uint64_t n) {
@@ -93,6 +333,7 @@ static BsPlan bs_plan(uint64_t n) {
   const uint64_t q = 1ull << c;
   auto bnd = [&](uint64_t i) { return (n * i) >> c; };
   uint32_t level = 0;
+  uint64_t emit = 0, emit_rank = 0;
   for (uint64_t p = 1; p < q; p += p, ++level) {
     pl.level_start.push_back((uint32_t)pl.pairs.size());
     for (uint64_t i = 0; i < q; i += 2 * p) {
@@ -107,13 +348,31 @@ static BsPlan bs_plan(uint64_t n) {
       P.rank_off = pl.rank_limbs;
       pl.rank_limbs += 1 + bs_limbs(m);
       P.word_off = (uint64_t)level * n + j;
-      P.scr_off = pl.scratch_limbs;
-      if (m > (uint32_t)kBsSmall) pl.scratch_limbs += bs_scratch_limbs(m);
+      P.scr_off = 0;
+      if (m > kBsTop) {
+        pl.big.push_back((uint32_t)pl.pairs.size());
+        pl.max_big = std::max(pl.max_big, m);
+        // its sub-problems have > kBsTop / 2 positions each
+        const uint64_t jobs = 2ull * m / kBsTop + 2;
+        emit += jobs;
+        emit_rank += m / 32 + 3 * jobs;
+      } else {
+        BsJob J;
+        J.m = m;
+        J.k = P.n1;
+        J.word_off = P.word_off;
+        J.rank_off = P.rank_off;
+        J.scr_off = pl.scratch_limbs;
+        if (m > (uint32_t)kBsSmall) pl.scratch_limbs += bs_scratch_limbs(m);
+        pl.jobs.push_back(J);
+      }
       pl.pairs.push_back(P);
     }
   }
   pl.level_start.push_back((uint32_t)pl.pairs.size());
   pl.word_bytes = (uint64_t)level * n;
+  pl.job_cap = pl.jobs.size() + emit;
+  pl.pool_cap = pl.rank_limbs + emit_rank + 16;
   return pl;
 }
 
@@ -123,44 +382,69 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
   if (n < 2) return;
   if (n > balanced_max_n()) throw std::invalid_argument("balanced_shuffle: n above the supported 2^17");
   BsPlan pl = bs_plan(n);
-  const uint32_t np = (uint32_t)pl.pairs.size();
+  const uint32_t np = (uint32_t)pl.pairs.size(), nbig = (uint32_t)pl.big.size();
   std::vector<uint32_t> primes = primes_upto((uint32_t)n);
   const uint32_t wl = bs_limbs((uint32_t)n) + 8;
+  const uint64_t emit_scr = (pl.job_cap - pl.jobs.size()) * bs_scratch_limbs(kBsTop);
+  BsCounters hc{(unsigned long long)pl.jobs.size(), (unsigned long long)pl.rank_limbs, 0ull};
   BsPair* d_pairs = nullptr;
-  uint32_t *d_primes = nullptr, *d_pool = nullptr, *d_work = nullptr, *d_scr = nullptr;
+  BsJob* d_jobs = nullptr;
+  BsCounters* d_cnt = nullptr;
+  uint32_t *d_primes = nullptr, *d_pool = nullptr, *d_scr = nullptr, *d_big = nullptr;
   uint8_t* d_words = nullptr;
   void* d_tmp = nullptr;
   auto cleanup = [&]() {
-    cudaFreeAsync(d_pairs, st);
-    cudaFreeAsync(d_primes, st);
-    cudaFreeAsync(d_pool, st);
-    cudaFreeAsync(d_work, st);
-    cudaFreeAsync(d_scr, st);
-    cudaFreeAsync(d_words, st);
-    cudaFreeAsync(d_tmp, st);
+    for (void* ptr : {(void*)d_pairs, (void*)d_jobs, (void*)d_cnt, (void*)d_primes, (void*)d_pool, (void*)d_scr,
+                      (void*)d_big, (void*)d_words, d_tmp})
+      if (ptr) cudaFreeAsync(ptr, st);
   };
   try {
     if (cudaMallocAsync((void**)&d_pairs, np * sizeof(BsPair), st) ||
+        cudaMallocAsync((void**)&d_jobs, std::max<uint64_t>(1, pl.job_cap) * sizeof(BsJob), st) ||
+        cudaMallocAsync((void**)&d_cnt, sizeof(BsCounters), st) ||
         cudaMallocAsync((void**)&d_primes, std::max<size_t>(1, primes.size()) * 4, st) ||
-        cudaMallocAsync((void**)&d_pool, (pl.rank_limbs + 1) * 4, st) ||
-        cudaMallocAsync((void**)&d_work, (size_t)4 * wl * 4, st) ||
-        cudaMallocAsync((void**)&d_scr, (pl.scratch_limbs + 1) * 4, st) ||
+        cudaMallocAsync((void**)&d_pool, (pl.pool_cap + 1) * 4, st) ||
+        cudaMallocAsync((void**)&d_scr, (pl.scratch_limbs + emit_scr + 1) * 4, st) ||
+        cudaMallocAsync((void**)&d_big, std::max<size_t>(1, nbig) * 4, st) ||
         cudaMallocAsync((void**)&d_words, pl.word_bytes + 1, st) || cudaMallocAsync(&d_tmp, n * eb, st))
       throw std::runtime_error("balanced_shuffle: device allocation failed");
     if (cudaMemcpyAsync(d_pairs, pl.pairs.data(), np * sizeof(BsPair), cudaMemcpyHostToDevice, st) ||
-        cudaMemcpyAsync(d_primes, primes.data(), primes.size() * 4, cudaMemcpyHostToDevice, st))
+        cudaMemcpyAsync(d_jobs, pl.jobs.data(), pl.jobs.size() * sizeof(BsJob), cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(d_cnt, &hc, sizeof(hc), cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(d_primes, primes.data(), primes.size() * 4, cudaMemcpyHostToDevice, st) ||
+        (nbig && cudaMemcpyAsync(d_big, pl.big.data(), nbig * 4, cudaMemcpyHostToDevice, st)))
       throw std::runtime_error("balanced_shuffle: upload failed");
     // the host vectors must outlive the (stream-ordered) copies
     if (cudaStreamSynchronize(st)) throw std::runtime_error("balanced_shuffle: upload failed");
-    bs_ranks_kernel<<<1, 1, 0, st>>>(d_pairs, np, sd, d_primes, (uint32_t)primes.size(), d_pool, d_work, wl,
-                                     d_bits);
+    const uint32_t npr = (uint32_t)primes.size();
+    const size_t smemA = (size_t)4 * wl * 4;
+    cudaFuncSetAttribute(bs_ranks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA);
+    bs_ranks_kernel<<<1, 32, smemA, st>>>(d_pairs, np, sd, d_primes, npr, d_pool, wl, d_bits);
     count_launch();
-    bs_words_kernel<<<(np + 63) / 64, 64, 0, st>>>(d_pairs, np, d_pool, d_scr, d_primes, (uint32_t)primes.size(),
-                                                   d_words);
+    if (nbig) {
+      const size_t smemB = bs_top_smem_limbs(pl.max_big) * 4;
+      cudaFuncSetAttribute(bs_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemB);
+      bs_top_kernel<<<nbig, 32, smemB, st>>>(d_pairs, d_big, d_primes, npr, d_jobs, d_pool, pl.pool_cap,
+                                             pl.scratch_limbs, d_cnt);
+      count_launch();
+    }
+    bs_jobs_kernel<<<(unsigned)((pl.job_cap + 63) / 64), 64, 0, st>>>(d_jobs, d_cnt, d_pool, d_scr, d_primes, npr,
+                                                                       d_words);
     count_launch();
     for (size_t L = 0; L + 1 < pl.level_start.size(); ++L) {
       const uint32_t p0 = pl.level_start[L], p1 = pl.level_start[L + 1];
       if (p1 == p0) continue;
+      const uint32_t mlev = pl.pairs[p0].n1 + pl.pairs[p0].n2;
+      if (mlev >= 1024) {  // the top levels: a block per pair
+        if (eb == 4)
+          bs_interleave_block_kernel<uint32_t><<<p1 - p0, kBsIlBlock, 0, st>>>(d_pairs, p0, (uint32_t*)data,
+                                                                               (uint32_t*)d_tmp, d_words);
+        else
+          bs_interleave_block_kernel<unsigned long long><<<p1 - p0, kBsIlBlock, 0, st>>>(
+              d_pairs, p0, (unsigned long long*)data, (unsigned long long*)d_tmp, d_words);
+        count_launch();
+        continue;
+      }
       const unsigned blocks = (p1 - p0 + 127) / 128;
       if (eb == 4)
         bs_interleave_kernel<uint32_t><<<blocks, 128, 0, st>>>(d_pairs, p0, p1, (uint32_t*)data, (uint32_t*)d_tmp,

@@ -348,38 +348,192 @@ struct BsTask {
 };
 constexpr int kBsStack = 64;
 
+// One split of _unrank_into (balanced.py:146-155): _locate_split
+// (balanced.py:98-143) of the rank rk (nr limbs) of a node of m positions
+// with k zeros, then divmod(rank - cum, right factor).  Leaves the left
+// half's zero count in t, its sub-rank in q (nq limbs) and the right half's in
+// rr (nrr limbs).  O: the serial (SerialOps) or warp-cooperative (WarpOps,
+// bs_warp.cuh) limb arithmetic; wk: working numbers of W limbs each.
+// Working numbers of one split (node of m positions): full-size ones hold up
+// to m + 1 bits, half-size ones up to m/2 + 1 bits (plus a limb of growth).
+struct BsWork {
+  uint32_t *wL, *wR, *wU, *wD, *rU, *rD, *cum, *tmp, *q, *rr, *un, *vn;
+  // carve from one region: W limbs per full-size number, H per half-size one
+  SK_HD static BsWork carve(uint32_t* p, uint32_t W, uint32_t H) {
+    BsWork w;
+    w.wU = p; p += W;
+    w.wD = p; p += W;
+    w.cum = p; p += W;
+    w.tmp = p; p += W;
+    w.un = p; p += W + 2;
+    w.wL = p; p += H;
+    w.wR = p; p += H;
+    w.rU = p; p += H;
+    w.rD = p; p += H;
+    w.q = p; p += H;
+    w.rr = p; p += H;
+    w.vn = p;
+    return w;
+  }
+  SK_HD static uint64_t limbs(uint32_t W, uint32_t H) { return 5ull * W + 2 + 7ull * H; }
+};
+
+// One split of _unrank_into (balanced.py:146-155): _locate_split
+// (balanced.py:98-143) of the rank rk (nr limbs) of a node of m positions
+// with k zeros, then divmod(rank - cum, right factor).  Leaves the left
+// half's zero count in t, its sub-rank in w.q (nq limbs) and the right half's
+// in w.rr (nrr limbs).  O: the serial (SerialOps) or warp-cooperative
+// (WarpOps, bs_warp.cuh) limb arithmetic.
+#pragma nv_exec_check_disable
+template <class O>
+SK_HD inline void bs_split(uint32_t m, uint32_t k, const uint32_t* rk, uint32_t nr, const BsWork& w,
+                           const uint32_t* primes, uint32_t nprimes, uint32_t& t, uint32_t& nq, uint32_t& nrr) {
+  uint32_t* wL = w.wL;    // C(mL, t0)
+  uint32_t* wR = w.wR;    // C(mR, k - t0)
+  uint32_t* wU = w.wU;    // weight of the upward block (first: of the block at t0)
+  uint32_t* wD = w.wD;    // weight of the downward block
+  uint32_t* rU = w.rU;    // right factor of the upward block
+  uint32_t* rD = w.rD;    // right factor of the downward block
+  uint32_t* cum = w.cum;
+  uint32_t* tmp = w.tmp;
+  uint32_t* q = w.q;
+  uint32_t* rr = w.rr;
+  uint32_t* un = w.un;
+  uint32_t* vn = w.vn;
+  const uint32_t mL = m >> 1, mR = m - mL;
+  // _locate_split(mL, mR, k, rank)
+  const uint32_t tmin = k > mR ? k - mR : 0u;
+  const uint32_t tmax = mL < k ? mL : k;
+  uint32_t t0 = (uint32_t)(((uint64_t)k * mL) / (mL + mR));
+  t0 = t0 < tmin ? tmin : (t0 > tmax ? tmax : t0);
+  uint32_t nL = O::binom(wL, mL, t0, primes, nprimes);
+  uint32_t nR = O::binom(wR, mR, k - t0, primes, nprimes);
+  uint32_t nU = O::mul(wU, wL, nL, wR, nR);
+  t = t0;
+  const uint32_t* rf = wR;  // right factor of the chosen block
+  uint32_t nrf = nR;
+  const uint32_t* base = nullptr;  // rank - cum of the chosen block
+  uint32_t nbase = 0;
+  if (O::cmp(rk, nr, wU, nU) < 0) {
+    base = rk;
+    nbase = nr;
+  } else {
+    uint32_t nc = nU;
+    O::copy(cum, wU, nU);
+    uint32_t nD = nU;
+    O::copy(wD, wU, nU);
+    uint32_t nRU = nR, nRD = nR;
+    O::copy(rU, wR, nR);
+    O::copy(rD, wR, nR);
+    uint32_t ut = t0, dt = t0;
+    for (;;) {
+      if (ut < tmax) {
+        const uint32_t j = k - ut;
+        // C(mL, ut+1) C(mR, j-1) = C(mL, ut) C(mR, j) (mL-ut)/(ut+1) j/(mR-j+1)
+        nU = O::mul_small(wU, nU, mL - ut);
+        nU = O::divexact_small(wU, nU, ut + 1);
+        nU = O::mul_small(wU, nU, j);
+        nU = O::divexact_small(wU, nU, mR - j + 1);
+        nRU = O::mul_small(rU, nRU, j);
+        nRU = O::divexact_small(rU, nRU, mR - j + 1);
+        ++ut;
+        const uint32_t nt = O::add(tmp, cum, nc, wU, nU);
+        if (O::cmp(rk, nr, tmp, nt) < 0) {
+          t = ut;
+          rf = rU;
+          nrf = nRU;
+          break;
+        }
+        O::copy(cum, tmp, nt);
+        nc = nt;
+      }
+      if (dt > tmin) {
+        const uint32_t j = k - dt;
+        // C(mL, dt-1) C(mR, j+1) = C(mL, dt) C(mR, j) dt/(mL-dt+1) (mR-j)/(j+1)
+        nD = O::mul_small(wD, nD, dt);
+        nD = O::divexact_small(wD, nD, mL - dt + 1);
+        nD = O::mul_small(wD, nD, mR - j);
+        nD = O::divexact_small(wD, nD, j + 1);
+        nRD = O::mul_small(rD, nRD, mR - j);
+        nRD = O::divexact_small(rD, nRD, j + 1);
+        --dt;
+        const uint32_t nt = O::add(tmp, cum, nc, wD, nD);
+        if (O::cmp(rk, nr, tmp, nt) < 0) {
+          t = dt;
+          rf = rD;
+          nrf = nRD;
+          break;
+        }
+        O::copy(cum, tmp, nt);
+        nc = nt;
+      }
+    }
+    nbase = O::sub(tmp, rk, nr, cum, nc);
+    base = tmp;
+  }
+  // (rank_left, rank_right) = divmod(rank - cum, right factor)
+  nq = 0;
+  nrr = 0;
+  if (O::cmp(base, nbase, rf, nrf) < 0) {
+    nq = 0;
+    O::copy(rr, base, nbase);
+    nrr = nbase;
+  } else if (nrf == 1) {
+    nrr = O::set1(rr, O::divmod_small(q, base, nbase, rf[0], nq));
+  } else {
+    O::divmod(q, nq, rr, nrr, base, nbase, rf, nrf, un, vn);
+  }
+}
+
+struct SerialOps {
+  SK_HD static uint32_t binom(uint32_t* r, uint32_t a, uint32_t b, const uint32_t* p, uint32_t np) {
+    return bn::binom(r, a, b, p, np);
+  }
+  SK_HD static uint32_t mul(uint32_t* r, const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+    return bn::mul(r, a, na, b, nb);
+  }
+  SK_HD static int cmp(const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) { return bn::cmp(a, na, b, nb); }
+  SK_HD static void copy(uint32_t* r, const uint32_t* a, uint32_t n) { bn::copy(r, a, n); }
+  SK_HD static uint32_t add(uint32_t* r, const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+    return bn::add(r, a, na, b, nb);
+  }
+  SK_HD static uint32_t sub(uint32_t* r, const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+    return bn::sub(r, a, na, b, nb);
+  }
+  SK_HD static uint32_t mul_small(uint32_t* a, uint32_t na, uint32_t m) { return bn::mul_small(a, na, m); }
+  SK_HD static uint32_t divexact_small(uint32_t* a, uint32_t na, uint32_t d) { return bn::divexact_small(a, na, d); }
+  SK_HD static uint32_t divmod_small(uint32_t* q, const uint32_t* a, uint32_t na, uint32_t d, uint32_t& nq) {
+    return bn::divmod_small(q, a, na, d, nq);
+  }
+  SK_HD static void divmod(uint32_t* q, uint32_t& nq, uint32_t* r, uint32_t& nr, const uint32_t* a, uint32_t na,
+                           const uint32_t* b, uint32_t nb, uint32_t* un, uint32_t* vn) {
+    bn::divmod(q, nq, r, nr, a, na, b, nb, un, vn);
+  }
+  SK_HD static uint32_t set1(uint32_t* r, uint32_t v) {
+    r[0] = v;
+    return v ? 1u : 0u;
+  }
+};
+
+// The word of M positions with K zeros and rank R0 ([limb count, limbs]) into
+// out, serially (one thread); S: 20 * bs_limbs(M) limbs of scratch when M > 32.
 // C: the 33 x 33 table of C(a, b) (0 for b > a).
-SK_HD inline void bs_word_pair(const BsPair& P, const uint32_t* pool, uint32_t* scratch, const uint32_t* primes,
-                               uint32_t nprimes, uint8_t* words, const uint64_t* C) {
-  const uint32_t M = P.n1 + P.n2;
-  const uint32_t* R0 = pool + P.rank_off;
-  uint8_t* out = words + P.word_off;
+SK_HD inline void bs_word_task(uint32_t M, uint32_t K, const uint32_t* R0, uint8_t* out, uint32_t* S,
+                               const uint32_t* primes, uint32_t nprimes, const uint64_t* C) {
   if (M <= (uint32_t)kBsSmall) {
     const uint64_t r = R0[0] == 0 ? 0ull : (R0[0] == 1 ? (uint64_t)R0[1] : ((uint64_t)R0[2] << 32 | R0[1]));
-    bs_unrank_small(M, P.n1, r, out, C);
+    bs_unrank_small(M, K, r, out, C);
     return;
   }
-  uint32_t* S = scratch + P.scr_off;
   const uint32_t W = bs_limbs(M);
   // arena: [0, 2W) pending sub-ranks (LIFO); [2W, ...) working numbers
   uint32_t* wk = S + 2 * W;
-  uint32_t* wL = wk;            // C(mL, t0)
-  uint32_t* wR = wk + W;        // C(mR, k - t0), then the chosen direction's right factor
-  uint32_t* wU = wk + 2 * W;    // weight of the upward block
-  uint32_t* wD = wk + 3 * W;    // weight of the downward block
-  uint32_t* rU = wk + 4 * W;    // right factor of the upward block
-  uint32_t* rD = wk + 5 * W;    // right factor of the downward block
-  uint32_t* cum = wk + 6 * W;
-  uint32_t* tmp = wk + 7 * W;
-  uint32_t* q = wk + 8 * W;
-  uint32_t* rr = wk + 9 * W;
-  uint32_t* un = wk + 10 * W;   // 2W limbs
-  uint32_t* vn = wk + 12 * W;
-  uint32_t* rk = wk + 13 * W;   // the current task's rank
+  uint32_t* rk = wk;            // the current task's rank
+  const BsWork bw = BsWork::carve(wk + W, W, W / 2 + 3);
   BsTask st[kBsStack];
   int sp = 0;
   uint64_t top = 0;  // arena top (limbs)
-  st[sp++] = BsTask{M, P.n1, 0, R0[0], top};
+  st[sp++] = BsTask{M, K, 0, R0[0], top};
   bn::copy(S, R0 + 1, R0[0]);
   top += R0[0];
   while (sp) {
@@ -390,88 +544,10 @@ SK_HD inline void bs_word_pair(const BsPair& P, const uint32_t* pool, uint32_t* 
     uint32_t m = T.m, k = T.k, off = T.off;
     while (m > (uint32_t)kBsSmall) {
       const uint32_t mL = m >> 1, mR = m - mL;
-      // _locate_split(mL, mR, k, rank)
-      const uint32_t tmin = k > mR ? k - mR : 0u;
-      const uint32_t tmax = mL < k ? mL : k;
-      uint32_t t0 = (uint32_t)(((uint64_t)k * mL) / (mL + mR));
-      t0 = t0 < tmin ? tmin : (t0 > tmax ? tmax : t0);
-      uint32_t nL = bn::binom(wL, mL, t0, primes, nprimes);
-      uint32_t nR = bn::binom(wR, mR, k - t0, primes, nprimes);
-      uint32_t nU = bn::mul(wU, wL, nL, wR, nR);
-      uint32_t t = t0;
-      const uint32_t* rf = wR;  // right factor of the chosen block
-      uint32_t nrf = nR;
-      const uint32_t* base = nullptr;  // rank - cum of the chosen block
-      uint32_t nbase = 0;
-      if (bn::cmp(rk, nr, wU, nU) < 0) {
-        base = rk;
-        nbase = nr;
-      } else {
-        uint32_t nc = nU;
-        bn::copy(cum, wU, nU);
-        uint32_t nD = nU;
-        bn::copy(wD, wU, nU);
-        uint32_t nRU = nR, nRD = nR;
-        bn::copy(rU, wR, nR);
-        bn::copy(rD, wR, nR);
-        uint32_t ut = t0, dt = t0;
-        for (;;) {
-          if (ut < tmax) {
-            const uint32_t j = k - ut;
-            // C(mL, ut+1) C(mR, j-1) = C(mL, ut) C(mR, j) (mL-ut)/(ut+1) j/(mR-j+1)
-            nU = bn::mul_small(wU, nU, mL - ut);
-            nU = bn::divexact_small(wU, nU, ut + 1);
-            nU = bn::mul_small(wU, nU, j);
-            nU = bn::divexact_small(wU, nU, mR - j + 1);
-            nRU = bn::mul_small(rU, nRU, j);
-            nRU = bn::divexact_small(rU, nRU, mR - j + 1);
-            ++ut;
-            const uint32_t nt = bn::add(tmp, cum, nc, wU, nU);
-            if (bn::cmp(rk, nr, tmp, nt) < 0) {
-              t = ut;
-              rf = rU;
-              nrf = nRU;
-              break;
-            }
-            bn::copy(cum, tmp, nt);
-            nc = nt;
-          }
-          if (dt > tmin) {
-            const uint32_t j = k - dt;
-            // C(mL, dt-1) C(mR, j+1) = C(mL, dt) C(mR, j) dt/(mL-dt+1) (mR-j)/(j+1)
-            nD = bn::mul_small(wD, nD, dt);
-            nD = bn::divexact_small(wD, nD, mL - dt + 1);
-            nD = bn::mul_small(wD, nD, mR - j);
-            nD = bn::divexact_small(wD, nD, j + 1);
-            nRD = bn::mul_small(rD, nRD, mR - j);
-            nRD = bn::divexact_small(rD, nRD, j + 1);
-            --dt;
-            const uint32_t nt = bn::add(tmp, cum, nc, wD, nD);
-            if (bn::cmp(rk, nr, tmp, nt) < 0) {
-              t = dt;
-              rf = rD;
-              nrf = nRD;
-              break;
-            }
-            bn::copy(cum, tmp, nt);
-            nc = nt;
-          }
-        }
-        nbase = bn::sub(tmp, rk, nr, cum, nc);
-        base = tmp;
-      }
-      // (rank_left, rank_right) = divmod(rank - cum, right factor)
-      uint32_t nq = 0, nrr = 0;
-      if (bn::cmp(base, nbase, rf, nrf) < 0) {
-        nq = 0;
-        bn::copy(rr, base, nbase);
-        nrr = nbase;
-      } else if (nrf == 1) {
-        rr[0] = bn::divmod_small(q, base, nbase, rf[0], nq);
-        nrr = rr[0] ? 1u : 0u;
-      } else {
-        bn::divmod(q, nq, rr, nrr, base, nbase, rf, nrf, un, vn);
-      }
+      uint32_t t, nq, nrr;
+      bs_split<SerialOps>(m, k, rk, nr, bw, primes, nprimes, t, nq, nrr);
+      const uint32_t* q = bw.q;
+      const uint32_t* rr = bw.rr;
       // the left half becomes a pending task (its sub-rank on the arena);
       // this loop continues with the right half (balanced.py:152-154)
       if (sp < kBsStack) st[sp++] = BsTask{mL, t, off, nq, top};  // (depth <= log2(m / 32) + 1)
@@ -488,6 +564,11 @@ SK_HD inline void bs_word_pair(const BsPair& P, const uint32_t* pool, uint32_t* 
   }
 }
 
+
+SK_HD inline void bs_word_pair(const BsPair& P, const uint32_t* pool, uint32_t* scratch, const uint32_t* primes,
+                               uint32_t nprimes, uint8_t* words, const uint64_t* C) {
+  bs_word_task(P.n1 + P.n2, P.n1, pool + P.rank_off, words + P.word_off, scratch + P.scr_off, primes, nprimes, C);
+}
 
 SK_HD inline void bs_small_table(uint64_t* C, uint32_t i0, uint32_t step) {
   for (uint32_t i = i0; i < (kBsSmall + 1) * (kBsSmall + 1); i += step) {

@@ -1,0 +1,409 @@
+// bs_warp.cuh -- warp-cooperative multi-limb naturals for the large pairs of
+// BalancedShuffle (balanced.cu).  Same number format and semantics as the
+// serial bn:: functions of bs_core.cuh (little-endian 32-bit limbs, tracked
+// lengths); every function is called by all 32 lanes of a warp with uniform
+// arguments and returns uniform results.  Lane l works on the contiguous chunk
+// [l*L, (l+1)*L) of the limbs (L = ceil(span / 32)); the carry (or borrow)
+// that leaves a chunk is then added (subtracted) at the next chunk's bottom by
+// lane 0, in lane order, rippling as far as it goes -- exact whatever the
+// order, since every fix-up is an exact addition.  A division by a small
+// number runs top-down, each chunk's incoming remainder from a suffix scan of
+// the chunks' affine remainder maps r -> (r * 2^(32 len) + value) mod d.
+#pragma once
+#include "bs_core.cuh"
+
+namespace sk {
+namespace wb {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+// chunk of this lane over [0, S)
+__device__ __forceinline__ void chunk_of(uint32_t S, uint32_t& lo, uint32_t& hi) {
+  const uint32_t L = (S + 31) >> 5;
+  lo = min(lane_id() * L, S);
+  hi = min(lo + L, S);
+}
+// x / d and x % d for d >= 2 by a reciprocal (minv = floor((2^64 - 1) / d))
+struct Div {
+  uint64_t d, minv;
+  __device__ __forceinline__ explicit Div(uint64_t dd) : d(dd), minv(~0ull / dd) {}
+  __device__ __forceinline__ uint64_t qr(uint64_t x, uint64_t& r) const {
+    uint64_t q = __umul64hi(x, minv);
+    r = x - q * d;
+    if (r >= d) { ++q; r -= d; }
+    return q;
+  }
+  __device__ __forceinline__ uint64_t mod(uint64_t x) const {
+    uint64_t r;
+    qr(x, r);
+    return r;
+  }
+};
+
+// Carry (borrow) hand-off between chunks: every lane passes what leaves its
+// chunk to the lane above, which adds (subtracts) it at its chunk's bottom
+// (at limb lo + skip in the first round); what leaves a chunk again goes up
+// in the next round -- rounds end when no lane has anything to pass, almost
+// always after the first.  Returns what escapes above lane 31.
+__device__ __forceinline__ uint64_t ripple_add(uint32_t* r, uint32_t lo, uint32_t hi, uint64_t cout,
+                                               uint32_t skip = 0) {
+  uint64_t esc = 0;
+  for (;;) {
+    uint64_t cin = __shfl_up_sync(kFull, cout, 1);
+    esc += __shfl_sync(kFull, cout, 31);
+    if (lane_id() == 0) cin = 0;
+    if (!__any_sync(kFull, cin != 0)) break;
+    uint64_t c = cin;
+    for (uint32_t i = lo + skip; i < hi && c; ++i) {
+      const uint64_t sm = (uint64_t)r[i] + (c & 0xffffffffull);
+      r[i] = (uint32_t)sm;
+      c = (c >> 32) + (sm >> 32);
+    }
+    skip = 0;
+    cout = c;
+  }
+  __syncwarp();
+  return esc;
+}
+__device__ __forceinline__ uint64_t ripple_sub(uint32_t* r, uint32_t lo, uint32_t hi, uint64_t bout) {
+  uint64_t esc = 0;
+  for (;;) {
+    uint64_t bin = __shfl_up_sync(kFull, bout, 1);
+    esc += __shfl_sync(kFull, bout, 31);
+    if (lane_id() == 0) bin = 0;
+    if (!__any_sync(kFull, bin != 0)) break;
+    uint64_t b = bin;
+    for (uint32_t i = lo; i < hi && b; ++i) {
+      const uint32_t x = r[i], lv = (uint32_t)b;
+      r[i] = x - lv;
+      b = (b >> 32) + (x < lv ? 1u : 0u);
+    }
+    bout = b;
+  }
+  __syncwarp();
+  return esc;
+}
+
+__device__ uint32_t trim(const uint32_t* a, uint32_t n) {
+  uint32_t lo, hi;
+  chunk_of(n, lo, hi);
+  uint32_t top = 0;
+  for (uint32_t i = hi; i > lo; --i)
+    if (a[i - 1]) { top = i; break; }
+  return __reduce_max_sync(kFull, top);
+}
+__device__ void copy(uint32_t* r, const uint32_t* a, uint32_t n) {
+  __syncwarp();
+  for (uint32_t i = lane_id(); i < n; i += 32) r[i] = a[i];
+  __syncwarp();
+}
+__device__ int cmp(const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+  if (na != nb) return na < nb ? -1 : 1;
+  uint32_t lo, hi;
+  chunk_of(na, lo, hi);
+  int s = 0;
+  for (uint32_t i = hi; i > lo; --i)
+    if (a[i - 1] != b[i - 1]) { s = a[i - 1] < b[i - 1] ? -1 : 1; break; }
+  const uint32_t m = __ballot_sync(kFull, s != 0);
+  return m ? __shfl_sync(kFull, s, 31 - __clz(m)) : 0;
+}
+__device__ uint32_t bitlen(const uint32_t* a, uint32_t n) { return n ? 32 * n - __clz(a[n - 1]) : 0; }
+// r = a + b (r may alias a or b)
+__device__ uint32_t add(uint32_t* r, const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+  const uint32_t S = max(na, nb) + 1;
+  uint32_t lo, hi;
+  chunk_of(S, lo, hi);
+  uint64_t c = 0;
+  for (uint32_t i = lo; i < hi; ++i) {
+    c += (uint64_t)(i < na ? a[i] : 0u) + (i < nb ? b[i] : 0u);
+    r[i] = (uint32_t)c;
+    c >>= 32;
+  }
+  ripple_add(r, lo, hi, c);
+  return trim(r, S);
+}
+// r = a - b, a >= b (r may alias a)
+__device__ uint32_t sub(uint32_t* r, const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+  uint32_t lo, hi;
+  chunk_of(na, lo, hi);
+  uint32_t br = 0;
+  for (uint32_t i = lo; i < hi; ++i) {
+    const uint64_t s = (uint64_t)(i < nb ? b[i] : 0u) + br;
+    const uint32_t ai = a[i];
+    r[i] = ai - (uint32_t)s;
+    br = (uint64_t)ai < s ? 1u : 0u;
+  }
+  ripple_sub(r, lo, hi, br);
+  return trim(r, na);
+}
+// a *= m (in place; a has room for one more limb)
+__device__ uint32_t mul_small(uint32_t* a, uint32_t na, uint32_t m) {
+  const uint32_t S = na + 1;
+  uint32_t lo, hi;
+  chunk_of(S, lo, hi);
+  uint64_t c = 0;
+  for (uint32_t i = lo; i < hi; ++i) {
+    c += (uint64_t)(i < na ? a[i] : 0u) * m;
+    a[i] = (uint32_t)c;
+    c >>= 32;
+  }
+  ripple_add(a, lo, hi, c);
+  return trim(a, S);
+}
+// q = a / d (q may alias a), returns the remainder; d >= 2
+__device__ uint32_t div_small(uint32_t* q, const uint32_t* a, uint32_t na, uint32_t d, uint32_t& nq) {
+  uint32_t lo, hi;
+  chunk_of(na, lo, hi);
+  const Div D(d);
+  // this chunk's value mod d and 2^(32 len) mod d
+  uint64_t V = 0, P = 1;
+  const uint64_t t32 = D.mod(1ull << 32);
+  for (uint32_t i = hi; i > lo; --i) {
+    V = D.mod((V << 32) | a[i - 1]);
+    P = D.mod(P * t32);
+  }
+  // suffix composition of the maps r -> r * P + V (the top lane's applies first):
+  // C_l = f_l o f_{l+1} o ... o f_31
+  uint64_t CP = P, CV = V;
+  for (uint32_t s = 1; s < 32; s <<= 1) {
+    const uint64_t P2 = __shfl_down_sync(kFull, CP, s), V2 = __shfl_down_sync(kFull, CV, s);
+    if (lane_id() + s < 32) {  // f_this o f_upper: r -> (r * P2 + V2) * CP + CV
+      CV = D.mod(D.mod(V2 * CP) + CV);
+      CP = D.mod(P2 * CP);
+    }
+  }
+  uint64_t r = __shfl_down_sync(kFull, CV, 1);  // remainder entering this chunk
+  if (lane_id() == 31) r = 0;
+  __syncwarp();
+  for (uint32_t i = hi; i > lo; --i) {
+    uint64_t rr;
+    q[i - 1] = (uint32_t)D.qr((r << 32) | a[i - 1], rr);
+    r = rr;
+  }
+  const uint32_t rem = (uint32_t)__shfl_sync(kFull, r, 0);
+  __syncwarp();
+  nq = trim(q, na);
+  return rem;
+}
+// a /= d, d divides a (in place)
+__device__ uint32_t divexact_small(uint32_t* a, uint32_t na, uint32_t d) {
+  if (d == 1) return na;
+  uint32_t nq;
+  div_small(a, a, na, d, nq);
+  return nq;
+}
+// r = a << k (r distinct from a; room for na + k/32 + 1 limbs)
+__device__ uint32_t shl(uint32_t* r, const uint32_t* a, uint32_t na, uint32_t k) {
+  if (!na) return 0;
+  const uint32_t w = k >> 5, s = k & 31, S = na + w + 1;
+  __syncwarp();
+  for (uint32_t i = lane_id(); i < S; i += 32) {
+    const int64_t src = (int64_t)i - w;
+    const uint32_t hi = (src >= 0 && src < (int64_t)na) ? a[src] : 0u;
+    const uint32_t lo = (s && src - 1 >= 0 && src - 1 < (int64_t)na) ? a[src - 1] : 0u;
+    r[i] = s ? (hi << s) | (lo >> (32 - s)) : hi;
+  }
+  __syncwarp();
+  return trim(r, S);
+}
+// (v << d) compared with b
+__device__ int cmp_shl(const uint32_t* v, uint32_t nv, uint32_t d, const uint32_t* b, uint32_t nb) {
+  const uint32_t lv = bitlen(v, nv) + d, lb = bitlen(b, nb);
+  if (lv != lb) return lv < lb ? -1 : 1;
+  const uint32_t w = d >> 5, s = d & 31;
+  uint32_t lo, hi;
+  chunk_of(nb, lo, hi);
+  int sg = 0;
+  for (uint32_t i = hi; i > lo; --i) {
+    const int64_t src = (int64_t)(i - 1) - w;
+    const uint32_t h = (src >= 0 && src < (int64_t)nv) ? v[src] : 0u;
+    const uint32_t l = (s && src - 1 >= 0 && src - 1 < (int64_t)nv) ? v[src - 1] : 0u;
+    const uint32_t x = s ? (h << s) | (l >> (32 - s)) : h;
+    if (x != b[i - 1]) { sg = x < b[i - 1] ? -1 : 1; break; }
+  }
+  const uint32_t m = __ballot_sync(kFull, sg != 0);
+  return m ? __shfl_sync(kFull, sg, 31 - __clz(m)) : 0;
+}
+// r = a * b (r distinct): lane l owns the output columns of its chunk (column
+// sums with a 96-bit running carry); the carries out of the chunks are then
+// added by lane 0
+__device__ uint32_t mul(uint32_t* r, const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+  if (!na || !nb) return 0;
+  const uint32_t S = na + nb;
+  if (S < 96) {  // short: one lane (the chunks would be shorter than a carry)
+    __syncwarp();
+    if (lane_id() == 0) bn::mul(r, a, na, b, nb);
+    __syncwarp();
+    return trim(r, S);
+  }
+  uint32_t lo, hi;
+  chunk_of(S, lo, hi);
+  uint64_t clo = 0;  // running carry, bits 0..63
+  uint32_t chi = 0;  // bits 64..95
+  for (uint32_t c = lo; c < hi; ++c) {
+    uint64_t slo = clo, shi = chi;
+    const uint32_t i0 = c + 1 > nb ? c + 1 - nb : 0u, i1 = min(c + 1, na);
+    for (uint32_t i = i0; i < i1; ++i) {
+      const uint64_t p = (uint64_t)a[i] * b[c - i];
+      slo += p;
+      shi += slo < p ? 1u : 0u;
+    }
+    r[c] = (uint32_t)slo;
+    clo = (slo >> 32) | (shi << 32);
+    chi = (uint32_t)(shi >> 32);
+  }
+  ripple_add(r, lo, hi, clo);
+  ripple_add(r, lo, hi, chi, 2);  // bits 64..95 of the carries: two limbs up
+  return trim(r, S);
+}
+// Schoolbook long division as bn::divmod (b has >= 2 limbs, a >= b), the
+// multiply-subtract of each quotient limb spread over the lanes.
+// un: na + 1 limbs of work, vn: nb limbs of work.  q, r distinct from a, b.
+__device__ void divmod(uint32_t* q, uint32_t& nq, uint32_t* r, uint32_t& nr, const uint32_t* a, uint32_t na,
+                       const uint32_t* b, uint32_t nb, uint32_t* un, uint32_t* vn) {
+  const uint32_t s = __clz(b[nb - 1]);
+  __syncwarp();
+  for (uint32_t i = lane_id(); i < nb; i += 32) vn[i] = s ? (b[i] << s) | (i ? b[i - 1] >> (32 - s) : 0u) : b[i];
+  for (uint32_t i = lane_id(); i <= na; i += 32) {
+    const uint32_t x = i < na ? a[i] : 0u;
+    un[i] = s ? (x << s) | (i ? a[i - 1] >> (32 - s) : 0u) : x;
+  }
+  __syncwarp();
+  const uint64_t vt = vn[nb - 1], vs = vn[nb - 2];
+  const Div DV(vt);
+  uint32_t lo, hi;
+  chunk_of(nb, lo, hi);
+  for (int64_t j = (int64_t)na - nb; j >= 0; --j) {
+    const uint64_t top = ((uint64_t)un[j + nb] << 32) | un[j + nb - 1];
+    uint64_t rh;
+    uint64_t qh = DV.qr(top, rh);
+    while (qh >> 32 || qh * vs > ((rh << 32) | un[j + nb - 2])) {
+      --qh;
+      rh += vt;
+      if (rh >> 32) break;
+    }
+    __syncwarp();
+    // un[j .. j+nb] -= qh * vn: each lane its chunk of vn, the carry of the
+    // product and the borrow leaving the chunk as one debt at its top
+    uint64_t pc = 0;
+    uint32_t br = 0;
+    for (uint32_t i = lo; i < hi; ++i) {
+      const uint64_t p = qh * vn[i] + pc;
+      pc = p >> 32;
+      const uint64_t sb = (uint64_t)(uint32_t)p + br;
+      const uint32_t u = un[i + j];
+      un[i + j] = u - (uint32_t)sb;
+      br = (uint64_t)u < sb ? 1u : 0u;
+    }
+    // the debt leaving the top chunk lands on limb j + nb (chunks cover [0, nb))
+    const uint64_t top_debt = ripple_sub(un + j, lo, hi, pc + br);
+    uint64_t neg = 0;
+    if (lane_id() == 0 && top_debt) {
+      const uint32_t u2 = un[j + nb];
+      un[j + nb] = u2 - (uint32_t)top_debt;
+      neg = ((uint64_t)u2 < top_debt) ? 1u : 0u;
+    }
+    neg = __shfl_sync(kFull, neg, 0);
+    __syncwarp();
+    if (neg) {  // qh was one too large: add vn back (the top wraps to the right value)
+      --qh;
+      uint64_t c = 0;
+      for (uint32_t i = lo; i < hi; ++i) {
+        c += (uint64_t)un[i + j] + vn[i];
+        un[i + j] = (uint32_t)c;
+        c >>= 32;
+      }
+      const uint64_t top_c = ripple_add(un + j, lo, hi, c);
+      if (lane_id() == 0) un[j + nb] += (uint32_t)top_c;
+      __syncwarp();
+    }
+    if (lane_id() == 0) q[j] = (uint32_t)qh;
+  }
+  __syncwarp();
+  nq = trim(q, na - nb + 1);
+  for (uint32_t i = lane_id(); i < nb; i += 32) r[i] = s ? (un[i] >> s) | (un[i + 1] << (32 - s)) : un[i];
+  __syncwarp();
+  nr = trim(r, nb);
+}
+// r = C(a, b) as the product of its prime powers (bn::binom): the factors of
+// 32 primes at a time (one per lane), multiplied in as packed limbs
+__device__ uint32_t binom(uint32_t* r, uint32_t a, uint32_t b, const uint32_t* primes, uint32_t np) {
+  __syncwarp();
+  if (lane_id() == 0) r[0] = 1;
+  __syncwarp();
+  uint32_t n = 1;
+  if (b > a) {
+    if (lane_id() == 0) r[0] = 0;
+    __syncwarp();
+    return 0;
+  }
+  if (b > a - b) b = a - b;
+  if (b == 0) return 1;
+  uint64_t acc = 1;
+  for (uint32_t base = 0; base < np && primes[base] <= a; base += 32) {
+    const uint32_t i = base + lane_id();
+    uint64_t f = 1;
+    if (i < np && primes[i] <= a) {
+      const uint32_t p = primes[i];
+      for (uint64_t pk = p; pk <= a; pk *= p)
+        if (a / pk - b / pk - (a - b) / pk) f *= p;
+    }
+    uint32_t m = __ballot_sync(kFull, f != 1);
+    while (m) {
+      const int l = __ffs(m) - 1;
+      m &= m - 1;
+      const uint64_t fl = __shfl_sync(kFull, f, l);
+      if ((acc * fl) >> 32) {
+        n = mul_small(r, n, (uint32_t)acc);
+        acc = fl;
+      } else {
+        acc *= fl;
+      }
+    }
+  }
+  if (acc > 1) n = mul_small(r, n, (uint32_t)acc);
+  return n;
+}
+
+}  // namespace wb
+}  // namespace sk
+
+namespace sk {
+// bs_split's arithmetic on the whole warp
+struct WarpOps {
+  __device__ static uint32_t binom(uint32_t* r, uint32_t a, uint32_t b, const uint32_t* p, uint32_t np) {
+    return wb::binom(r, a, b, p, np);
+  }
+  __device__ static uint32_t mul(uint32_t* r, const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+    return wb::mul(r, a, na, b, nb);
+  }
+  __device__ static int cmp(const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+    return wb::cmp(a, na, b, nb);
+  }
+  __device__ static void copy(uint32_t* r, const uint32_t* a, uint32_t n) { wb::copy(r, a, n); }
+  __device__ static uint32_t add(uint32_t* r, const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+    return wb::add(r, a, na, b, nb);
+  }
+  __device__ static uint32_t sub(uint32_t* r, const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+    return wb::sub(r, a, na, b, nb);
+  }
+  __device__ static uint32_t mul_small(uint32_t* a, uint32_t na, uint32_t m) { return wb::mul_small(a, na, m); }
+  __device__ static uint32_t divexact_small(uint32_t* a, uint32_t na, uint32_t d) {
+    return wb::divexact_small(a, na, d);
+  }
+  __device__ static uint32_t divmod_small(uint32_t* q, const uint32_t* a, uint32_t na, uint32_t d, uint32_t& nq) {
+    return wb::div_small(q, a, na, d, nq);
+  }
+  __device__ static void divmod(uint32_t* q, uint32_t& nq, uint32_t* r, uint32_t& nr, const uint32_t* a,
+                                uint32_t na, const uint32_t* b, uint32_t nb, uint32_t* un, uint32_t* vn) {
+    wb::divmod(q, nq, r, nr, a, na, b, nb, un, vn);
+  }
+  __device__ static uint32_t set1(uint32_t* r, uint32_t v) {
+    __syncwarp();
+    if (wb::lane_id() == 0) r[0] = v;
+    __syncwarp();
+    return v ? 1u : 0u;
+  }
+};
+}  // namespace sk
