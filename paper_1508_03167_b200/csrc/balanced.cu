@@ -51,21 +51,24 @@ struct BsCounters {
   unsigned long long njobs, pool_top, scr_top;
 };
 
-// bits [o, o + k) of the stream, k <= 64
-__device__ __forceinline__ uint64_t bs_bits64(const StreamDesc& sd, uint64_t o, uint32_t k) {
-  const uint64_t w = o >> 6;
-  const uint32_t s = (uint32_t)(o & 63);
-  uint64_t x = bs_word(sd, w);
-  if (s) x = (x << s) | (bs_word(sd, w + 1) >> (64 - s));
-  return k == 64 ? x : (x >> (64 - k));
+// The class sizes C(m, n1) of the pairs above kBsWord positions, one warp
+// each (data independent: computed before the sequential rolls need them);
+// entry b at table + boff[b] as [limb count, limbs].
+__global__ void __launch_bounds__(32) bs_binoms_kernel(const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bk,
+                                                       const uint64_t* __restrict__ boff, uint32_t* table,
+                                                       const uint32_t* __restrict__ primes, uint32_t nprimes) {
+  extern __shared__ uint32_t num[];
+  const uint32_t n = wb::binom(num, bm[blockIdx.x], bk[blockIdx.x], primes, nprimes);
+  uint32_t* T = table + boff[blockIdx.x];
+  if (threadIdx.x == 0) T[0] = n;
+  wb::copy(T + 1, num, n);
 }
 
 // A. (one warp)
 constexpr uint32_t kBsWord = 64;  // C(m, n1) < 2^62 for m <= 64
 __global__ void __launch_bounds__(32) bs_ranks_kernel(const BsPair* __restrict__ pairs, uint32_t npairs,
-                                                      StreamDesc sd, const uint32_t* __restrict__ primes,
-                                                      uint32_t nprimes, uint32_t* pool, uint32_t wl,
-                                                      unsigned long long* bits) {
+                                                      StreamDesc sd, const uint32_t* __restrict__ btab,
+                                                      uint32_t* pool, uint32_t wl, unsigned long long* bits) {
   __shared__ uint64_t Cw[(kBsWord + 1) * (kBsWord + 1)];  // C(a, b), a, b <= 64 (Pascal)
   extern __shared__ uint32_t work[];                     // B, v, c and a spare: wl limbs each
   const uint32_t lane = threadIdx.x;
@@ -79,21 +82,25 @@ __global__ void __launch_bounds__(32) bs_ranks_kernel(const BsPair* __restrict__
   uint32_t* v = work + wl;
   uint32_t* c = work + 2 * wl;
   uint32_t* t = work + 3 * wl;
-  uint32_t nB = 0, cm = 0, cn1 = 0;
+  uint32_t nB = 0, cb = ~0u;
   uint64_t o = 0;  // stream offset (uniform)
-  uint32_t bn1 = 0, bn2 = 0;
+  uint32_t bn1 = 0, bn2 = 0, bbi = 0;
   uint64_t broff = 0;
+  // lane 0's cache of the stream words w0 and w0 + 1 (the machine-word rolls)
+  uint64_t cw = ~1ull, cw0 = 0, cw1 = 0;  // (no word cached: cw + 1 != 0)
   for (uint32_t p = 0; p < npairs; ++p) {
     if ((p & 31) == 0 && p + lane < npairs) {  // the next 32 pairs' sizes, one per lane (coalesced)
       const BsPair Q = pairs[p + lane];
       bn1 = Q.n1;
       bn2 = Q.n2;
       broff = Q.rank_off;
+      bbi = Q.bidx;
     }
     BsPair P;
     P.n1 = __shfl_sync(wb::kFull, bn1, p & 31);
     P.n2 = __shfl_sync(wb::kFull, bn2, p & 31);
     P.rank_off = __shfl_sync(wb::kFull, broff, p & 31);
+    P.bidx = __shfl_sync(wb::kFull, bbi, p & 31);
     const uint32_t m = P.n1 + P.n2;
     uint32_t* R = pool + P.rank_off;
     if (m <= kBsWord) {  // bitstream.py:187-210 in machine words (one lane)
@@ -104,7 +111,24 @@ __global__ void __launch_bounds__(32) bs_ranks_kernel(const BsPair* __restrict__
         for (;;) {
           uint32_t k = lb - (64 - __clzll(vv));  // smallest k with vv << k >= bound
           if ((vv << k) < bound) ++k;
-          cc = (cc << k) | (k ? bs_bits64(sd, o, k) : 0ull);
+          if (k) {  // the next k bits from the cached words
+            const uint64_t w = o >> 6;
+            if (w != cw) {
+              if (w == cw + 1) {
+                cw0 = cw1;
+                cw1 = bs_word(sd, w + 1);
+              } else {
+                cw0 = bs_word(sd, w);
+                cw1 = bs_word(sd, w + 1);
+              }
+              cw = w;
+            }
+            const uint32_t sh = (uint32_t)(o & 63);
+            const uint64_t x = sh ? (cw0 << sh) | (cw1 >> (64 - sh)) : cw0;
+            cc = (cc << k) | (x >> (64 - k));
+          } else {
+            cc <<= k;
+          }
           o += k;
           vv <<= k;
           if (cc < bound) break;
@@ -118,10 +142,11 @@ __global__ void __launch_bounds__(32) bs_ranks_kernel(const BsPair* __restrict__
       o = __shfl_sync(wb::kFull, o, 0);
       continue;
     }
-    if (m != cm || P.n1 != cn1) {  // pairs of a level repeat a handful of sizes
-      nB = wb::binom(B, m, P.n1, primes, nprimes);
-      cm = m;
-      cn1 = P.n1;
+    if (P.bidx != cb) {  // pairs of a level repeat a handful of sizes
+      const uint32_t* T = btab + P.bidx;
+      nB = T[0];
+      wb::copy(B, T + 1, nB);
+      cb = P.bidx;
     }
     // fast dice roller below B (>= 2): v = 1, c = 0
     if (lane == 0) v[0] = 1;
@@ -322,6 +347,9 @@ struct BsPlan {
   std::vector<uint32_t> level_start;  // pairs of level L: [level_start[L], level_start[L+1])
   std::vector<BsJob> jobs;            // pairs of <= kBsTop positions
   std::vector<uint32_t> big;          // pairs above kBsTop
+  std::vector<uint32_t> bm, bk;       // distinct class sizes C(bm, bk) of pairs above kBsWord
+  std::vector<uint64_t> boff;         // their table offsets
+  uint64_t btab_limbs = 0;
   uint64_t rank_limbs = 0, scratch_limbs = 0, word_bytes = 0, job_cap = 0, pool_cap = 0;
   uint32_t max_big = 0;
 };
@@ -345,6 +373,18 @@ static BsPlan bs_plan(uint64_t n) {
       P.n2 = (uint32_t)(l - k);
       P.level = level;
       const uint32_t m = P.n1 + P.n2;
+      P.bidx = 0;
+      if (m > kBsWord) {
+        size_t b = 0;
+        while (b < pl.bm.size() && !(pl.bm[b] == m && pl.bk[b] == P.n1)) ++b;
+        if (b == pl.bm.size()) {
+          pl.bm.push_back(m);
+          pl.bk.push_back(P.n1);
+          pl.boff.push_back(pl.btab_limbs);
+          pl.btab_limbs += 1 + bs_limbs(m);
+        }
+        P.bidx = (uint32_t)pl.boff[b];
+      }
       P.rank_off = pl.rank_limbs;
       pl.rank_limbs += 1 + bs_limbs(m);
       P.word_off = (uint64_t)level * n + j;
@@ -390,12 +430,14 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
   BsPair* d_pairs = nullptr;
   BsJob* d_jobs = nullptr;
   BsCounters* d_cnt = nullptr;
-  uint32_t *d_primes = nullptr, *d_pool = nullptr, *d_scr = nullptr, *d_big = nullptr;
+  uint32_t *d_primes = nullptr, *d_pool = nullptr, *d_scr = nullptr, *d_big = nullptr, *d_bm = nullptr,
+           *d_bk = nullptr, *d_btab = nullptr;
+  uint64_t* d_boff = nullptr;
   uint8_t* d_words = nullptr;
   void* d_tmp = nullptr;
   auto cleanup = [&]() {
     for (void* ptr : {(void*)d_pairs, (void*)d_jobs, (void*)d_cnt, (void*)d_primes, (void*)d_pool, (void*)d_scr,
-                      (void*)d_big, (void*)d_words, d_tmp})
+                      (void*)d_big, (void*)d_words, d_tmp, (void*)d_bm, (void*)d_bk, (void*)d_boff, (void*)d_btab})
       if (ptr) cudaFreeAsync(ptr, st);
   };
   try {
@@ -406,20 +448,34 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
         cudaMallocAsync((void**)&d_pool, (pl.pool_cap + 1) * 4, st) ||
         cudaMallocAsync((void**)&d_scr, (pl.scratch_limbs + emit_scr + 1) * 4, st) ||
         cudaMallocAsync((void**)&d_big, std::max<size_t>(1, nbig) * 4, st) ||
+        cudaMallocAsync((void**)&d_bm, std::max<size_t>(1, pl.bm.size()) * 4, st) ||
+        cudaMallocAsync((void**)&d_bk, std::max<size_t>(1, pl.bm.size()) * 4, st) ||
+        cudaMallocAsync((void**)&d_boff, std::max<size_t>(1, pl.bm.size()) * 8, st) ||
+        cudaMallocAsync((void**)&d_btab, (pl.btab_limbs + 1) * 4, st) ||
         cudaMallocAsync((void**)&d_words, pl.word_bytes + 1, st) || cudaMallocAsync(&d_tmp, n * eb, st))
       throw std::runtime_error("balanced_shuffle: device allocation failed");
     if (cudaMemcpyAsync(d_pairs, pl.pairs.data(), np * sizeof(BsPair), cudaMemcpyHostToDevice, st) ||
         cudaMemcpyAsync(d_jobs, pl.jobs.data(), pl.jobs.size() * sizeof(BsJob), cudaMemcpyHostToDevice, st) ||
         cudaMemcpyAsync(d_cnt, &hc, sizeof(hc), cudaMemcpyHostToDevice, st) ||
         cudaMemcpyAsync(d_primes, primes.data(), primes.size() * 4, cudaMemcpyHostToDevice, st) ||
-        (nbig && cudaMemcpyAsync(d_big, pl.big.data(), nbig * 4, cudaMemcpyHostToDevice, st)))
+        (nbig && cudaMemcpyAsync(d_big, pl.big.data(), nbig * 4, cudaMemcpyHostToDevice, st)) ||
+        (!pl.bm.empty() && (cudaMemcpyAsync(d_bm, pl.bm.data(), pl.bm.size() * 4, cudaMemcpyHostToDevice, st) ||
+                            cudaMemcpyAsync(d_bk, pl.bk.data(), pl.bk.size() * 4, cudaMemcpyHostToDevice, st) ||
+                            cudaMemcpyAsync(d_boff, pl.boff.data(), pl.boff.size() * 8, cudaMemcpyHostToDevice, st))))
       throw std::runtime_error("balanced_shuffle: upload failed");
     // the host vectors must outlive the (stream-ordered) copies
     if (cudaStreamSynchronize(st)) throw std::runtime_error("balanced_shuffle: upload failed");
     const uint32_t npr = (uint32_t)primes.size();
+    const uint32_t nbin = (uint32_t)pl.bm.size();
+    if (nbin) {
+      const size_t smemT = (size_t)(bs_limbs((uint32_t)n) + 2) * 4;
+      cudaFuncSetAttribute(bs_binoms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemT);
+      bs_binoms_kernel<<<nbin, 32, smemT, st>>>(d_bm, d_bk, d_boff, d_btab, d_primes, npr);
+      count_launch();
+    }
     const size_t smemA = (size_t)4 * wl * 4;
     cudaFuncSetAttribute(bs_ranks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA);
-    bs_ranks_kernel<<<1, 32, smemA, st>>>(d_pairs, np, sd, d_primes, npr, d_pool, wl, d_bits);
+    bs_ranks_kernel<<<1, 32, smemA, st>>>(d_pairs, np, sd, d_btab, d_pool, wl, d_bits);
     count_launch();
     if (nbig) {
       const size_t smemB = bs_top_smem_limbs(pl.max_big) * 4;

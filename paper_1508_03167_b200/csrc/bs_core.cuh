@@ -244,6 +244,7 @@ constexpr int kBsSmall = 32;  // balanced.py:40 _SMALL_N
 // One pair of the singleton schedule that draws (both sides non-empty).
 struct BsPair {
   uint32_t j, n1, n2, level;
+  uint32_t bidx;       // its class size in the binomial table (m > 64)
   uint64_t rank_off;   // limbs into the rank pool
   uint64_t word_off;   // bytes into the word buffer (level * n + j)
   uint64_t scr_off;    // limbs into the unrank scratch pool (m > 32)
@@ -354,6 +355,27 @@ constexpr int kBsStack = 64;
 // half's zero count in t, its sub-rank in q (nq limbs) and the right half's in
 // rr (nrr limbs).  O: the serial (SerialOps) or warp-cooperative (WarpOps,
 // bs_warp.cuh) limb arithmetic; wk: working numbers of W limbs each.
+// a = a * x * y / (u * v), exact: one limb pass per side when the products
+// fit a limb
+#pragma nv_exec_check_disable
+template <class O>
+SK_HD inline uint32_t bs_muldiv(uint32_t* a, uint32_t na, uint32_t x, uint32_t y, uint32_t u, uint32_t v) {
+  const uint64_t xy = (uint64_t)x * y, uv = (uint64_t)u * v;
+  if (xy >> 32) {
+    na = O::mul_small(a, na, x);
+    na = O::mul_small(a, na, y);
+  } else {
+    na = O::mul_small(a, na, (uint32_t)xy);
+  }
+  if (uv >> 32) {
+    na = O::divexact_small(a, na, u);
+    na = O::divexact_small(a, na, v);
+  } else {
+    na = O::divexact_small(a, na, (uint32_t)uv);
+  }
+  return na;
+}
+
 // Working numbers of one split (node of m positions): full-size ones hold up
 // to m + 1 bits, half-size ones up to m/2 + 1 bits (plus a limb of growth).
 struct BsWork {
@@ -430,10 +452,7 @@ SK_HD inline void bs_split(uint32_t m, uint32_t k, const uint32_t* rk, uint32_t 
       if (ut < tmax) {
         const uint32_t j = k - ut;
         // C(mL, ut+1) C(mR, j-1) = C(mL, ut) C(mR, j) (mL-ut)/(ut+1) j/(mR-j+1)
-        nU = O::mul_small(wU, nU, mL - ut);
-        nU = O::divexact_small(wU, nU, ut + 1);
-        nU = O::mul_small(wU, nU, j);
-        nU = O::divexact_small(wU, nU, mR - j + 1);
+        nU = bs_muldiv<O>(wU, nU, mL - ut, j, ut + 1, mR - j + 1);
         nRU = O::mul_small(rU, nRU, j);
         nRU = O::divexact_small(rU, nRU, mR - j + 1);
         ++ut;
@@ -444,16 +463,13 @@ SK_HD inline void bs_split(uint32_t m, uint32_t k, const uint32_t* rk, uint32_t 
           nrf = nRU;
           break;
         }
-        O::copy(cum, tmp, nt);
+        { uint32_t* x = cum; cum = tmp; tmp = x; }  // cum += weight
         nc = nt;
       }
       if (dt > tmin) {
         const uint32_t j = k - dt;
         // C(mL, dt-1) C(mR, j+1) = C(mL, dt) C(mR, j) dt/(mL-dt+1) (mR-j)/(j+1)
-        nD = O::mul_small(wD, nD, dt);
-        nD = O::divexact_small(wD, nD, mL - dt + 1);
-        nD = O::mul_small(wD, nD, mR - j);
-        nD = O::divexact_small(wD, nD, j + 1);
+        nD = bs_muldiv<O>(wD, nD, dt, mR - j, mL - dt + 1, j + 1);
         nRD = O::mul_small(rD, nRD, mR - j);
         nRD = O::divexact_small(rD, nRD, j + 1);
         --dt;
@@ -464,7 +480,7 @@ SK_HD inline void bs_split(uint32_t m, uint32_t k, const uint32_t* rk, uint32_t 
           nrf = nRD;
           break;
         }
-        O::copy(cum, tmp, nt);
+        { uint32_t* x = cum; cum = tmp; tmp = x; }
         nc = nt;
       }
     }
