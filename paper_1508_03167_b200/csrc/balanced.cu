@@ -28,6 +28,7 @@
 // the remaining division (the sub-ranks) is schoolbook long division.
 #include <algorithm>
 #include <stdexcept>
+#include <string>
 #include <vector>
 #include "sk_kernels.h"
 #include "bs_core.cuh"
@@ -49,6 +50,7 @@ struct BsJob {
 // device-side bump counters of stage B
 struct BsCounters {
   unsigned long long njobs, pool_top, scr_top;
+  unsigned long long nnodes[16];  // B1 nodes per recursion depth
 };
 
 // The class sizes C(m, n1) of the pairs above kBsWord positions, one warp
@@ -180,70 +182,63 @@ __global__ void __launch_bounds__(32) bs_ranks_kernel(const BsPair* __restrict__
   if (lane == 0) bits[0] = o;
 }
 
-// B1. the splits above kBsTop of the pairs above kBsTop: one warp (and one
-// block) per pair, its numbers in shared memory: the pending sub-ranks
-// (W + 64 limbs), the current rank (W) and bs_split's working numbers.
-struct BsWarpTask {
-  uint32_t m, k, off, rlen;
-  uint64_t rank;
+// B1. the splits above kBsTop, one recursion depth per launch and one warp
+// (and block) per node: a node of more than kBsTop positions loads its rank
+// into shared memory, splits (bs_split on WarpOps), and hands its halves on --
+// as nodes of the next depth when they are still above kBsTop, as B2 jobs
+// otherwise; their sub-ranks go to the pool.  The halves of a node are
+// independent, so the nodes of one depth run side by side.
+struct BsNode {
+  uint32_t m, k;
+  uint64_t word_off, rank_off;
 };
-__host__ __device__ inline uint64_t bs_top_smem_limbs(uint32_t M) {
-  const uint32_t W = bs_limbs(M), H = W / 2 + 3;
-  return (uint64_t)W + 64 + W + BsWork::limbs(W, H);
+constexpr int kBsMaxDepth = 16;
+
+__host__ __device__ inline uint64_t bs_split_smem_limbs(uint32_t m) {
+  const uint32_t W = bs_limbs(m), H = W / 2 + 3;
+  return (uint64_t)W + BsWork::limbs(W, H);
 }
-__global__ void __launch_bounds__(32) bs_top_kernel(const BsPair* __restrict__ pairs, const uint32_t* __restrict__ big,
-                                                    const uint32_t* __restrict__ primes, uint32_t nprimes, BsJob* jobs,
-                                                    uint32_t* pool, uint64_t pool_cap, uint64_t scr_base,
-                                                    BsCounters* cnt) {
-  extern __shared__ uint32_t sm[];
-  const uint32_t lane = threadIdx.x;
-  const BsPair P = pairs[big[blockIdx.x]];
-  const uint32_t M = P.n1 + P.n2, W = bs_limbs(M);
-  uint32_t* S = sm;                  // pending sub-ranks
-  uint32_t* rk = sm + W + 64;
-  const BsWork bw = BsWork::carve(rk + W, W, W / 2 + 3);
-  const uint32_t* pool_in = pool;
-  const uint32_t* R0 = pool_in + P.rank_off;
-  BsWarpTask st[kBsStack];
-  int sp = 0;
-  uint64_t top = 0;
-  st[sp++] = BsWarpTask{M, P.n1, 0, R0[0], top};
-  wb::copy(S, R0 + 1, R0[0]);
-  top += R0[0];
-  while (sp) {
-    const BsWarpTask T = st[--sp];
-    uint32_t nr = T.rlen;
-    wb::copy(rk, S + T.rank, nr);
-    top = T.rank;
-    uint32_t m = T.m, k = T.k, off = T.off;
-    while (m > kBsTop) {
-      const uint32_t mL = m >> 1, mR = m - mL;
-      uint32_t t, nq, nrr;
-      bs_split<WarpOps>(m, k, rk, nr, bw, primes, nprimes, t, nq, nrr);
-      const uint32_t* q = bw.q;
-      const uint32_t* rr = bw.rr;
-      if (sp < kBsStack) st[sp++] = BsWarpTask{mL, t, off, nq, top};
-      wb::copy(S + top, q, nq);
-      top += nq;
-      wb::copy(rk, rr, nrr);
-      nr = nrr;
-      off += mL;
-      m = mR;
-      k -= t;
+
+__device__ void bs_emit(uint32_t m, uint32_t k, uint64_t word_off, const uint32_t* rank, uint32_t nr, BsNode* next,
+                        unsigned long long* nnext, BsJob* jobs, uint32_t* pool, uint64_t pool_cap,
+                        uint64_t scr_base, BsCounters* cnt) {
+  uint64_t ro = 0;
+  if (threadIdx.x == 0) {
+    ro = atomicAdd(&cnt->pool_top, (unsigned long long)(nr + 1));
+    if (ro + nr + 1 > pool_cap) __trap();  // (the pool is sized for every sub-rank)
+    pool[ro] = nr;
+    if (m > kBsTop) {
+      next[atomicAdd(nnext, 1ull)] = BsNode{m, k, word_off, ro};
+    } else {
+      const uint64_t j = atomicAdd(&cnt->njobs, 1ull);
+      const uint64_t so =
+          m > (uint32_t)kBsSmall ? atomicAdd(&cnt->scr_top, (unsigned long long)bs_scratch_limbs(m)) : 0ull;
+      jobs[j] = BsJob{m, k, word_off, ro, scr_base + so};
     }
-    // a job for B2: its rank into the pool, its serial scratch
-    uint64_t j = 0, ro = 0, so = 0;
-    if (lane == 0) {
-      j = atomicAdd(&cnt->njobs, 1ull);
-      ro = atomicAdd(&cnt->pool_top, (unsigned long long)(nr + 1));
-      so = m > (uint32_t)kBsSmall ? atomicAdd(&cnt->scr_top, (unsigned long long)bs_scratch_limbs(m)) : 0ull;
-      if (ro + nr + 1 > pool_cap) __trap();  // (the pool is sized for every job's rank)
-      jobs[j] = BsJob{m, k, P.word_off + off, ro, scr_base + so};
-      pool[ro] = nr;
-    }
-    ro = __shfl_sync(wb::kFull, ro, 0);
-    wb::copy(pool + ro + 1, rk, nr);
   }
+  ro = __shfl_sync(wb::kFull, ro, 0);
+  wb::copy(pool + ro + 1, rank, nr);
+}
+
+__global__ void __launch_bounds__(32) bs_split_kernel(const BsNode* __restrict__ nodes,
+                                                      const unsigned long long* __restrict__ nnodes, BsNode* next,
+                                                      unsigned long long* nnext, const uint32_t* __restrict__ primes,
+                                                      uint32_t nprimes, BsJob* jobs, uint32_t* pool,
+                                                      uint64_t pool_cap, uint64_t scr_base, BsCounters* cnt) {
+  if (blockIdx.x >= *nnodes) return;
+  extern __shared__ uint32_t sm[];
+  const BsNode N = nodes[blockIdx.x];
+  const uint32_t W = bs_limbs(N.m);
+  uint32_t* rk = sm;
+  const BsWork bw = BsWork::carve(sm + W, W, W / 2 + 3);
+  const uint32_t* R = pool + N.rank_off;
+  const uint32_t nr = R[0];
+  wb::copy(rk, R + 1, nr);
+  uint32_t t, nq, nrr;
+  bs_split<WarpOps>(N.m, N.k, rk, nr, bw, primes, nprimes, t, nq, nrr);
+  const uint32_t mL = N.m >> 1;
+  bs_emit(mL, t, N.word_off, bw.q, nq, next, nnext, jobs, pool, pool_cap, scr_base, cnt);
+  bs_emit(N.m - mL, N.k - t, N.word_off + mL, bw.rr, nrr, next, nnext, jobs, pool, pool_cap, scr_base, cnt);
 }
 
 // B2. one thread per job (pairs of <= kBsTop positions and B1's sub-problems)
@@ -346,7 +341,8 @@ struct BsPlan {
   std::vector<BsPair> pairs;
   std::vector<uint32_t> level_start;  // pairs of level L: [level_start[L], level_start[L+1])
   std::vector<BsJob> jobs;            // pairs of <= kBsTop positions
-  std::vector<uint32_t> big;          // pairs above kBsTop
+  std::vector<BsNode> roots;          // pairs above kBsTop (B1's depth 0)
+  std::vector<uint64_t> node_cap;     // B1 nodes per depth (upper bounds)
   std::vector<uint32_t> bm, bk;       // distinct class sizes C(bm, bk) of pairs above kBsWord
   std::vector<uint64_t> boff;         // their table offsets
   uint64_t btab_limbs = 0;
@@ -390,12 +386,17 @@ static BsPlan bs_plan(uint64_t n) {
       P.word_off = (uint64_t)level * n + j;
       P.scr_off = 0;
       if (m > kBsTop) {
-        pl.big.push_back((uint32_t)pl.pairs.size());
+        pl.roots.push_back(BsNode{m, P.n1, P.word_off, P.rank_off});
         pl.max_big = std::max(pl.max_big, m);
-        // its sub-problems have > kBsTop / 2 positions each
+        // its jobs have > kBsTop / 2 positions each; its nodes at depth d
+        // have at most ceil(m / 2^d) positions
         const uint64_t jobs = 2ull * m / kBsTop + 2;
         emit += jobs;
-        emit_rank += m / 32 + 3 * jobs;
+        for (int d = 0; d < kBsMaxDepth && ((m + (1ull << d) - 1) >> d) > kBsTop; ++d) {
+          if (pl.node_cap.size() <= (size_t)d) pl.node_cap.push_back(0);
+          pl.node_cap[d] += 1ull << d;
+          emit_rank += m / 32 + 8 + 4 * (2ull << d);
+        }
       } else {
         BsJob J;
         J.m = m;
@@ -422,32 +423,47 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
   if (n < 2) return;
   if (n > balanced_max_n()) throw std::invalid_argument("balanced_shuffle: n above the supported 2^17");
   BsPlan pl = bs_plan(n);
-  const uint32_t np = (uint32_t)pl.pairs.size(), nbig = (uint32_t)pl.big.size();
+  const uint32_t np = (uint32_t)pl.pairs.size(), nbig = (uint32_t)pl.roots.size();
+  const int depths = (int)pl.node_cap.size();
+  std::vector<uint64_t> node_off(depths + 2, 0);
+  for (int d = 0; d < depths; ++d) node_off[d + 1] = node_off[d] + pl.node_cap[d];
+  node_off[depths + 1] = node_off[depths] + 1;  // (the last depth's "next" list stays empty)
   std::vector<uint32_t> primes = primes_upto((uint32_t)n);
   const uint32_t wl = bs_limbs((uint32_t)n) + 8;
   const uint64_t emit_scr = (pl.job_cap - pl.jobs.size()) * bs_scratch_limbs(kBsTop);
-  BsCounters hc{(unsigned long long)pl.jobs.size(), (unsigned long long)pl.rank_limbs, 0ull};
+  BsCounters hc{};
+  hc.njobs = pl.jobs.size();
+  hc.pool_top = pl.rank_limbs;
+  hc.nnodes[0] = nbig;
   BsPair* d_pairs = nullptr;
   BsJob* d_jobs = nullptr;
   BsCounters* d_cnt = nullptr;
-  uint32_t *d_primes = nullptr, *d_pool = nullptr, *d_scr = nullptr, *d_big = nullptr, *d_bm = nullptr,
+  BsNode* d_nodes = nullptr;
+  uint32_t *d_primes = nullptr, *d_pool = nullptr, *d_scr = nullptr, *d_bm = nullptr,
            *d_bk = nullptr, *d_btab = nullptr;
   uint64_t* d_boff = nullptr;
   uint8_t* d_words = nullptr;
   void* d_tmp = nullptr;
   auto cleanup = [&]() {
     for (void* ptr : {(void*)d_pairs, (void*)d_jobs, (void*)d_cnt, (void*)d_primes, (void*)d_pool, (void*)d_scr,
-                      (void*)d_big, (void*)d_words, d_tmp, (void*)d_bm, (void*)d_bk, (void*)d_boff, (void*)d_btab})
+                      (void*)d_nodes, (void*)d_words, d_tmp, (void*)d_bm, (void*)d_bk, (void*)d_boff,
+                      (void*)d_btab})
       if (ptr) cudaFreeAsync(ptr, st);
   };
+  auto chk = [](const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+      throw std::runtime_error(std::string("balanced_shuffle: ") + what + ": " + cudaGetErrorString(e));
+  };
   try {
+    chk("before");
     if (cudaMallocAsync((void**)&d_pairs, np * sizeof(BsPair), st) ||
         cudaMallocAsync((void**)&d_jobs, std::max<uint64_t>(1, pl.job_cap) * sizeof(BsJob), st) ||
         cudaMallocAsync((void**)&d_cnt, sizeof(BsCounters), st) ||
         cudaMallocAsync((void**)&d_primes, std::max<size_t>(1, primes.size()) * 4, st) ||
         cudaMallocAsync((void**)&d_pool, (pl.pool_cap + 1) * 4, st) ||
         cudaMallocAsync((void**)&d_scr, (pl.scratch_limbs + emit_scr + 1) * 4, st) ||
-        cudaMallocAsync((void**)&d_big, std::max<size_t>(1, nbig) * 4, st) ||
+        cudaMallocAsync((void**)&d_nodes, node_off[depths + 1] * sizeof(BsNode), st) ||
         cudaMallocAsync((void**)&d_bm, std::max<size_t>(1, pl.bm.size()) * 4, st) ||
         cudaMallocAsync((void**)&d_bk, std::max<size_t>(1, pl.bm.size()) * 4, st) ||
         cudaMallocAsync((void**)&d_boff, std::max<size_t>(1, pl.bm.size()) * 8, st) ||
@@ -458,7 +474,7 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
         cudaMemcpyAsync(d_jobs, pl.jobs.data(), pl.jobs.size() * sizeof(BsJob), cudaMemcpyHostToDevice, st) ||
         cudaMemcpyAsync(d_cnt, &hc, sizeof(hc), cudaMemcpyHostToDevice, st) ||
         cudaMemcpyAsync(d_primes, primes.data(), primes.size() * 4, cudaMemcpyHostToDevice, st) ||
-        (nbig && cudaMemcpyAsync(d_big, pl.big.data(), nbig * 4, cudaMemcpyHostToDevice, st)) ||
+        (nbig && cudaMemcpyAsync(d_nodes, pl.roots.data(), nbig * sizeof(BsNode), cudaMemcpyHostToDevice, st)) ||
         (!pl.bm.empty() && (cudaMemcpyAsync(d_bm, pl.bm.data(), pl.bm.size() * 4, cudaMemcpyHostToDevice, st) ||
                             cudaMemcpyAsync(d_bk, pl.bk.data(), pl.bk.size() * 4, cudaMemcpyHostToDevice, st) ||
                             cudaMemcpyAsync(d_boff, pl.boff.data(), pl.boff.size() * 8, cudaMemcpyHostToDevice, st))))
@@ -472,21 +488,29 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
       cudaFuncSetAttribute(bs_binoms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemT);
       bs_binoms_kernel<<<nbin, 32, smemT, st>>>(d_bm, d_bk, d_boff, d_btab, d_primes, npr);
       count_launch();
+      chk("class sizes");
     }
     const size_t smemA = (size_t)4 * wl * 4;
     cudaFuncSetAttribute(bs_ranks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA);
     bs_ranks_kernel<<<1, 32, smemA, st>>>(d_pairs, np, sd, d_btab, d_pool, wl, d_bits);
     count_launch();
-    if (nbig) {
-      const size_t smemB = bs_top_smem_limbs(pl.max_big) * 4;
-      cudaFuncSetAttribute(bs_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemB);
-      bs_top_kernel<<<nbig, 32, smemB, st>>>(d_pairs, d_big, d_primes, npr, d_jobs, d_pool, pl.pool_cap,
-                                             pl.scratch_limbs, d_cnt);
+    chk("ranks");
+    if (depths) {
+      const size_t smem0 = bs_split_smem_limbs(pl.max_big + 1) * 4;  // depth 0's (the largest)
+      cudaFuncSetAttribute(bs_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem0);
+    }
+    for (int d = 0; d < depths; ++d) {  // one recursion depth per launch
+      const uint32_t mmax = (uint32_t)((pl.max_big + (1ull << d) - 1) >> d) + 1;
+      bs_split_kernel<<<(unsigned)pl.node_cap[d], 32, bs_split_smem_limbs(mmax) * 4, st>>>(
+          d_nodes + node_off[d], &d_cnt->nnodes[d], d_nodes + node_off[d + 1], &d_cnt->nnodes[d + 1], d_primes, npr,
+          d_jobs, d_pool, pl.pool_cap, pl.scratch_limbs, d_cnt);
       count_launch();
+      chk("splits");
     }
     bs_jobs_kernel<<<(unsigned)((pl.job_cap + 63) / 64), 64, 0, st>>>(d_jobs, d_cnt, d_pool, d_scr, d_primes, npr,
                                                                        d_words);
     count_launch();
+    chk("jobs");
     for (size_t L = 0; L + 1 < pl.level_start.size(); ++L) {
       const uint32_t p0 = pl.level_start[L], p1 = pl.level_start[L + 1];
       if (p1 == p0) continue;
@@ -510,7 +534,8 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
             d_pairs, p0, p1, (unsigned long long*)data, (unsigned long long*)d_tmp, d_words);
       count_launch();
     }
-    if (cudaGetLastError() != cudaSuccess) throw std::runtime_error("balanced_shuffle: launch failed");
+    const cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) throw std::runtime_error(std::string("balanced_shuffle: launch failed: ") + cudaGetErrorString(le));
   } catch (...) {
     cleanup();
     throw;
