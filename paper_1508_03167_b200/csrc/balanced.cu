@@ -66,88 +66,129 @@ __global__ void __launch_bounds__(32) bs_binoms_kernel(const uint32_t* __restric
   wb::copy(T + 1, num, n);
 }
 
-// A. (one warp)
+// A. the rolls, in schedule order on the one stream, as two kernels of one
+// warp: A1 the leading pairs of <= kBsWord positions (no class-size table
+// needed, so the table kernel runs beside it), A2 the rest.  The machine-word
+// rolls of one lane are bitstream.py:187-210 on uint64; the pairs of level 0
+// (one element per side: the roll below 2 is exactly one bit, always
+// accepted) are read in parallel.
 constexpr uint32_t kBsWord = 64;  // C(m, n1) < 2^62 for m <= 64
-__global__ void __launch_bounds__(32) bs_ranks_kernel(const BsPair* __restrict__ pairs, uint32_t npairs,
-                                                      StreamDesc sd, const uint32_t* __restrict__ btab,
-                                                      uint32_t* pool, uint32_t wl, unsigned long long* bits) {
-  __shared__ uint64_t Cw[(kBsWord + 1) * (kBsWord + 1)];  // C(a, b), a, b <= 64 (Pascal)
-  extern __shared__ uint32_t work[];                     // B, v, c and a spare: wl limbs each
-  const uint32_t lane = threadIdx.x;
+struct BsSmallTab {
+  uint64_t C[(kBsWord + 1) * (kBsWord + 1)];  // C(a, b), a, b <= 64 (Pascal)
+  uint8_t lb[(kBsWord + 1) * (kBsWord + 1)];  // bits of C(a, b) - 1
+};
+__device__ void bs_small_tab(BsSmallTab& T) {
+  const uint32_t lane = threadIdx.x & 31;
   for (uint32_t a = 0; a <= kBsWord; ++a) {
-    for (uint32_t b = lane; b <= kBsWord; b += 32)
-      Cw[a * (kBsWord + 1) + b] =
-          b > a ? 0ull : (b == 0 || b == a ? 1ull : Cw[(a - 1) * (kBsWord + 1) + b - 1] + Cw[(a - 1) * (kBsWord + 1) + b]);
+    for (uint32_t b = lane; b <= kBsWord; b += 32) {
+      const uint64_t v = b > a ? 0ull
+                               : (b == 0 || b == a ? 1ull
+                                                   : T.C[(a - 1) * (kBsWord + 1) + b - 1] +
+                                                         T.C[(a - 1) * (kBsWord + 1) + b]);
+      T.C[a * (kBsWord + 1) + b] = v;
+      T.lb[a * (kBsWord + 1) + b] = v > 1 ? (uint8_t)(64 - __clzll(v - 1)) : 0;
+    }
     __syncwarp();
   }
+}
+// one machine-word roll below C(m, n1) at stream offset o (one lane), with a
+// cache of the stream words cw, cw + 1
+__device__ __forceinline__ uint64_t bs_roll_word(const BsSmallTab& T, uint32_t m, uint32_t n1, const StreamDesc& sd,
+                                                 uint64_t& o, uint64_t& cw, uint64_t& cw0, uint64_t& cw1) {
+  const uint64_t bound = T.C[m * (kBsWord + 1) + n1];
+  const uint32_t lb = T.lb[m * (kBsWord + 1) + n1];
+  uint64_t vv = 1, cc = 0;
+  for (;;) {
+    uint32_t k = lb - (64 - __clzll(vv));  // smallest k with vv << k >= bound
+    if ((vv << k) < bound) ++k;
+    const uint64_t w = o >> 6;
+    if (w != cw) {
+      if (w == cw + 1) {
+        cw0 = cw1;
+        cw1 = bs_word(sd, w + 1);
+      } else {
+        cw0 = bs_word(sd, w);
+        cw1 = bs_word(sd, w + 1);
+      }
+      cw = w;
+    }
+    const uint32_t sh = (uint32_t)(o & 63);
+    const uint64_t x = sh ? (cw0 << sh) | (cw1 >> (64 - sh)) : cw0;
+    cc = k ? (cc << k) | (x >> (64 - k)) : cc;
+    o += k;
+    vv <<= k;
+    if (cc < bound) return cc;
+    cc -= bound;
+    vv -= bound;
+  }
+}
+__device__ __forceinline__ void bs_store_word_rank(uint32_t* R, uint64_t cc) {
+  R[0] = cc ? (cc >> 32 ? 2u : 1u) : 0u;
+  R[1] = (uint32_t)cc;
+  R[2] = (uint32_t)(cc >> 32);
+}
+
+// A1: pairs [0, p_end) (level 0 = [0, n0)), all of <= kBsWord positions;
+// leaves the stream offset in *o_out
+__global__ void __launch_bounds__(32) bs_ranks_small_kernel(const BsPair* __restrict__ pairs, uint32_t n0,
+                                                            uint32_t p_end, StreamDesc sd, uint32_t* pool,
+                                                            unsigned long long* o_out) {
+  __shared__ BsSmallTab T;
+  __shared__ uint32_t sm1[32], sm2[32];
+  __shared__ uint64_t sro[32];
+  const uint32_t lane = threadIdx.x;
+  bs_small_tab(T);
+  for (uint32_t p = lane; p < n0; p += 32)  // level 0: pair p is bit p
+    bs_store_word_rank(pool + pairs[p].rank_off, (bs_word(sd, p >> 6) >> (63 - (p & 63))) & 1u);
+  uint64_t o = n0, cw = ~1ull, cw0 = 0, cw1 = 0;
+  for (uint32_t p0 = n0; p0 < p_end; p0 += 32) {
+    if (p0 + lane < p_end) {
+      const BsPair& Q = pairs[p0 + lane];
+      sm1[lane] = Q.n1;
+      sm2[lane] = Q.n2;
+      sro[lane] = Q.rank_off;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t cnt = min(32u, p_end - p0);
+      for (uint32_t i = 0; i < cnt; ++i)
+        bs_store_word_rank(pool + sro[i], bs_roll_word(T, sm1[i] + sm2[i], sm1[i], sd, o, cw, cw0, cw1));
+    }
+    __syncwarp();
+  }
+  if (lane == 0) o_out[0] = o;
+}
+
+// A2: pairs [p_begin, npairs) from stream offset *bits; the class sizes of
+// the pairs above kBsWord from the table; the total bits into *bits
+__global__ void __launch_bounds__(32) bs_ranks_kernel(const BsPair* __restrict__ pairs, uint32_t p_begin,
+                                                      uint32_t npairs, StreamDesc sd,
+                                                      const uint32_t* __restrict__ btab, uint32_t* pool, uint32_t wl,
+                                                      unsigned long long* bits) {
+  __shared__ BsSmallTab T;
+  extern __shared__ uint32_t work[];  // B, v, c and a spare: wl limbs each
+  const uint32_t lane = threadIdx.x;
+  bs_small_tab(T);
   uint32_t* B = work;
   uint32_t* v = work + wl;
   uint32_t* c = work + 2 * wl;
   uint32_t* t = work + 3 * wl;
   uint32_t nB = 0, cb = ~0u;
-  uint64_t o = 0;  // stream offset (uniform)
-  uint32_t bn1 = 0, bn2 = 0, bbi = 0;
-  uint64_t broff = 0;
-  // lane 0's cache of the stream words w0 and w0 + 1 (the machine-word rolls)
-  uint64_t cw = ~1ull, cw0 = 0, cw1 = 0;  // (no word cached: cw + 1 != 0)
-  for (uint32_t p = 0; p < npairs; ++p) {
-    if ((p & 31) == 0 && p + lane < npairs) {  // the next 32 pairs' sizes, one per lane (coalesced)
-      const BsPair Q = pairs[p + lane];
-      bn1 = Q.n1;
-      bn2 = Q.n2;
-      broff = Q.rank_off;
-      bbi = Q.bidx;
-    }
-    BsPair P;
-    P.n1 = __shfl_sync(wb::kFull, bn1, p & 31);
-    P.n2 = __shfl_sync(wb::kFull, bn2, p & 31);
-    P.rank_off = __shfl_sync(wb::kFull, broff, p & 31);
-    P.bidx = __shfl_sync(wb::kFull, bbi, p & 31);
+  uint64_t o = bits[0];  // stream offset (uniform)
+  uint64_t cw = ~1ull, cw0 = 0, cw1 = 0;  // lane 0's word cache (no word cached: cw + 1 != 0)
+  for (uint32_t p = p_begin; p < npairs; ++p) {
+    const BsPair P = pairs[p];
     const uint32_t m = P.n1 + P.n2;
     uint32_t* R = pool + P.rank_off;
-    if (m <= kBsWord) {  // bitstream.py:187-210 in machine words (one lane)
-      if (lane == 0) {
-        const uint64_t bound = Cw[m * (kBsWord + 1) + P.n1];
-        const uint32_t lb = 64 - __clzll(bound - 1);  // bits of bound - 1
-        uint64_t vv = 1, cc = 0;
-        for (;;) {
-          uint32_t k = lb - (64 - __clzll(vv));  // smallest k with vv << k >= bound
-          if ((vv << k) < bound) ++k;
-          if (k) {  // the next k bits from the cached words
-            const uint64_t w = o >> 6;
-            if (w != cw) {
-              if (w == cw + 1) {
-                cw0 = cw1;
-                cw1 = bs_word(sd, w + 1);
-              } else {
-                cw0 = bs_word(sd, w);
-                cw1 = bs_word(sd, w + 1);
-              }
-              cw = w;
-            }
-            const uint32_t sh = (uint32_t)(o & 63);
-            const uint64_t x = sh ? (cw0 << sh) | (cw1 >> (64 - sh)) : cw0;
-            cc = (cc << k) | (x >> (64 - k));
-          } else {
-            cc <<= k;
-          }
-          o += k;
-          vv <<= k;
-          if (cc < bound) break;
-          cc -= bound;
-          vv -= bound;
-        }
-        R[0] = cc ? (cc >> 32 ? 2u : 1u) : 0u;
-        R[1] = (uint32_t)cc;
-        R[2] = (uint32_t)(cc >> 32);
-      }
+    if (m <= kBsWord) {
+      if (lane == 0) bs_store_word_rank(R, bs_roll_word(T, m, P.n1, sd, o, cw, cw0, cw1));
       o = __shfl_sync(wb::kFull, o, 0);
       continue;
     }
     if (P.bidx != cb) {  // pairs of a level repeat a handful of sizes
-      const uint32_t* T = btab + P.bidx;
-      nB = T[0];
-      wb::copy(B, T + 1, nB);
+      const uint32_t* TB = btab + P.bidx;
+      nB = TB[0];
+      wb::copy(B, TB + 1, nB);
       cb = P.bidx;
     }
     // fast dice roller below B (>= 2): v = 1, c = 0
@@ -348,6 +389,8 @@ struct BsPlan {
   uint64_t btab_limbs = 0;
   uint64_t rank_limbs = 0, scratch_limbs = 0, word_bytes = 0, job_cap = 0, pool_cap = 0;
   uint32_t max_big = 0;
+  uint32_t n_level0 = 0;     // pairs of level 0 (a prefix)
+  uint32_t p_small_end = 0;  // the leading pairs of <= kBsWord positions end here
 };
 
 static BsPlan bs_plan(uint64_t n) {
@@ -412,6 +455,9 @@ static BsPlan bs_plan(uint64_t n) {
   }
   pl.level_start.push_back((uint32_t)pl.pairs.size());
   pl.word_bytes = (uint64_t)level * n;
+  pl.n_level0 = pl.level_start.size() > 1 ? pl.level_start[1] : 0;
+  while (pl.p_small_end < pl.pairs.size() && pl.pairs[pl.p_small_end].n1 + pl.pairs[pl.p_small_end].n2 <= kBsWord)
+    ++pl.p_small_end;
   pl.job_cap = pl.jobs.size() + emit;
   pl.pool_cap = pl.rank_limbs + emit_rank + 16;
   return pl;
@@ -482,17 +528,35 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
     // the host vectors must outlive the (stream-ordered) copies
     if (cudaStreamSynchronize(st)) throw std::runtime_error("balanced_shuffle: upload failed");
     const uint32_t npr = (uint32_t)primes.size();
+    // A1 on st while the class sizes are computed on a side stream; A2 after both
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_tab = nullptr;
     const uint32_t nbin = (uint32_t)pl.bm.size();
     if (nbin) {
+      if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) || cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) ||
+          cudaEventCreateWithFlags(&ev_tab, cudaEventDisableTiming))
+        throw std::runtime_error("balanced_shuffle: stream setup failed");
+      cudaEventRecord(ev_fork, st);
+      cudaStreamWaitEvent(side, ev_fork, 0);
       const size_t smemT = (size_t)(bs_limbs((uint32_t)n) + 2) * 4;
       cudaFuncSetAttribute(bs_binoms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemT);
-      bs_binoms_kernel<<<nbin, 32, smemT, st>>>(d_bm, d_bk, d_boff, d_btab, d_primes, npr);
+      bs_binoms_kernel<<<nbin, 32, smemT, side>>>(d_bm, d_bk, d_boff, d_btab, d_primes, npr);
       count_launch();
+      cudaEventRecord(ev_tab, side);
       chk("class sizes");
+    }
+    bs_ranks_small_kernel<<<1, 32, 0, st>>>(d_pairs, pl.n_level0, pl.p_small_end, sd, d_pool, d_bits);
+    count_launch();
+    chk("small rolls");
+    if (nbin) {
+      cudaStreamWaitEvent(st, ev_tab, 0);
+      cudaEventDestroy(ev_fork);
+      cudaEventDestroy(ev_tab);
+      cudaStreamDestroy(side);  // (destroyed once its work completes)
     }
     const size_t smemA = (size_t)4 * wl * 4;
     cudaFuncSetAttribute(bs_ranks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA);
-    bs_ranks_kernel<<<1, 32, smemA, st>>>(d_pairs, np, sd, d_btab, d_pool, wl, d_bits);
+    bs_ranks_kernel<<<1, 32, smemA, st>>>(d_pairs, pl.p_small_end, np, sd, d_btab, d_pool, wl, d_bits);
     count_launch();
     chk("ranks");
     if (depths) {
