@@ -67,3 +67,18 @@ for lg in (24, 30):
     line(f"F2: rs_shuffle_parallel 2^{lg} u32",
          timed(lambda: sk.rs_shuffle_parallel(x, sk.ShuffleConfig(), sk.BitSource(0)), reps=3), 1 << lg)
     del x
+# F1 (config 5 names BalancedShuffle): the largest sizes served (wall time of
+# the call, which includes its host-side plan and uploads)
+for lg in (14, 16, 17):
+    x = torch.arange(1 << lg, dtype=torch.int32, device="cuda")
+
+    def bal():
+        sk.balanced_shuffle(x, sk.ShuffleConfig(), sk.BitSource(1))
+    bal()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        bal()
+    torch.cuda.synchronize()
+    line(f"F1: balanced_shuffle 2^{lg} u32", (time.perf_counter() - t0) * 1e3 / 3, 1 << lg, wall=True)
+    del x

@@ -8,7 +8,7 @@ Run in the build container only (the reference is not on the GPU box):
 Writes tests/golden/cli.json: for each command line, the reference's exit
 code, stdout and stderr (wall-clock columns of `bench` are blanked).  The
 commands only use algorithms the B200 backend serves (fy, merge, rs,
-balanced for n <= 32; chisq for fy / merge / merge_parallel / balanced).
+balanced for n <= 2^17; chisq for fy / merge / merge_parallel / balanced).
 """
 from __future__ import annotations
 
@@ -45,6 +45,10 @@ CASES = [
     {"argv": ["bench", "--algos", "balanced,merge", "--sizes", "5,17,32", "--trials", "4", "--seed", "2",
               "--threads", "2"]},
     {"argv": ["verify", "--mode", "chisq", "--algo", "balanced", "--n", "4", "--trials", "5000", "--seed", "3"]},
+    # BalancedShuffle with multi-limb ranks (n > 32)
+    {"argv": ["shuffle", "--algo", "balanced", "--n", "100", "--seed", "4", "--report"]},
+    {"argv": ["bench", "--algos", "balanced", "--sizes", "33,1000,5000", "--trials", "2", "--seed", "6",
+              "--threads", "1"]},
 ]
 
 
