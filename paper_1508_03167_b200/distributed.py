@@ -236,7 +236,15 @@ def _spanning_rounds_peer(shard, n, seed, engine, c, q, bounds, nblk, local_roun
             dist.barrier(group=grp)
             if rank == g0:
                 bits += engine.merge_peers(bases, starts, 0, eb, k - j, l - k, sseed, 2)
-            dist.barrier(group=grp)
+            # the next round's pairs span twice as many ranks: none of them may
+            # start touching this pair's buffers before its tail is applied, so
+            # the closing barrier is over the NEXT round's group (this one's at
+            # the top)
+            if r < c:
+                nspan = 2 * span
+                dist.barrier(group=groups.get(nspan, (rank // nspan) * nspan))
+            else:
+                dist.barrier(group=grp)
     finally:
         engine.close_peers()
     return bits
