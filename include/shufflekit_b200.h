@@ -138,13 +138,13 @@ int sk_merge_shuffle_seq(void *data, int elem_bytes, uint64_t n, uint64_t cutoff
 int sk_balanced_small(void *data, int elem_bytes, uint64_t n, uint64_t state_io[4], void *stream);
 
 /* Replaces balanced.balanced_shuffle (balanced.py:219-245) for any n up to
- * 2^17: the same singleton schedule and ONE stream;
+ * 2^20: the same singleton schedule and ONE stream;
  * each pair's class size C(n1+n2, n1) exact in multi-limb integers, the fast
  * dice roll below it (bitstream.py:187-210 random_int), the word by the
  * recursive-halving unranking (balanced.py:98-155 _locate_split /
  * _unrank_into), the interleave (balanced.py:198-216).  n <= 32 takes the
  * machine-word kernel of sk_balanced_small.  state_io as sk_fy_range.
- * SK_EINVAL above 2^17. */
+ * SK_EINVAL above 2^20. */
 int sk_balanced_shuffle(void *data, int elem_bytes, uint64_t n, uint64_t state_io[4], void *stream);
 
 /* Replaces _kernels.chi_counts (_kernels.py:489-526) for algo "fy" (0),

@@ -6,10 +6,10 @@ from the composition class C(n1+n2, n1) -- a fast dice roll below the class
 size on the caller's single stream -- and interleaves its two sides along
 it.  For n <= 32 the class sizes are machine words and the rank is decoded by
 the lexicographic walk (balanced.py:78-93, _unrank_small; sk_balanced_small).
-Larger n (up to 2^17) run sk_balanced_shuffle: the class sizes, the dice
+Larger n (up to 2^20) run sk_balanced_shuffle: the class sizes, the dice
 roll and the recursive-halving unranking with exact binomials
 (balanced.py:98-164) on multi-limb integers on the GPU, bit-exact with the
-reference.  Beyond 2^17 the call is refused rather than run on the CPU.
+reference.  Beyond 2^20 the call is refused rather than run on the CPU.
 """
 from __future__ import annotations
 
@@ -20,7 +20,7 @@ from .bitstream import BitSource, require_plain
 from .shufflers import ShuffleConfig, ShuffleReport, _Device
 
 SMALL_N = 32  # balanced.py:40
-MAX_N = 1 << 17
+MAX_N = 1 << 20
 
 
 def balanced_small_inplace(arr, src: BitSource) -> None:

@@ -164,9 +164,10 @@ __global__ void __launch_bounds__(32) bs_ranks_small_kernel(const BsPair* __rest
 __global__ void __launch_bounds__(32) bs_ranks_kernel(const BsPair* __restrict__ pairs, uint32_t p_begin,
                                                       uint32_t npairs, StreamDesc sd,
                                                       const uint32_t* __restrict__ btab, uint32_t* pool, uint32_t wl,
-                                                      unsigned long long* bits) {
+                                                      unsigned long long* bits, uint32_t* gwork) {
   __shared__ BsSmallTab T;
-  extern __shared__ uint32_t work[];  // B, v, c and a spare: wl limbs each
+  extern __shared__ uint32_t swork[];  // B, v, c and a spare: wl limbs each
+  uint32_t* work = gwork ? gwork : swork;  // (global when they do not fit)
   const uint32_t lane = threadIdx.x;
   bs_small_tab(T);
   uint32_t* B = work;
@@ -234,6 +235,7 @@ struct BsNode {
   uint64_t word_off, rank_off;
 };
 constexpr int kBsMaxDepth = 16;
+constexpr uint32_t kBsGlobM = 1u << 16;  // nodes above this may need global slots (the kernel decides exactly)
 
 __host__ __device__ inline uint64_t bs_split_smem_limbs(uint32_t m) {
   const uint32_t W = bs_limbs(m), H = W / 2 + 3;
@@ -265,10 +267,19 @@ __global__ void __launch_bounds__(32) bs_split_kernel(const BsNode* __restrict__
                                                       const unsigned long long* __restrict__ nnodes, BsNode* next,
                                                       unsigned long long* nnext, const uint32_t* __restrict__ primes,
                                                       uint32_t nprimes, BsJob* jobs, uint32_t* pool,
-                                                      uint64_t pool_cap, uint64_t scr_base, BsCounters* cnt) {
+                                                      uint64_t pool_cap, uint64_t scr_base, BsCounters* cnt,
+                                                      uint32_t smem_max_m, uint32_t* gscr, uint64_t gstride,
+                                                      unsigned long long* gslot) {
   if (blockIdx.x >= *nnodes) return;
-  extern __shared__ uint32_t sm[];
+  extern __shared__ uint32_t smem[];
   const BsNode N = nodes[blockIdx.x];
+  // nodes above smem_max_m positions work in a global slot
+  uint32_t* sm = smem;
+  if (N.m > smem_max_m) {
+    uint64_t slot = 0;
+    if (threadIdx.x == 0) slot = atomicAdd(gslot, 1ull);
+    sm = gscr + __shfl_sync(wb::kFull, slot, 0) * gstride;
+  }
   const uint32_t W = bs_limbs(N.m);
   uint32_t* rk = sm;
   const BsWork bw = BsWork::carve(sm + W, W, W / 2 + 3);
@@ -384,6 +395,7 @@ struct BsPlan {
   std::vector<BsJob> jobs;            // pairs of <= kBsTop positions
   std::vector<BsNode> roots;          // pairs above kBsTop (B1's depth 0)
   std::vector<uint64_t> node_cap;     // B1 nodes per depth (upper bounds)
+  std::vector<uint64_t> glob_cap;     // ... of them above kBsGlobM positions
   std::vector<uint32_t> bm, bk;       // distinct class sizes C(bm, bk) of pairs above kBsWord
   std::vector<uint64_t> boff;         // their table offsets
   uint64_t btab_limbs = 0;
@@ -436,8 +448,12 @@ static BsPlan bs_plan(uint64_t n) {
         const uint64_t jobs = 2ull * m / kBsTop + 2;
         emit += jobs;
         for (int d = 0; d < kBsMaxDepth && ((m + (1ull << d) - 1) >> d) > kBsTop; ++d) {
-          if (pl.node_cap.size() <= (size_t)d) pl.node_cap.push_back(0);
+          if (pl.node_cap.size() <= (size_t)d) {
+            pl.node_cap.push_back(0);
+            pl.glob_cap.push_back(0);
+          }
           pl.node_cap[d] += 1ull << d;
+          if (((m + (1ull << d) - 1) >> d) > kBsGlobM) pl.glob_cap[d] += 1ull << d;
           emit_rank += m / 32 + 8 + 4 * (2ull << d);
         }
       } else {
@@ -463,11 +479,12 @@ static BsPlan bs_plan(uint64_t n) {
   return pl;
 }
 
-uint64_t balanced_max_n() { return 1ull << 17; }
+uint64_t balanced_max_n() { return 1ull << 20; }
+constexpr size_t kBsSmemBudget = 200 * 1024;  // dynamic shared memory per CTA we plan with
 
 void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long long* d_bits, cudaStream_t st) {
   if (n < 2) return;
-  if (n > balanced_max_n()) throw std::invalid_argument("balanced_shuffle: n above the supported 2^17");
+  if (n > balanced_max_n()) throw std::invalid_argument("balanced_shuffle: n above the supported 2^20");
   BsPlan pl = bs_plan(n);
   const uint32_t np = (uint32_t)pl.pairs.size(), nbig = (uint32_t)pl.roots.size();
   const int depths = (int)pl.node_cap.size();
@@ -485,6 +502,8 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
   BsJob* d_jobs = nullptr;
   BsCounters* d_cnt = nullptr;
   BsNode* d_nodes = nullptr;
+  uint32_t *d_gwork = nullptr, *d_gscr = nullptr;
+  unsigned long long* d_gslot = nullptr;
   uint32_t *d_primes = nullptr, *d_pool = nullptr, *d_scr = nullptr, *d_bm = nullptr,
            *d_bk = nullptr, *d_btab = nullptr;
   uint64_t* d_boff = nullptr;
@@ -493,7 +512,7 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
   auto cleanup = [&]() {
     for (void* ptr : {(void*)d_pairs, (void*)d_jobs, (void*)d_cnt, (void*)d_primes, (void*)d_pool, (void*)d_scr,
                       (void*)d_nodes, (void*)d_words, d_tmp, (void*)d_bm, (void*)d_bk, (void*)d_boff,
-                      (void*)d_btab})
+                      (void*)d_btab, (void*)d_gwork, (void*)d_gscr, (void*)d_gslot})
       if (ptr) cudaFreeAsync(ptr, st);
   };
   auto chk = [](const char* what) {
@@ -555,19 +574,38 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
       cudaStreamDestroy(side);  // (destroyed once its work completes)
     }
     const size_t smemA = (size_t)4 * wl * 4;
-    cudaFuncSetAttribute(bs_ranks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA);
-    bs_ranks_kernel<<<1, 32, smemA, st>>>(d_pairs, pl.p_small_end, np, sd, d_btab, d_pool, wl, d_bits);
+    if (smemA > kBsSmemBudget) {
+      if (cudaMallocAsync((void**)&d_gwork, smemA, st)) throw std::runtime_error("balanced_shuffle: allocation failed");
+    } else {
+      cudaFuncSetAttribute(bs_ranks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA);
+    }
+    bs_ranks_kernel<<<1, 32, d_gwork ? 0 : smemA, st>>>(d_pairs, pl.p_small_end, np, sd, d_btab, d_pool, wl, d_bits,
+                                                        d_gwork);
     count_launch();
     chk("ranks");
+    // nodes up to smem_max_m positions split in shared memory, larger ones
+    // (n > 2^17) in global slots
+    uint32_t smem_max_m = 1;
+    while (bs_split_smem_limbs(2 * smem_max_m + 1) * 4 <= kBsSmemBudget) smem_max_m *= 2;
     if (depths) {
-      const size_t smem0 = bs_split_smem_limbs(pl.max_big + 1) * 4;  // depth 0's (the largest)
+      const size_t smem0 = bs_split_smem_limbs(std::min<uint32_t>(pl.max_big, smem_max_m) + 1) * 4;
       cudaFuncSetAttribute(bs_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem0);
+      // global slots: at depth d the nodes above smem_max_m are at most
+      // glob_cap[d], each of at most ceil(max_big / 2^d) + 1 positions
+      uint64_t gmax = 0;
+      for (int d = 0; d < depths; ++d)
+        gmax = std::max(gmax, pl.glob_cap[d] * bs_split_smem_limbs((uint32_t)((pl.max_big + (1ull << d) - 1) >> d) + 1));
+      if (gmax && (cudaMallocAsync((void**)&d_gscr, gmax * 4, st) ||
+                   cudaMallocAsync((void**)&d_gslot, depths * sizeof(unsigned long long), st) ||
+                   cudaMemsetAsync(d_gslot, 0, depths * sizeof(unsigned long long), st)))
+        throw std::runtime_error("balanced_shuffle: allocation failed");
     }
     for (int d = 0; d < depths; ++d) {  // one recursion depth per launch
       const uint32_t mmax = (uint32_t)((pl.max_big + (1ull << d) - 1) >> d) + 1;
-      bs_split_kernel<<<(unsigned)pl.node_cap[d], 32, bs_split_smem_limbs(mmax) * 4, st>>>(
+      const uint64_t stride = bs_split_smem_limbs(mmax);
+      bs_split_kernel<<<(unsigned)pl.node_cap[d], 32, bs_split_smem_limbs(std::min(mmax, smem_max_m + 1)) * 4, st>>>(
           d_nodes + node_off[d], &d_cnt->nnodes[d], d_nodes + node_off[d + 1], &d_cnt->nnodes[d + 1], d_primes, npr,
-          d_jobs, d_pool, pl.pool_cap, pl.scratch_limbs, d_cnt);
+          d_jobs, d_pool, pl.pool_cap, pl.scratch_limbs, d_cnt, smem_max_m, d_gscr, stride, d_gslot ? d_gslot + d : nullptr);
       count_launch();
       chk("splits");
     }

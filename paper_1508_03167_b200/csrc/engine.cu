@@ -1396,7 +1396,7 @@ int sk_balanced_shuffle(void* data, int elem_bytes, uint64_t n, uint64_t state_i
   if (int e = check_eb(elem_bytes)) return e;
   if (!state_io || !data) { set_err("balanced_shuffle: data and a state"); return SK_EINVAL; }
   if (state_io[2] > 63) { set_err("buffered_bits must be < 64"); return SK_EINVAL; }
-  if (n > balanced_max_n()) { set_err("balanced_shuffle: n above the supported 2^17"); return SK_EINVAL; }
+  if (n > balanced_max_n()) { set_err("balanced_shuffle: n above the supported 2^20"); return SK_EINVAL; }
   SK_TRY
   cudaStream_t st = (cudaStream_t)stream;
   setup_pool_once();

@@ -1,6 +1,6 @@
 """Goldens for BalancedShuffle beyond the machine-word slice (SURVEY.md
-section 8 row F1, n = 33 .. 2^17) from the UNMODIFIED reference.  Build
-container only (the reference's pure-Python big-integer path; ~4 s at 2^17):
+section 8 row F1, n = 33 .. 2^20) from the UNMODIFIED reference.  Build
+container only (the reference's pure-Python big-integer path; ~4 min with 2^18..2^20):
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \\
         python tests/golden/make_balanced_big_golden.py
@@ -23,13 +23,13 @@ from shufflekit.shufflers import ShuffleConfig
 OUT = os.path.dirname(os.path.abspath(__file__))
 SIZES = [33, 34, 40, 47, 63, 64, 65, 96, 100, 127, 128, 129, 200, 255, 256, 257, 333, 500, 511, 512, 513, 600,
          1000, 1023, 1024, 1025, 2047, 2048, 3000, 4093, 4096, 5000, 8191, 10007, 16384, 30000, 65535, 65536,
-         100000, 131072]
+         100000, 131072, 1 << 18, 1 << 19, 1 << 20]
 
 
 def main():
     cases = []
     for n in SIZES:
-        pres = ((0,), (13,), (64, 5)) if n <= 4096 else ((0,), (37,))
+        pres = ((0,), (13,), (64, 5)) if n <= 4096 else (((0,), (37,)) if n <= 131072 else ((0,),))
         for q, pre in enumerate(pres):
             src = sk.BitSource((n * 2654435761 + 17 * q) % (1 << 64))
             for k in pre:

@@ -42,4 +42,4 @@ def test_invalid_arguments_rejected_without_gpu():
     assert lib.sk_fy_range(None, 4, 5, 2, st, None) == -1                          # hi < lo
     assert lib.sk_merge_range(None, 4, 0, 5, 2, st, None) == -1                   # l < k
     assert lib.sk_chi_counts(7, 6, 10, 0, 0, None, None) == -1                     # algo
-    assert lib.sk_balanced_shuffle(ctypes.c_void_p(16), 4, (1 << 17) + 1, st, None) == -1  # n above 2^17
+    assert lib.sk_balanced_shuffle(ctypes.c_void_p(16), 4, (1 << 20) + 1, st, None) == -1  # n above 2^20

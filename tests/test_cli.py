@@ -42,7 +42,7 @@ def test_cli_matches_reference(case):
     assert p.stderr == case["stderr"]
 
 
-@pytest.mark.parametrize("argv", [["shuffle", "--algo", "balanced", "--n", str((1 << 17) + 1), "--seed", "1"],
+@pytest.mark.parametrize("argv", [["shuffle", "--algo", "balanced", "--n", str((1 << 20) + 1), "--seed", "1"],
                                   ["verify", "--mode", "exact", "--algo", "merge", "--n", "4"],
                                   ["shuffle", "--algo", "merge", "--n", "-1", "--seed", "1"],
                                   ["bench", "--algos", "merge", "--sizes", "x", "--seed", "1"]])

@@ -1,6 +1,6 @@
 """BalancedShuffle on the GPU: bit-exact against
 the reference's goldens (balanced_shuffle with state write-back for n <= 32
-and for n = 33 .. 2^17, chi_counts("balanced") histograms) and the oracles
+and for n = 33 .. 2^20, chi_counts("balanced") histograms) and the oracles
 (the C restatement for n <= 32, oracle/balanced_oracle.py beyond)."""
 import hashlib
 import json
@@ -69,7 +69,7 @@ def test_balanced_chi_square_passes():
 
 @pytest.mark.parametrize("case", BIG, ids=lambda c: f"n{c['n']}_{c['state_in'][3]}_{c['state_in'][0] % 997}")
 def test_balanced_multilimb_reference_goldens(case):
-    # n = 33 .. 2^17: multi-limb class sizes, dice rolls and unranking
+    # n = 33 .. 2^20: multi-limb class sizes, dice rolls and unranking
     dtype = torch.int32 if case["n"] % 2 else torch.int64
     src = sk.BitSource(0)
     src.set_state_tuple(case["state_in"])
@@ -113,4 +113,4 @@ def test_balanced_items_list_multilimb():
 
 def test_balanced_beyond_supported_refused():
     with pytest.raises(NotImplementedError):
-        sk.balanced_shuffle(torch.arange((1 << 17) + 1, device="cuda"), sk.ShuffleConfig(), sk.BitSource(1))
+        sk.balanced_shuffle(torch.arange((1 << 20) + 1, device="cuda"), sk.ShuffleConfig(), sk.BitSource(1))

@@ -1,6 +1,6 @@
 """The multi-limb BalancedShuffle oracle (oracle/balanced_oracle.py) against the unmodified
 reference's outputs (tests/golden/balanced.json for n <= 32,
-balanced_big.json for n = 33 .. 2^17): permutation, bit count, end state."""
+balanced_big.json for n = 33 .. 2^20): permutation, bit count, end state."""
 import hashlib
 import json
 import os
