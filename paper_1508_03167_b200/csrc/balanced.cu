@@ -50,7 +50,6 @@ struct BsJob {
 // device-side bump counters of stage B
 struct BsCounters {
   unsigned long long njobs, pool_top, scr_top;
-  unsigned long long nnodes[16];  // B1 nodes per recursion depth
 };
 
 // The class sizes C(m, n1) of the pairs above kBsWord positions, one warp
@@ -242,8 +241,10 @@ __host__ __device__ inline uint64_t bs_split_smem_limbs(uint32_t m) {
   return (uint64_t)W + BsWork::limbs(W, H);
 }
 
+// a half of a split: a node of the next depth in slot `slot` (when it is
+// still above kBsTop) or a B2 job (then the slot holds an empty node)
 __device__ void bs_emit(uint32_t m, uint32_t k, uint64_t word_off, const uint32_t* rank, uint32_t nr, BsNode* next,
-                        unsigned long long* nnext, BsJob* jobs, uint32_t* pool, uint64_t pool_cap,
+                        uint64_t slot, uint64_t next_cap, BsJob* jobs, uint32_t* pool, uint64_t pool_cap,
                         uint64_t scr_base, BsCounters* cnt) {
   uint64_t ro = 0;
   if (threadIdx.x == 0) {
@@ -251,8 +252,10 @@ __device__ void bs_emit(uint32_t m, uint32_t k, uint64_t word_off, const uint32_
     if (ro + nr + 1 > pool_cap) __trap();  // (the pool is sized for every sub-rank)
     pool[ro] = nr;
     if (m > kBsTop) {
-      next[atomicAdd(nnext, 1ull)] = BsNode{m, k, word_off, ro};
+      if (slot >= next_cap) __trap();  // (the slots of a depth cover its nodes)
+      next[slot] = BsNode{m, k, word_off, ro};
     } else {
+      if (slot < next_cap) next[slot] = BsNode{0, 0, 0, 0};
       const uint64_t j = atomicAdd(&cnt->njobs, 1ull);
       const uint64_t so =
           m > (uint32_t)kBsSmall ? atomicAdd(&cnt->scr_top, (unsigned long long)bs_scratch_limbs(m)) : 0ull;
@@ -263,16 +266,23 @@ __device__ void bs_emit(uint32_t m, uint32_t k, uint64_t word_off, const uint32_
   wb::copy(pool + ro + 1, rank, nr);
 }
 
-__global__ void __launch_bounds__(32) bs_split_kernel(const BsNode* __restrict__ nodes,
-                                                      const unsigned long long* __restrict__ nnodes, BsNode* next,
-                                                      unsigned long long* nnext, const uint32_t* __restrict__ primes,
+// Node slots: the roots (pairs above kBsTop) largest first, the children of
+// slot i in slots 2i, 2i + 1 of the next depth -- so every depth starts its
+// largest splits first; empty slots (m = 0) pass emptiness on.
+__global__ void __launch_bounds__(32) bs_split_kernel(const BsNode* __restrict__ nodes, BsNode* next,
+                                                      uint64_t next_cap, const uint32_t* __restrict__ primes,
                                                       uint32_t nprimes, BsJob* jobs, uint32_t* pool,
                                                       uint64_t pool_cap, uint64_t scr_base, BsCounters* cnt,
                                                       uint32_t smem_max_m, uint32_t* gscr, uint64_t gstride,
                                                       unsigned long long* gslot) {
-  if (blockIdx.x >= *nnodes) return;
   extern __shared__ uint32_t smem[];
   const BsNode N = nodes[blockIdx.x];
+  const uint64_t s0 = 2ull * blockIdx.x;
+  if (N.m == 0) {
+    if (threadIdx.x == 0)
+      for (uint64_t s = s0; s < s0 + 2 && s < next_cap; ++s) next[s] = BsNode{0, 0, 0, 0};
+    return;
+  }
   // nodes above smem_max_m positions work in a global slot
   uint32_t* sm = smem;
   if (N.m > smem_max_m) {
@@ -289,8 +299,9 @@ __global__ void __launch_bounds__(32) bs_split_kernel(const BsNode* __restrict__
   uint32_t t, nq, nrr;
   bs_split<WarpOps>(N.m, N.k, rk, nr, bw, primes, nprimes, t, nq, nrr);
   const uint32_t mL = N.m >> 1;
-  bs_emit(mL, t, N.word_off, bw.q, nq, next, nnext, jobs, pool, pool_cap, scr_base, cnt);
-  bs_emit(N.m - mL, N.k - t, N.word_off + mL, bw.rr, nrr, next, nnext, jobs, pool, pool_cap, scr_base, cnt);
+  bs_emit(mL, t, N.word_off, bw.q, nq, next, s0, next_cap, jobs, pool, pool_cap, scr_base, cnt);
+  bs_emit(N.m - mL, N.k - t, N.word_off + mL, bw.rr, nrr, next, s0 + 1, next_cap, jobs, pool, pool_cap, scr_base,
+          cnt);
 }
 
 // B2. one thread per job (pairs of <= kBsTop positions and B1's sub-problems)
@@ -448,11 +459,7 @@ static BsPlan bs_plan(uint64_t n) {
         const uint64_t jobs = 2ull * m / kBsTop + 2;
         emit += jobs;
         for (int d = 0; d < kBsMaxDepth && ((m + (1ull << d) - 1) >> d) > kBsTop; ++d) {
-          if (pl.node_cap.size() <= (size_t)d) {
-            pl.node_cap.push_back(0);
-            pl.glob_cap.push_back(0);
-          }
-          pl.node_cap[d] += 1ull << d;
+          if (pl.glob_cap.size() <= (size_t)d) pl.glob_cap.push_back(0);
           if (((m + (1ull << d) - 1) >> d) > kBsGlobM) pl.glob_cap[d] += 1ull << d;
           emit_rank += m / 32 + 8 + 4 * (2ull << d);
         }
@@ -471,6 +478,15 @@ static BsPlan bs_plan(uint64_t n) {
   }
   pl.level_start.push_back((uint32_t)pl.pairs.size());
   pl.word_bytes = (uint64_t)level * n;
+  // node slots: roots largest first; depth d has 2^d slots per root that
+  // still has nodes there (a prefix of the roots)
+  std::stable_sort(pl.roots.begin(), pl.roots.end(), [](const BsNode& x, const BsNode& y) { return x.m > y.m; });
+  for (int d = 0; d < kBsMaxDepth; ++d) {
+    uint64_t r = 0;
+    while (r < pl.roots.size() && ((pl.roots[r].m + (1ull << d) - 1) >> d) > kBsTop) ++r;
+    if (!r) break;
+    pl.node_cap.push_back(r << d);
+  }
   pl.n_level0 = pl.level_start.size() > 1 ? pl.level_start[1] : 0;
   while (pl.p_small_end < pl.pairs.size() && pl.pairs[pl.p_small_end].n1 + pl.pairs[pl.p_small_end].n2 <= kBsWord)
     ++pl.p_small_end;
@@ -497,7 +513,6 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
   BsCounters hc{};
   hc.njobs = pl.jobs.size();
   hc.pool_top = pl.rank_limbs;
-  hc.nnodes[0] = nbig;
   BsPair* d_pairs = nullptr;
   BsJob* d_jobs = nullptr;
   BsCounters* d_cnt = nullptr;
@@ -603,9 +618,10 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
     for (int d = 0; d < depths; ++d) {  // one recursion depth per launch
       const uint32_t mmax = (uint32_t)((pl.max_big + (1ull << d) - 1) >> d) + 1;
       const uint64_t stride = bs_split_smem_limbs(mmax);
+      const uint64_t next_cap = d + 1 < depths ? pl.node_cap[d + 1] : 0;
       bs_split_kernel<<<(unsigned)pl.node_cap[d], 32, bs_split_smem_limbs(std::min(mmax, smem_max_m + 1)) * 4, st>>>(
-          d_nodes + node_off[d], &d_cnt->nnodes[d], d_nodes + node_off[d + 1], &d_cnt->nnodes[d + 1], d_primes, npr,
-          d_jobs, d_pool, pl.pool_cap, pl.scratch_limbs, d_cnt, smem_max_m, d_gscr, stride, d_gslot ? d_gslot + d : nullptr);
+          d_nodes + node_off[d], d_nodes + node_off[d + 1], next_cap, d_primes, npr, d_jobs, d_pool, pl.pool_cap,
+          pl.scratch_limbs, d_cnt, smem_max_m, d_gscr, stride, d_gslot ? d_gslot + d : nullptr);
       count_launch();
       chk("splits");
     }

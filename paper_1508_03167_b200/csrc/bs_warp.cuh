@@ -143,7 +143,20 @@ __device__ uint32_t mul_small(uint32_t* a, uint32_t na, uint32_t m) {
   uint32_t lo, hi;
   chunk_of(S, lo, hi);
   uint64_t c = 0;
-  for (uint32_t i = lo; i < hi; ++i) {
+  uint32_t i = lo;
+  // (loads batched eight at a time: the walk is a carry chain, the loads are not)
+  for (const uint32_t hn = min(hi, na); i + 8 <= hn; i += 8) {
+    uint32_t x[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) x[e] = a[i + e];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      c += (uint64_t)x[e] * m;
+      a[i + e] = (uint32_t)c;
+      c >>= 32;
+    }
+  }
+  for (; i < hi; ++i) {
     c += (uint64_t)(i < na ? a[i] : 0u) * m;
     a[i] = (uint32_t)c;
     c >>= 32;
@@ -156,12 +169,23 @@ __device__ uint32_t div_small(uint32_t* q, const uint32_t* a, uint32_t na, uint3
   uint32_t lo, hi;
   chunk_of(na, lo, hi);
   const Div D(d);
-  // this chunk's value mod d and 2^(32 len) mod d
+  // this chunk's value mod d (loads batched) and 2^(32 len) mod d (by squaring)
   uint64_t V = 0, P = 1;
-  const uint64_t t32 = D.mod(1ull << 32);
-  for (uint32_t i = hi; i > lo; --i) {
-    V = D.mod((V << 32) | a[i - 1]);
-    P = D.mod(P * t32);
+  {
+    uint32_t i = hi;
+    for (; i >= lo + 8; i -= 8) {
+      uint32_t x[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = a[i - 1 - e];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) V = D.mod((V << 32) | x[e]);
+    }
+    for (; i > lo; --i) V = D.mod((V << 32) | a[i - 1]);
+    uint64_t base = D.mod(1ull << 32);
+    for (uint32_t e = hi - lo; e; e >>= 1) {
+      if (e & 1) P = D.mod(P * base);
+      base = D.mod(base * base);
+    }
   }
   // suffix composition of the maps r -> r * P + V (the top lane's applies first):
   // C_l = f_l o f_{l+1} o ... o f_31
@@ -176,10 +200,24 @@ __device__ uint32_t div_small(uint32_t* q, const uint32_t* a, uint32_t na, uint3
   uint64_t r = __shfl_down_sync(kFull, CV, 1);  // remainder entering this chunk
   if (lane_id() == 31) r = 0;
   __syncwarp();
-  for (uint32_t i = hi; i > lo; --i) {
-    uint64_t rr;
-    q[i - 1] = (uint32_t)D.qr((r << 32) | a[i - 1], rr);
-    r = rr;
+  {
+    uint32_t i = hi;
+    for (; i >= lo + 8; i -= 8) {
+      uint32_t x[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = a[i - 1 - e];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        uint64_t rr;
+        q[i - 1 - e] = (uint32_t)D.qr((r << 32) | x[e], rr);
+        r = rr;
+      }
+    }
+    for (; i > lo; --i) {
+      uint64_t rr;
+      q[i - 1] = (uint32_t)D.qr((r << 32) | a[i - 1], rr);
+      r = rr;
+    }
   }
   const uint32_t rem = (uint32_t)__shfl_sync(kFull, r, 0);
   __syncwarp();
