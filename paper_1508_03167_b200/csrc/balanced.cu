@@ -32,13 +32,14 @@
 #include <vector>
 #include "sk_kernels.h"
 #include "bs_core.cuh"
-#include "bs_warp.cuh"
+#include "bs_group.cuh"
 
 namespace sk {
 // (the multi-limb naturals and the per-pair stages: bs_core.cuh)
 
 
-constexpr uint32_t kBsTop = 1024;  // pairs / sub-problems above this many positions: a warp
+constexpr uint32_t kBsTop = 1024;
+constexpr int kBsGroupBlock = 256;  // threads of a block group  // pairs / sub-problems above this many positions: a warp
 
 // A sub-problem of stage B: the word of m positions with k zeros and rank at
 // pool + rank_off ([limb count, limbs]), into words + word_off; its serial
@@ -54,15 +55,15 @@ struct BsCounters {
 
 // The class sizes C(m, n1) of the pairs above kBsWord positions, one warp
 // each (data independent: computed before the sequential rolls need them);
-// entry b at table + boff[b] as [limb count, limbs].
-__global__ void __launch_bounds__(32) bs_binoms_kernel(const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bk,
+// entry b at table + boff[b] as [limb count, limbs].  One block each.
+__global__ void __launch_bounds__(kBsGroupBlock) bs_binoms_kernel(const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bk,
                                                        const uint64_t* __restrict__ boff, uint32_t* table,
                                                        const uint32_t* __restrict__ primes, uint32_t nprimes) {
   extern __shared__ uint32_t num[];
-  const uint32_t n = wb::binom(num, bm[blockIdx.x], bk[blockIdx.x], primes, nprimes);
+  const uint32_t n = gp::binom<gp::BlockG>(num, bm[blockIdx.x], bk[blockIdx.x], primes, nprimes);
   uint32_t* T = table + boff[blockIdx.x];
   if (threadIdx.x == 0) T[0] = n;
-  wb::copy(T + 1, num, n);
+  gp::copy<gp::BlockG>(T + 1, num, n);
 }
 
 // A. the rolls, in schedule order on the one stream, as two kernels of one
@@ -182,43 +183,43 @@ __global__ void __launch_bounds__(32) bs_ranks_kernel(const BsPair* __restrict__
     uint32_t* R = pool + P.rank_off;
     if (m <= kBsWord) {
       if (lane == 0) bs_store_word_rank(R, bs_roll_word(T, m, P.n1, sd, o, cw, cw0, cw1));
-      o = __shfl_sync(wb::kFull, o, 0);
+      o = __shfl_sync(gp::kFull, o, 0);
       continue;
     }
     if (P.bidx != cb) {  // pairs of a level repeat a handful of sizes
       const uint32_t* TB = btab + P.bidx;
       nB = TB[0];
-      wb::copy(B, TB + 1, nB);
+      gp::copy<gp::WarpG>(B, TB + 1, nB);
       cb = P.bidx;
     }
     // fast dice roller below B (>= 2): v = 1, c = 0
     if (lane == 0) v[0] = 1;
     __syncwarp();
     uint32_t nv = 1, nc = 0;
-    const uint32_t lb = wb::bitlen(B, nB);
+    const uint32_t lb = gp::bitlen<gp::WarpG>(B, nB);
     for (;;) {
-      uint32_t k = lb - wb::bitlen(v, nv);  // smallest k with v << k >= B
-      if (wb::cmp_shl(v, nv, k, B, nB) < 0) ++k;
+      uint32_t k = lb - gp::bitlen<gp::WarpG>(v, nv);  // smallest k with v << k >= B
+      if (gp::cmp_shl<gp::WarpG>(v, nv, k, B, nB) < 0) ++k;
       // c = (c << k) | the next k bits: limb i of them is stream bits
       // [o + k - 32(i+1), o + k - 32 i)
-      nc = wb::shl(t, c, nc, k);
+      nc = gp::shl<gp::WarpG>(t, c, nc, k);
       const uint32_t full = k >> 5, part = k & 31, nk = full + (part ? 1u : 0u);
       for (uint32_t i = nc + lane; i < nk; i += 32) t[i] = 0;
       __syncwarp();
       for (uint32_t i = lane; i < full; i += 32) t[i] |= bs_bits(sd, o + k - 32 * (i + 1), 32);
       if (part && lane == 0) t[full] |= bs_bits(sd, o, part);
       __syncwarp();
-      nc = wb::trim(t, nc > nk ? nc : nk);
+      nc = gp::trim<gp::WarpG>(t, nc > nk ? nc : nk);
       { uint32_t* x = c; c = t; t = x; }
       o += k;
-      nv = wb::shl(t, v, nv, k);
+      nv = gp::shl<gp::WarpG>(t, v, nv, k);
       { uint32_t* x = v; v = t; t = x; }
-      if (wb::cmp(c, nc, B, nB) < 0) break;
-      nc = wb::sub(c, c, nc, B, nB);
-      nv = wb::sub(v, v, nv, B, nB);
+      if (gp::cmp<gp::WarpG>(c, nc, B, nB) < 0) break;
+      nc = gp::sub<gp::WarpG>(c, c, nc, B, nB);
+      nv = gp::sub<gp::WarpG>(v, v, nv, B, nB);
     }
     if (lane == 0) R[0] = nc;
-    wb::copy(R + 1, c, nc);
+    gp::copy<gp::WarpG>(R + 1, c, nc);
   }
   if (lane == 0) bits[0] = o;
 }
@@ -234,6 +235,7 @@ struct BsNode {
   uint64_t word_off, rank_off;
 };
 constexpr int kBsMaxDepth = 16;
+constexpr uint32_t kBsBlockM = 1u << 15;  // nodes above this split on a block of kBsGroupBlock threads
 constexpr uint32_t kBsGlobM = 1u << 16;  // nodes above this may need global slots (the kernel decides exactly)
 
 __host__ __device__ inline uint64_t bs_split_smem_limbs(uint32_t m) {
@@ -243,6 +245,7 @@ __host__ __device__ inline uint64_t bs_split_smem_limbs(uint32_t m) {
 
 // a half of a split: a node of the next depth in slot `slot` (when it is
 // still above kBsTop) or a B2 job (then the slot holds an empty node)
+template <class G>
 __device__ void bs_emit(uint32_t m, uint32_t k, uint64_t word_off, const uint32_t* rank, uint32_t nr, BsNode* next,
                         uint64_t slot, uint64_t next_cap, BsJob* jobs, uint32_t* pool, uint64_t pool_cap,
                         uint64_t scr_base, BsCounters* cnt) {
@@ -262,22 +265,24 @@ __device__ void bs_emit(uint32_t m, uint32_t k, uint64_t word_off, const uint32_
       jobs[j] = BsJob{m, k, word_off, ro, scr_base + so};
     }
   }
-  ro = __shfl_sync(wb::kFull, ro, 0);
-  wb::copy(pool + ro + 1, rank, nr);
+  ro = G::from(ro, 0);
+  gp::copy<G>(pool + ro + 1, rank, nr);
 }
 
 // Node slots: the roots (pairs above kBsTop) largest first, the children of
 // slot i in slots 2i, 2i + 1 of the next depth -- so every depth starts its
 // largest splits first; empty slots (m = 0) pass emptiness on.
-__global__ void __launch_bounds__(32) bs_split_kernel(const BsNode* __restrict__ nodes, BsNode* next,
+template <class G, int NT>
+__global__ void __launch_bounds__(NT) bs_split_kernel(uint64_t slot0, const BsNode* __restrict__ nodes, BsNode* next,
                                                       uint64_t next_cap, const uint32_t* __restrict__ primes,
                                                       uint32_t nprimes, BsJob* jobs, uint32_t* pool,
                                                       uint64_t pool_cap, uint64_t scr_base, BsCounters* cnt,
                                                       uint32_t smem_max_m, uint32_t* gscr, uint64_t gstride,
                                                       unsigned long long* gslot) {
   extern __shared__ uint32_t smem[];
-  const BsNode N = nodes[blockIdx.x];
-  const uint64_t s0 = 2ull * blockIdx.x;
+  const uint64_t slot = slot0 + blockIdx.x;
+  const BsNode N = nodes[slot];
+  const uint64_t s0 = 2ull * slot;
   if (N.m == 0) {
     if (threadIdx.x == 0)
       for (uint64_t s = s0; s < s0 + 2 && s < next_cap; ++s) next[s] = BsNode{0, 0, 0, 0};
@@ -286,21 +291,21 @@ __global__ void __launch_bounds__(32) bs_split_kernel(const BsNode* __restrict__
   // nodes above smem_max_m positions work in a global slot
   uint32_t* sm = smem;
   if (N.m > smem_max_m) {
-    uint64_t slot = 0;
-    if (threadIdx.x == 0) slot = atomicAdd(gslot, 1ull);
-    sm = gscr + __shfl_sync(wb::kFull, slot, 0) * gstride;
+    uint64_t gs = 0;
+    if (threadIdx.x == 0) gs = atomicAdd(gslot, 1ull);
+    sm = gscr + G::from(gs, 0) * gstride;
   }
   const uint32_t W = bs_limbs(N.m);
   uint32_t* rk = sm;
   const BsWork bw = BsWork::carve(sm + W, W, W / 2 + 3);
   const uint32_t* R = pool + N.rank_off;
   const uint32_t nr = R[0];
-  wb::copy(rk, R + 1, nr);
+  gp::copy<G>(rk, R + 1, nr);
   uint32_t t, nq, nrr;
-  bs_split<WarpOps>(N.m, N.k, rk, nr, bw, primes, nprimes, t, nq, nrr);
+  bs_split<GroupOps<G>>(N.m, N.k, rk, nr, bw, primes, nprimes, t, nq, nrr);
   const uint32_t mL = N.m >> 1;
-  bs_emit(mL, t, N.word_off, bw.q, nq, next, s0, next_cap, jobs, pool, pool_cap, scr_base, cnt);
-  bs_emit(N.m - mL, N.k - t, N.word_off + mL, bw.rr, nrr, next, s0 + 1, next_cap, jobs, pool, pool_cap, scr_base,
+  bs_emit<G>(mL, t, N.word_off, bw.q, nq, next, s0, next_cap, jobs, pool, pool_cap, scr_base, cnt);
+  bs_emit<G>(N.m - mL, N.k - t, N.word_off + mL, bw.rr, nrr, next, s0 + 1, next_cap, jobs, pool, pool_cap, scr_base,
           cnt);
 }
 
@@ -406,6 +411,7 @@ struct BsPlan {
   std::vector<BsJob> jobs;            // pairs of <= kBsTop positions
   std::vector<BsNode> roots;          // pairs above kBsTop (B1's depth 0)
   std::vector<uint64_t> node_cap;     // B1 nodes per depth (upper bounds)
+  std::vector<uint64_t> block_slots;  // ... the leading ones split by a block (above kBsBlockM)
   std::vector<uint64_t> glob_cap;     // ... of them above kBsGlobM positions
   std::vector<uint32_t> bm, bk;       // distinct class sizes C(bm, bk) of pairs above kBsWord
   std::vector<uint64_t> boff;         // their table offsets
@@ -486,6 +492,9 @@ static BsPlan bs_plan(uint64_t n) {
     while (r < pl.roots.size() && ((pl.roots[r].m + (1ull << d) - 1) >> d) > kBsTop) ++r;
     if (!r) break;
     pl.node_cap.push_back(r << d);
+    uint64_t rb = 0;
+    while (rb < r && ((pl.roots[rb].m + (1ull << d) - 1) >> d) > kBsBlockM) ++rb;
+    pl.block_slots.push_back(rb << d);
   }
   pl.n_level0 = pl.level_start.size() > 1 ? pl.level_start[1] : 0;
   while (pl.p_small_end < pl.pairs.size() && pl.pairs[pl.p_small_end].n1 + pl.pairs[pl.p_small_end].n2 <= kBsWord)
@@ -574,7 +583,7 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
       cudaStreamWaitEvent(side, ev_fork, 0);
       const size_t smemT = (size_t)(bs_limbs((uint32_t)n) + 2) * 4;
       cudaFuncSetAttribute(bs_binoms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemT);
-      bs_binoms_kernel<<<nbin, 32, smemT, side>>>(d_bm, d_bk, d_boff, d_btab, d_primes, npr);
+      bs_binoms_kernel<<<nbin, kBsGroupBlock, smemT, side>>>(d_bm, d_bk, d_boff, d_btab, d_primes, npr);
       count_launch();
       cudaEventRecord(ev_tab, side);
       chk("class sizes");
@@ -604,7 +613,9 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
     while (bs_split_smem_limbs(2 * smem_max_m + 1) * 4 <= kBsSmemBudget) smem_max_m *= 2;
     if (depths) {
       const size_t smem0 = bs_split_smem_limbs(std::min<uint32_t>(pl.max_big, smem_max_m) + 1) * 4;
-      cudaFuncSetAttribute(bs_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem0);
+      cudaFuncSetAttribute(bs_split_kernel<gp::WarpG, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem0);
+      cudaFuncSetAttribute(bs_split_kernel<gp::BlockG, kBsGroupBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem0);
       // global slots: at depth d the nodes above smem_max_m are at most
       // glob_cap[d], each of at most ceil(max_big / 2^d) + 1 positions
       uint64_t gmax = 0;
@@ -619,10 +630,20 @@ void run_balanced(int eb, void* data, uint64_t n, StreamDesc sd, unsigned long l
       const uint32_t mmax = (uint32_t)((pl.max_big + (1ull << d) - 1) >> d) + 1;
       const uint64_t stride = bs_split_smem_limbs(mmax);
       const uint64_t next_cap = d + 1 < depths ? pl.node_cap[d + 1] : 0;
-      bs_split_kernel<<<(unsigned)pl.node_cap[d], 32, bs_split_smem_limbs(std::min(mmax, smem_max_m + 1)) * 4, st>>>(
-          d_nodes + node_off[d], d_nodes + node_off[d + 1], next_cap, d_primes, npr, d_jobs, d_pool, pl.pool_cap,
-          pl.scratch_limbs, d_cnt, smem_max_m, d_gscr, stride, d_gslot ? d_gslot + d : nullptr);
-      count_launch();
+      const size_t smem = bs_split_smem_limbs(std::min(mmax, smem_max_m + 1)) * 4;
+      const uint64_t nblk = pl.block_slots[d];  // the leading slots: nodes above kBsBlockM, a block each
+      if (nblk) {
+        bs_split_kernel<gp::BlockG, kBsGroupBlock><<<(unsigned)nblk, kBsGroupBlock, smem, st>>>(
+            0, d_nodes + node_off[d], d_nodes + node_off[d + 1], next_cap, d_primes, npr, d_jobs, d_pool,
+            pl.pool_cap, pl.scratch_limbs, d_cnt, smem_max_m, d_gscr, stride, d_gslot ? d_gslot + d : nullptr);
+        count_launch();
+      }
+      if (pl.node_cap[d] > nblk) {
+        bs_split_kernel<gp::WarpG, 32><<<(unsigned)(pl.node_cap[d] - nblk), 32, smem, st>>>(
+            nblk, d_nodes + node_off[d], d_nodes + node_off[d + 1], next_cap, d_primes, npr, d_jobs, d_pool,
+            pl.pool_cap, pl.scratch_limbs, d_cnt, smem_max_m, d_gscr, stride, d_gslot ? d_gslot + d : nullptr);
+        count_launch();
+      }
       chk("splits");
     }
     bs_jobs_kernel<<<(unsigned)((pl.job_cap + 63) / 64), 64, 0, st>>>(d_jobs, d_cnt, d_pool, d_scr, d_primes, npr,
