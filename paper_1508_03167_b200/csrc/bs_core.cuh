@@ -349,12 +349,6 @@ struct BsTask {
 };
 constexpr int kBsStack = 64;
 
-// One split of _unrank_into (balanced.py:146-155): _locate_split
-// (balanced.py:98-143) of the rank rk (nr limbs) of a node of m positions
-// with k zeros, then divmod(rank - cum, right factor).  Leaves the left
-// half's zero count in t, its sub-rank in q (nq limbs) and the right half's in
-// rr (nrr limbs).  O: the serial (SerialOps) or warp-cooperative (WarpOps,
-// bs_warp.cuh) limb arithmetic; wk: working numbers of W limbs each.
 // a = a * x * y / (u * v), exact: one limb pass per side when the products
 // fit a limb
 #pragma nv_exec_check_disable
@@ -404,8 +398,8 @@ struct BsWork {
 // (balanced.py:98-143) of the rank rk (nr limbs) of a node of m positions
 // with k zeros, then divmod(rank - cum, right factor).  Leaves the left
 // half's zero count in t, its sub-rank in w.q (nq limbs) and the right half's
-// in w.rr (nrr limbs).  O: the serial (SerialOps) or warp-cooperative
-// (WarpOps, bs_warp.cuh) limb arithmetic.
+// in w.rr (nrr limbs).  O: the serial (SerialOps) or group-cooperative
+// (GroupOps<warp or block>, bs_group.cuh) limb arithmetic.
 #pragma nv_exec_check_disable
 template <class O>
 SK_HD inline void bs_split(uint32_t m, uint32_t k, const uint32_t* rk, uint32_t nr, const BsWork& w,
