@@ -29,8 +29,12 @@ def harness(tmp_path_factory):
 
 @pytest.mark.parametrize("n,state", [(33, (5, 0, 0, 0)), (64, (7, 0, 0, 0)), (100, (11, 0, 0, 0)),
                                      (257, (13, 0, 0, 0)), (1000, (17, 0, 0, 0)), (2049, (19, 0, 0, 0)),
-                                     (5000, (23, 0, 0, 0))])
+                                     (5000, (23, 0, 0, 0)), (300, "mid")])
 def test_host_stages_match_oracle(harness, n, state):
+    if state == "mid":  # a mid-stream source: 37 bits taken, 27 of a word buffered
+        s = BO.Stream((29, 0, 0, 0))
+        s.bits(37)
+        state = s.state()
     out = subprocess.run([harness, str(n), *map(str, state)], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
     lines = out.stdout.split("\n")
