@@ -386,7 +386,7 @@ static void run_job(int eb, void* data, const ArrayJob& J, unsigned long long* d
     fork_side(st, ps);
     {
       StageTimer tm(0, st);
-      if (fast_leaf) launch_leaf_decode16(J, E0, nleaves, draws, d_bits, A.alloc<uint4>(nleaves, st), st);
+      if (fast_leaf) launch_leaf_decode16(J, E0, nleaves, draws, d_bits, st);
     }
     void* cur = nullptr;
     {
@@ -465,7 +465,7 @@ static void run_job_host(int eb, void* host, const ArrayJob& J, int k, unsigned 
     }
     {
       StageTimer tm(0, st);
-      launch_leaf_decode16(J, E0, nleaves, draws, d_bits, A.alloc<uint4>(nleaves, st), st);  // needs no data
+      launch_leaf_decode16(J, E0, nleaves, draws, d_bits, st);  // needs no data
     }
     // leaves per chunk as it lands (on st), then the plans (host-blocking on
     // the side stream), then each chunk's local rounds -- rounds 1 .. c-k
@@ -839,7 +839,7 @@ static void run_single_leaf(int eb, void* data, uint64_t lo, uint64_t hi, const 
       unsigned char* scratch = A.alloc<unsigned char>(m * eb, st);
       uint16_t* lscr = A.alloc<uint16_t>(leaf_scratch_stride(m) + 8, st);
       // absolute-index kernels: shift bases so index lo lands on element 0
-      launch_leaf_decode16(J, E, 1, draws - lo, d_bits, A.alloc<uint4>(1, st), st);
+      launch_leaf_decode16(J, E, 1, draws - lo, d_bits, st);
       launch_leaf_apply(eb, J, E, 1, data, (void*)(scratch - lo * eb), draws - lo, lscr, (uint32_t)m, 1, st);
       CK(cudaMemcpyAsync((unsigned char*)data + lo * eb, scratch, m * eb, cudaMemcpyDeviceToDevice, st));
     } else {

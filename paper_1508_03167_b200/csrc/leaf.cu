@@ -2,10 +2,11 @@
 // shufflers.py:137-155, leaf tasks shufflers.py:268-278).
 //
 // Two stages:
-//  * decode (leaf_decode_lane_kernel): one lane per leaf decodes the m-1
-//    fast-dice-roller draws j_i (i = m-1 .. 1) of its substream.  This is the
-//    only serial part: draws are variable-length, so draw k's bit offset
-//    depends on the draws before it.
+//  * decode (leaf_decode_ws_kernel): one lane per leaf decodes the m-1
+//    fast-dice-roller draws j_i (i = m-1 .. 1) of its substream, helper warps
+//    feed it bits and store its draws.  This is the only serial part: draws
+//    are variable-length, so draw k's bit offset depends on the draws before
+//    it.
 //  * apply: the m-1 swaps in parallel via the successor-chain closed form
 //    (tests/decomp_model.py leaf_apply_model):
 //      N(i) = next larger step with target j_i,  H(x) = first step > x targeting x,
@@ -23,41 +24,58 @@ namespace sk {
 // debug: stop the leaf-apply pipeline after phase k (phase timing experiments)
 __device__ int g_leaf_stop = 99;
 
-// Bounds <= 65536: one FDR iteration takes k <= 16 bits, so TRIPS=16
-// iterations take at most 9 ring halves.
-constexpr int kDecodeTrips = 16;
-
 template <bool FRESH>
 __device__ __forceinline__ uint64_t leaf_word(const StreamDesc& sd, uint64_t w) {
   if (FRESH) return mix64(sd.state + (w + 1) * GOLDEN);  // fresh substream: no prefix
   return chunk(sd, w);
 }
 
-// Blocks of kDecodeBlock lanes: the decode is latency-bound with about one
-// warp per SM sub-partition, so each block's warps must land on distinct
-// schedulers (single-warp blocks were observed to share them).
+// Blocks of kDecodeBlock leaves: the decode is latency-bound with about one
+// chain warp per SM sub-partition, so each block's chain warps must land on
+// distinct schedulers.
 constexpr int kDecodeBlock = 128;
 
-// The decode: one lane per leaf, one fast-dice-roller ITERATION per loop trip
-// (lanes whose draw rejects do not stall the warp), bits served from a
-// per-lane ring of 32-bit half-words in shared memory that the warp tops up in
-// bulk (uniform mix64 work), extracted from a 4-half register window by two
-// funnel shifts.  Per trip:
-//  * the store address is a running 64-bit pointer (one 64-bit decrement per
-//    accepted draw instead of an address built from lo + i every trip);
-//  * every draw goes into the 8-draw shift register, and a full 16-byte
-//    chunk is stored when the pointer reaches a 16-byte boundary; the head
-//    chunk (it reaches past the leaf's last draw into the next leaf's draws)
-//    is stored to a per-leaf stash instead and copied out at the end, so
-//    there is no per-trip single-store path;
-//  * v << k is computed once per trip.
-template <bool FRESH>
-__global__ void __launch_bounds__(kDecodeBlock) leaf_decode_lane_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
-                                                                        uint16_t* __restrict__ draws,
-                                                                        uint4* __restrict__ stash,
-                                                                        unsigned long long* __restrict__ bits) {
-  __shared__ uint32_t ring[16][kDecodeBlock];
-  const uint32_t lane = threadIdx.x;
+// Warp-specialised decode: the same one-lane-per-leaf FDR, with everything
+// that is not on the draw's dependency chain moved to helper warps.
+//  * chain warps (threads kDecodeBlock..2*kDecodeBlock-1, one per leaf; the
+//    high warp ids, which the issue arbiter favours): per trip only the FDR
+//    iteration, the bit window shift, and one shared-memory store of an
+//    accepted draw into the lane's column of `stage`;
+//  * helper warps (threads 0..kDecodeBlock-1, helper t serves lane t):
+//    generate the lane's stream words into its column of `ring` and move
+//    accepted draws from `stage` to global memory as 16-byte chunks.
+// Both sides meet at a block barrier every T trips (an epoch): the chain
+// lanes publish their ring read position and bound there; between two
+// barriers the helpers refill ring slots the chain lanes have already passed
+// and flush draws staged before the barrier, while the chain lanes run their
+// next epoch.  Ring capacity 2T halves (an epoch reads at most T/2 + 1),
+// stage capacity 4T draws (an epoch accepts at most T; at most 7 wait for
+// their chunk).  Longer epochs cost fewer barriers but more shared memory:
+// T = 64 (128 KB, one block per SM) when the grid fits the SMs, else T = 32
+// (64 KB).  Measured alternatives: per-lane flags instead of barriers (two
+// CTA fences per epoch cost more than the barrier), precomputing the next
+// trip's batch size for both outcomes (no faster: the trip is bound by issue
+// and ALU-pipe throughput, not by the v -> k chain).
+template <int T>
+struct WsGeom {
+  static constexpr int kRing = 2 * T;
+  static constexpr int kStage = 4 * T;
+  static constexpr size_t kSmem = (size_t)kRing * kDecodeBlock * 4 + (size_t)kStage * kDecodeBlock * 2 + 2 * kDecodeBlock * 4;
+};
+
+template <bool FRESH, int T>
+__global__ void __launch_bounds__(2 * kDecodeBlock) leaf_decode_ws_kernel(ArrayJob J, ExplicitTask E,
+                                                                          uint64_t nleaves,
+                                                                          uint16_t* __restrict__ draws,
+                                                                          unsigned long long* __restrict__ bits) {
+  constexpr int kRing = WsGeom<T>::kRing, kStage = WsGeom<T>::kStage;
+  extern __shared__ uint4 ws_smem[];
+  uint32_t* const ring = reinterpret_cast<uint32_t*>(ws_smem);                        // [kRing][kDecodeBlock]
+  uint16_t* const stage = reinterpret_cast<uint16_t*>(ring + kRing * kDecodeBlock);  // [kStage][kDecodeBlock]
+  uint32_t* const ctl_rd = reinterpret_cast<uint32_t*>(stage + kStage * kDecodeBlock);
+  uint32_t* const ctl_b = ctl_rd + kDecodeBlock;
+  const bool chain = threadIdx.x >= kDecodeBlock;
+  const uint32_t lane = threadIdx.x & (kDecodeBlock - 1);
   const uint64_t g = (uint64_t)blockIdx.x * kDecodeBlock + lane;
   LeafDesc L;
   uint32_t m = 0;
@@ -67,96 +85,109 @@ __global__ void __launch_bounds__(kDecodeBlock) leaf_decode_lane_kernel(ArrayJob
   } else {
     L.lo = 0; L.hi = 0; L.array = 0; L.sd = fresh_stream(0);
   }
-  uint32_t i = m >= 2 ? m - 1 : 0;  // current step; its bound is b = i + 1
-  uint32_t b = i + 1;
+  if (m < 2) m = 1;  // no draws
   uint16_t* const dr = draws + L.lo;
-  // the head chunk: the 16-byte chunk holding draw m-1 (it may reach into the
-  // next leaf's draws); its store goes to the stash
-  uint16_t* const head = reinterpret_cast<uint16_t*>(reinterpret_cast<uintptr_t>(dr + i) & ~(uintptr_t)15);
-  uint4* const sp = stash + (g < nleaves ? g : 0);
-  uint16_t* p = dr + i;  // where draw i goes
-  uint64_t gw = 0;
-  uint32_t wr = 0;
-  if (i) {
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      uint64_t x = leaf_word<FRESH>(L.sd, gw++);
-      ring[wr & 15][lane] = (uint32_t)(x >> 32);
-      ring[(wr + 1) & 15][lane] = (uint32_t)x;
-      wr += 2;
+
+  if (chain) {
+    __syncthreads();  // the helpers' first fill
+    const uint32_t* const rcol = ring + lane;
+    uint32_t A = rcol[0], B = rcol[kDecodeBlock];
+    uint32_t rd = 2, pos = 0, v = 1, c = 0;
+    uint32_t b = m;  // bound of the current draw i = b - 1
+    // byte offset of the next accepted draw's stage slot (row * 256 + lane * 2)
+    uint32_t so = lane * 2;
+    uint8_t* const sbase = reinterpret_cast<uint8_t*>(stage);
+    for (;;) {
+#pragma unroll 8
+      for (int tr = 0; tr < T; ++tr) {
+        const uint32_t nxt = rcol[(rd & (kRing - 1)) * kDecodeBlock];  // next half, used on a crossing
+        const bool act = b > 1;
+        uint32_t k = __clz(v) - __clz(b);  // smallest k with v << k >= b
+        uint32_t vk = v << k;
+        const bool up = vk < b;
+        k += up ? 1u : 0u;
+        vk = up ? vk + vk : vk;
+        const uint32_t x = __funnelshift_l(B, A, pos);
+        const uint32_t cc = __funnelshift_l(x, c, k);  // (c << k) | top k bits of x
+        const bool acc = act && cc < b;
+        if (acc) *reinterpret_cast<uint16_t*>(sbase + so) = (uint16_t)cc;
+        so = acc ? ((so + 2 * kDecodeBlock) & (kStage * kDecodeBlock * 2 - 1)) : so;
+        c = acc ? 0u : cc - b;
+        v = acc ? 1u : vk - b;
+        b -= acc ? 1u : 0u;
+        pos += act ? k : 0u;
+        const bool cross = pos >= 32;
+        pos = cross ? pos - 32 : pos;
+        A = cross ? B : A;
+        B = cross ? nxt : B;
+        rd += cross ? 1u : 0u;
+      }
+      ctl_rd[lane] = rd;
+      ctl_b[lane] = b;
+      if (!__syncthreads_or(b > 1)) break;
     }
-  }
-  uint32_t A = ring[0][lane], B = ring[1][lane], C = ring[2][lane], D = ring[3][lane];
-  uint32_t rd = 4;
-  uint32_t pos = 0;
-  uint32_t v = 1, c = 0;
-  uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;  // last 8 packed draws, newest in w0's low half
-  while (__any_sync(0xffffffffu, i != 0)) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (i != 0 && wr - rd <= 14) {
-        uint64_t x = leaf_word<FRESH>(L.sd, gw++);
-        ring[wr & 15][lane] = (uint32_t)(x >> 32);
-        ring[(wr + 1) & 15][lane] = (uint32_t)x;
+    if (m >= 2) atomicAdd(&bits[L.array], 32ull * (rd - 2) + pos);  // bits consumed = halves passed + pos
+  } else {
+    uint64_t gw = 0;   // next stream word
+    uint32_t wr = 0;   // next ring half to fill
+    uint32_t fl = 0;   // draws flushed (draw index m-1-fl is the next)
+    auto fill = [&](uint32_t upto) {  // halves [wr, upto)
+      while (wr + 2 <= upto) {
+        const uint64_t w = leaf_word<FRESH>(L.sd, gw++);
+        ring[(wr & (kRing - 1)) * kDecodeBlock + lane] = (uint32_t)(w >> 32);
+        ring[((wr + 1) & (kRing - 1)) * kDecodeBlock + lane] = (uint32_t)w;
         wr += 2;
       }
-    }
-#pragma unroll 4
-    for (int tr = 0; tr < kDecodeTrips; ++tr) {
-      const bool act = i != 0;
-      uint32_t k = __clz(v) - __clz(b);  // smallest k with v << k >= b
-      uint32_t vk = v << k;
-      const bool up = vk < b;
-      k += up ? 1u : 0u;
-      vk = up ? vk + vk : vk;
-      const uint32_t x = __funnelshift_l(B, A, pos);
-      const uint32_t cc = __funnelshift_l(x, c, k);  // (c << k) | top k bits of x
-      const bool acc = act && cc < b;
-      if (acc) {
-        w3 = __byte_perm(w2, w3, 0x5432);
-        w2 = __byte_perm(w1, w2, 0x5432);
-        w1 = __byte_perm(w0, w1, 0x5432);
-        w0 = __byte_perm(cc, w0, 0x5410);
+    };
+    auto flush = [&](uint32_t cnt) {  // draws accepted: t < cnt is draw m-1-t
+      while (fl < cnt) {
+        const uint32_t itop = m - 1 - fl;
+        uint16_t* const p = dr + itop;
+        if (((reinterpret_cast<uintptr_t>(p) >> 1) & 7) == 7 && itop >= 8) {
+          if (cnt - fl < 8) break;
+          uint32_t w[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t lo16 = stage[((fl + 7 - 2 * q) & (kStage - 1)) * kDecodeBlock + lane];
+            const uint32_t hi16 = stage[((fl + 6 - 2 * q) & (kStage - 1)) * kDecodeBlock + lane];
+            w[q] = lo16 | (hi16 << 16);
+          }
+          *reinterpret_cast<uint4*>(p - 7) = make_uint4(w[0], w[1], w[2], w[3]);
+          fl += 8;
+        } else {
+          *p = stage[(fl & (kStage - 1)) * kDecodeBlock + lane];
+          fl += 1;
+        }
       }
-      const bool fl = acc && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
-      uint4* const dst = p == head ? sp : reinterpret_cast<uint4*>(p);
-      asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.global.v4.u32 [%1], {%2, %3, %4, %5};\n}" ::"r"(
-                       fl ? 1u : 0u),
-                   "l"(dst), "r"(w0), "r"(w1), "r"(w2), "r"(w3));
-      p -= acc ? 1 : 0;
-      c = acc ? 0u : cc - b;
-      v = acc ? 1u : vk - b;
-      i -= acc ? 1u : 0u;
-      b -= acc ? 1u : 0u;
-      pos += act ? k : 0u;
-      const bool cross = pos >= 32;
-      const uint32_t nxt = ring[rd & 15][lane];
-      pos = cross ? pos - 32 : pos;
-      A = cross ? B : A;
-      B = cross ? C : B;
-      C = cross ? D : C;
-      D = cross ? nxt : D;
-      rd += cross ? 1u : 0u;
+    };
+    if (m >= 2) fill(kRing);
+    __syncthreads();
+    for (;;) {
+      // the chain lanes run an epoch; meanwhile flush and top up from the
+      // positions published at the previous barrier
+      const bool more = __syncthreads_or(0);
+      const uint32_t rd = ctl_rd[lane], bb = ctl_b[lane];
+      if (m >= 2) {
+        flush(m - bb);
+        if (more) fill(rd + kRing);
+      }
+      if (!more) break;
     }
   }
-  if (m >= 2) {
-    // (a) the chunk holding draw 1 when it does not start at draw 1 is never
-    //     flushed: its draws 1 .. are the newest in the shift register
-    const uint32_t off1 = (uint32_t)((L.lo + 1) & 7);  // slot of draw 1 in its chunk
-    if (off1 != 0) {
-      const uint32_t wv[4] = {w0, w1, w2, w3};
-      const uint32_t pend = min(8u - off1, m - 1);  // draws 1 .. 8-off1 share draw 1's chunk
-      for (uint32_t k = 0; k < pend; ++k) dr[1 + k] = (uint16_t)(wv[k >> 1] >> (16 * (k & 1)));
-    }
-    // (b) the head chunk, when it was flushed (it starts at a draw >= 1): its
-    //     draws up to m-1 from the stash
-    const int64_t hd = head - dr;
-    if (hd >= 1) {
-      const uint16_t* const sv = reinterpret_cast<const uint16_t*>(sp);
-      for (int64_t d = hd; d < (int64_t)m; ++d) dr[d] = sv[d - hd];
-    }
-    atomicAdd(&bits[L.array], 32ull * (rd - 4) + pos);  // bits consumed = halves passed + pos
+}
+
+template <int T>
+static void launch_ws(bool fresh, unsigned blocks, const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves,
+                      uint16_t* draws, unsigned long long* bits, cudaStream_t st) {
+  constexpr size_t smem = WsGeom<T>::kSmem;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(leaf_decode_ws_kernel<true, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(leaf_decode_ws_kernel<false, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
   }
+  if (fresh) leaf_decode_ws_kernel<true, T><<<blocks, 2 * kDecodeBlock, smem, st>>>(J, E, nleaves, draws, bits);
+  else leaf_decode_ws_kernel<false, T><<<blocks, 2 * kDecodeBlock, smem, st>>>(J, E, nleaves, draws, bits);
 }
 
 // Warp-segmented exclusive scan over `m` 16-bit counters packed in smem.
@@ -852,12 +883,14 @@ void debug_set_leaf_l2pol(int v) { g_leaf_l2pol_host = v; }
 void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int)); }
 
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
-                          unsigned long long* bits, uint4* stash, cudaStream_t st) {
+                          unsigned long long* bits, cudaStream_t st) {
   if (!nleaves) return;
-  unsigned blocks = (unsigned)((nleaves + kDecodeBlock - 1) / kDecodeBlock);
+  const unsigned blocks = (unsigned)((nleaves + kDecodeBlock - 1) / kDecodeBlock);
   const bool fresh = !(E.active && E.sd.plen != 0);
-  if (fresh) leaf_decode_lane_kernel<true><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, stash, bits);
-  else leaf_decode_lane_kernel<false><<<blocks, kDecodeBlock, 0, st>>>(J, E, nleaves, draws, stash, bits);
+  // T = 64 needs one 128 KB block per SM; with more blocks than SMs the
+  // 64 KB T = 32 blocks run two or three per SM
+  if (blocks <= (unsigned)num_sms()) launch_ws<64>(fresh, blocks, J, E, nleaves, draws, bits, st);
+  else launch_ws<32>(fresh, blocks, J, E, nleaves, draws, bits, st);
   count_launch();
 }
 

@@ -10,9 +10,9 @@ void count_launch();          // engine-wide launch counter (bench "gpu_launches
 int num_sms();
 
 // leaf.cu
-// stash: nleaves x 16 B of scratch (each leaf's head chunk of draws)
+// draws[lo + i] = j_i (uint16) for every leaf [lo, lo + m) with m <= 65536
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
-                          unsigned long long* bits, uint4* stash, cudaStream_t st);
+                          unsigned long long* bits, cudaStream_t st);
 uint32_t leaf_apply_grid(uint64_t nleaves, uint32_t mmax, int num_sms, int eb = 8);
 // per-CTA leaf-apply scratch (uint16 elements)
 __host__ __device__ inline uint64_t leaf_scratch_stride(uint64_t mmax) { return 3 * ((mmax + 15) & ~15ULL) + 16; }

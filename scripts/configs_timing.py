@@ -36,6 +36,12 @@ def line(name, ms, n, **kw):
           flush=True)
 
 
+# SK_KNOBS="key=value,..." sets internal performance knobs (sk_debug_set) for A/B runs
+for kv in filter(None, os.environ.get("SK_KNOBS", "").split(",")):
+    from paper_1508_03167_b200 import _lib
+    k, v = kv.split("=")
+    assert _lib.load().sk_debug_set(int(k), int(v)) == 0, kv
+
 g = torch.Generator(device="cuda").manual_seed(7)
 # 1. identity 2^20, default cutoff (bit-exact vs the reference golden in the tests)
 x = torch.arange(1 << 20, dtype=torch.int32, device="cuda")
