@@ -897,6 +897,7 @@ int sk_debug_set(int key, int value) {
   if (key == 4) { debug_set_tree_force_direct(value); return 0; }
   if (key == 6) { debug_set_leaf_fallback(value); return 0; }
   if (key == 7) { debug_set_leaf_l2pol(value); return 0; }
+  if (key == 8) { debug_set_spec_decode_max(value); return 0; }
   return -1;
 }
 const char* sk_last_error(void) { return g_err.c_str(); }

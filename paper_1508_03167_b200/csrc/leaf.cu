@@ -190,6 +190,170 @@ static void launch_ws(bool fresh, unsigned blocks, const ArrayJob& J, const Expl
   else leaf_decode_ws_kernel<false, T><<<blocks, 2 * kDecodeBlock, smem, st>>>(J, E, nleaves, draws, bits);
 }
 
+// Warp-per-leaf speculative decode, for jobs with few leaves (the
+// lane-per-leaf kernel above then leaves the GPU idle for the ~3.8 ms its
+// per-lane chain of 65 535 draws takes).  Bit-identical to the serial loop
+// (_kernels.py:64-93); what is speculated is only WHERE each draw starts.
+//
+// A batch is up to 32 consecutive steps s = i - lane whose first FDR
+// iteration takes the same K bits and whose second iteration (after one
+// rejection: v' = 2^K - b, c' = c - b) takes the same k1 bits -- both are
+// functions of the bound alone, constant over long runs of steps.  Lane l's
+// draw then starts at o + l*K + h*k1 when exactly h earlier draws of the
+// batch were rejected once and the rest accepted at once.  Every lane
+// evaluates its draw (first iteration and, on a rejection, the second) under
+// each hypothesis h < kSpecH from one 96-bit window of the stream; six
+// ballots per outcome class then resolve the batch without touching memory:
+// the lanes up to the first rejection under h = 0 are final, that lane's
+// second iteration accepts (the next lanes continue under h = 1) or rejects
+// again (it finishes its draw with the serial loop and the batch ends there).
+// A batch also ends when the hypotheses run out.  About 10 draws per batch
+// at full leaves (model: tests/decomp_model.py
+// spec_decode_model, checked against the serial loop on the CPU).
+constexpr int kSpecWarps = 4;
+constexpr uint32_t kSpecRing = 128;  // halves: 64 stream words per warp
+constexpr uint32_t kSpecAhead = 1536;  // bits kept generated past the batch start
+constexpr int kSpecH = 6;
+static uint64_t g_spec_decode_max = 2048;  // jobs with at most this many leaves take the warp-per-leaf decode
+
+template <bool FRESH>
+__global__ void __launch_bounds__(32 * kSpecWarps)
+    leaf_decode_spec_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves, uint16_t* __restrict__ draws,
+                            unsigned long long* __restrict__ bits) {
+  __shared__ uint32_t ring_all[kSpecWarps][kSpecRing];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t g = (uint64_t)blockIdx.x * kSpecWarps + wid;
+  if (g >= nleaves) return;  // whole warp
+  uint32_t* const ring = ring_all[wid];
+  const LeafDesc L = leaf_desc(J, E, g);
+  const uint32_t m = (uint32_t)(L.hi - L.lo);
+  if (m < 2) return;
+  uint16_t* const dr = draws + L.lo;
+  uint32_t wgen = 0;  // stream words [wgen - 64, wgen) are in the ring
+  auto refill = [&]() {
+    const uint64_t x = leaf_word<FRESH>(L.sd, (uint64_t)wgen + lane);
+    const uint32_t h = ((wgen + lane) * 2) & (kSpecRing - 1);
+    ring[h] = (uint32_t)(x >> 32);
+    ring[h + 1] = (uint32_t)x;
+    wgen += 32;
+    __syncwarp();
+  };
+  refill();
+  refill();
+  uint32_t o = 0;      // bit offset of the batch's first draw
+  uint32_t i = m - 1;  // the batch's first step (bound i + 1)
+  while (i >= 1) {
+    while (o + kSpecAhead > 64 * wgen) refill();
+    const uint32_t n = min(32u, i);
+    const uint32_t s = lane < n ? i - lane : 1u, b = s + 1;
+    const uint32_t K = 32 - __clz(i);
+    const uint32_t Kl = 32 - __clz(s);
+    const uint32_t v1 = (1u << Kl) - b;  // v after one rejection; 0 when b is a power of two (never rejects)
+    uint32_t k1l = __clz(v1) - __clz(b);
+    k1l += ((v1 << (k1l & 31)) < b) ? 1u : 0u;
+    uint32_t k1 = __shfl_sync(0xffffffffu, k1l, 0);
+    uint32_t neff;
+    if ((i & (i + 1)) == 0) {  // the batch's first bound is a power of two: that step alone
+      neff = 1;
+      k1 = 1;
+    } else {
+      const uint32_t same = __ballot_sync(0xffffffffu, lane < n && Kl == K && k1l == k1);
+      neff = same == 0xffffffffu ? 32u : (uint32_t)__ffs(~same) - 1;
+    }
+    const bool live = lane < neff;
+    // the 96 stream bits from this lane's h = 0 start
+    const uint32_t off0 = o + lane * K;
+    const uint32_t hw = off0 >> 5, a = off0 & 31;
+    const uint32_t w0 = ring[hw & (kSpecRing - 1)], w1 = ring[(hw + 1) & (kSpecRing - 1)];
+    const uint32_t w2 = ring[(hw + 2) & (kSpecRing - 1)], w3 = ring[(hw + 3) & (kSpecRing - 1)];
+    const uint32_t X0 = __funnelshift_l(w1, w0, a), X1 = __funnelshift_l(w2, w1, a), X2 = __funnelshift_l(w3, w2, a);
+    uint32_t val[kSpecH], R[kSpecH], D[kSpecH];
+#pragma unroll
+    for (int h = 0; h < kSpecH; ++h) {
+      const uint32_t sh = h * k1;  // <= 64 for the hypotheses that are used
+      const uint32_t wi = sh >> 5;
+      const uint32_t hiw = wi == 0 ? X0 : (wi == 1 ? X1 : X2);
+      const uint32_t low = wi == 0 ? X1 : X2;
+      const uint32_t Y = __funnelshift_l(low, hiw, sh);
+      const uint32_t c = Y >> (32 - K);
+      const bool r1 = live && c >= b;
+      const uint32_t c2 = ((c - b) << k1) | ((Y << K) >> (32 - k1));
+      const bool r2 = r1 && c2 >= b;
+      val[h] = r1 ? c2 : c;
+      R[h] = __ballot_sync(0xffffffffu, r1);
+      D[h] = __ballot_sync(0xffffffffu, r2);
+    }
+    // resolve: hypothesis h covers the lanes from `start` to its first rejection
+    uint32_t start = 0, consumed = neff, extra = 0, myval = 0;
+    int serial_lane = -1, hs = 0;
+    bool done = false;
+#pragma unroll
+    for (int h = 0; h < kSpecH; ++h) {
+      if (!done) {
+        if (h * k1 > 64) {  // not evaluable from the window
+          consumed = start;
+          extra = h * k1;
+          done = true;
+        } else {
+          const uint32_t rm = R[h] & (0xffffffffu << start);
+          const uint32_t f = rm ? (uint32_t)__ffs(rm) - 1 : neff;
+          if (lane >= start && lane <= f) myval = val[h];
+          if (!rm) {
+            extra = h * k1;
+            done = true;
+          } else if ((D[h] >> f) & 1) {
+            serial_lane = (int)f;
+            hs = h;
+            consumed = f + 1;
+            done = true;
+          } else {
+            start = f + 1;
+            if (start == neff) {
+              extra = (h + 1) * k1;
+              done = true;
+            }
+          }
+        }
+      }
+    }
+    if (!done) {  // every hypothesis used up by single rejections
+      consumed = start;
+      extra = kSpecH * k1;
+    }
+    if (serial_lane >= 0) {
+      uint32_t e = 0;
+      if ((int)lane == serial_lane) {  // the rest of this draw's FDR loop (_kernels.py:71-82)
+        uint32_t v = (v1 << k1) - b, cc = myval - b;
+        uint32_t p = off0 + hs * k1 + K + k1;
+        for (;;) {
+          uint32_t k = __clz(v) - __clz(b);
+          k += ((v << k) < b) ? 1u : 0u;
+          uint32_t x;
+          if (p + 32 > 64 * wgen) {
+            x = (uint32_t)(bits64_at(L.sd, p) >> 32);
+          } else {
+            const uint32_t q = p >> 5;
+            x = __funnelshift_l(ring[(q + 1) & (kSpecRing - 1)], ring[q & (kSpecRing - 1)], p);
+          }
+          cc = (cc << k) | (x >> (32 - k));
+          v <<= k;
+          p += k;
+          if (cc < b) break;
+          cc -= b;
+          v -= b;
+        }
+        myval = cc;
+        e = p - off0 - K;
+      }
+      extra = __shfl_sync(0xffffffffu, e, serial_lane);
+    }
+    if (lane < consumed) dr[s] = (uint16_t)myval;
+    o += consumed * K + extra;
+    i -= consumed;
+  }
+  if (lane == 0) atomicAdd(&bits[L.array], (unsigned long long)o);
+}
+
 // Warp-segmented exclusive scan over `m` 16-bit counters packed in smem.
 // Each warp owns [w*S, (w+1)*S); lanes walk it 32 entries per round.
 __device__ __forceinline__ void scan_counts16(uint16_t* c16, uint32_t m, uint32_t* warp_tot) {
@@ -881,12 +1045,20 @@ __global__ void leaf_serial_kernel(ArrayJob J, ExplicitTask E, uint64_t nleaves,
 void debug_set_leaf_fallback(int v) { cudaMemcpyToSymbol(g_leaf_force_fallback, &v, sizeof(int)); }
 void debug_set_leaf_l2pol(int v) { g_leaf_l2pol_host = v; }
 void debug_set_leaf_stop(int v) { cudaMemcpyToSymbol(g_leaf_stop, &v, sizeof(int)); }
+void debug_set_spec_decode_max(int v) { g_spec_decode_max = v < 0 ? 0 : (uint64_t)v; }
 
 void launch_leaf_decode16(const ArrayJob& J, const ExplicitTask& E, uint64_t nleaves, uint16_t* draws,
                           unsigned long long* bits, cudaStream_t st) {
   if (!nleaves) return;
   const unsigned blocks = (unsigned)((nleaves + kDecodeBlock - 1) / kDecodeBlock);
   const bool fresh = !(E.active && E.sd.plen != 0);
+  if (nleaves <= g_spec_decode_max) {
+    const unsigned wb = (unsigned)((nleaves + kSpecWarps - 1) / kSpecWarps);
+    if (fresh) leaf_decode_spec_kernel<true><<<wb, 32 * kSpecWarps, 0, st>>>(J, E, nleaves, draws, bits);
+    else leaf_decode_spec_kernel<false><<<wb, 32 * kSpecWarps, 0, st>>>(J, E, nleaves, draws, bits);
+    count_launch();
+    return;
+  }
   // T = 64 needs one 128 KB block per SM; with more blocks than SMs the
   // 64 KB T = 32 blocks run two or three per SM
   if (blocks <= (unsigned)num_sms()) launch_ws<64>(fresh, blocks, J, E, nleaves, draws, bits, st);

@@ -23,6 +23,7 @@ void launch_leaf_serial(int eb, const ArrayJob& J, const ExplicitTask& E, uint64
                         unsigned long long* bits, cudaStream_t st);
 
 void debug_set_leaf_stop(int v);
+void debug_set_spec_decode_max(int v);
 void debug_set_leaf_fallback(int v);
 void debug_set_leaf_l2pol(int v);
 void debug_set_tree_force_direct(int v);

@@ -10,6 +10,8 @@ are validated on the CPU before any GPU run:
   segment/window chain (kernel: csrc/merge.cu, merge_level_kernel).
 * tail_plan_model:   merge phase-2 insertion as a (dst, src) list over the
   touched set (kernel: csrc/plan.cu, tail_plan_kernel).
+* spec_decode_model: the leaf's FDR draws decoded in batches of up to 32 steps
+  under start-offset hypotheses (kernel: csrc/leaf.cu, leaf_decode_spec_kernel).
 """
 from __future__ import annotations
 
@@ -247,3 +249,94 @@ def tail_apply(p1, plan):
     for d, s in plan:
         out[d] = p1[s]
     return out
+
+
+# ------------------------------------------------- speculative leaf decode ----
+def _bits_at(bits, p, k):
+    v = 0
+    for t in range(k):
+        v = (v << 1) | int(bits[p + t])
+    return v
+
+
+def _k_of(v, b):
+    k = 0
+    while (v << k) < b:
+        k += 1
+    return k
+
+
+def spec_decode_model(m, bits, H=6, lanes=32):
+    """Draws j_i (i = m-1 .. 1, bound i+1) of a leaf from `bits`, decoded as
+    leaf_decode_spec_kernel does: a batch = up to `lanes` consecutive steps with
+    the same first-iteration width K and the same second-iteration width k1;
+    lane l evaluates its draw at o + l*K + h*k1 for h < H; the first rejection
+    under hypothesis h hands the later lanes to h+1, a double rejection is
+    finished serially and ends the batch.  Returns (draws, bits consumed,
+    batches)."""
+    draws = [0] * max(m, 1)
+    o, i, batches = 0, m - 1, 0
+    while i >= 1:
+        n = min(lanes, i)
+        K = i.bit_length()
+        if (i & (i + 1)) == 0:          # bound a power of two: never rejects, alone
+            neff, k1 = 1, 1
+        else:
+            k1 = _k_of((1 << K) - (i + 1), i + 1)
+            neff = 0
+            while neff < n:
+                s = i - neff
+                if s.bit_length() != K or (1 << K) == s + 1 or _k_of((1 << K) - (s + 1), s + 1) != k1:
+                    break
+                neff += 1
+        ev = []
+        for h in range(H):
+            row = []
+            for l in range(neff):
+                if h * k1 > 64:
+                    row.append(None)
+                    continue
+                b = i - l + 1
+                off = o + l * K + h * k1
+                c = _bits_at(bits, off, K)
+                if c >= b:
+                    c2 = ((c - b) << k1) | _bits_at(bits, off + K, k1)
+                    row.append((True, c2 >= b, c2))
+                else:
+                    row.append((False, False, c))
+            ev.append(row)
+        h, start = 0, 0
+        while True:
+            if h == H or h * k1 > 64:
+                consumed, extra = start, h * k1
+                break
+            f = next((l for l in range(start, neff) if ev[h][l][0]), None)
+            for l in range(start, neff if f is None else f + 1):
+                draws[i - l] = ev[h][l][2]
+            if f is None:
+                consumed, extra = neff, h * k1
+                break
+            if ev[h][f][1]:               # rejected twice: finish serially, end of batch
+                b = i - f + 1
+                c, v = ev[h][f][2] - b, (((1 << K) - b) << k1) - b
+                p = o + f * K + h * k1 + K + k1
+                while True:
+                    k = _k_of(v, b)
+                    c = (c << k) | _bits_at(bits, p, k)
+                    p += k
+                    v <<= k
+                    if c < b:
+                        break
+                    c -= b
+                    v -= b
+                draws[i - f] = c
+                consumed, extra = f + 1, p - (o + (f + 1) * K)
+                break
+            h, start = h + 1, f + 1
+            if start == neff:
+                consumed, extra = neff, h * k1
+                break
+        batches += 1
+        o += consumed * K + extra
+        i -= consumed
+    return draws, o, batches

@@ -5,8 +5,8 @@ import random
 import numpy as np
 import pytest
 
-from decomp_model import (fy_serial, leaf_apply_model, merge_phase1_model, merge_serial, stream_bits,
-                          tail_apply, tail_plan_model)
+from decomp_model import (BitCursor, fy_serial, leaf_apply_model, merge_phase1_model, merge_serial,
+                          spec_decode_model, stream_bits, tail_apply, tail_plan_model)
 from oracle import oracle as O
 
 
@@ -57,3 +57,31 @@ def test_merge_model_matches_oracle_merge():
         st = O.state_vec(sseed, 0, 0, 0)
         O.merge(a, 0, n1, n1 + n2, st)
         assert a.tolist() == out and int(st[3]) == used
+
+
+@pytest.mark.parametrize("m", [2, 3, 5, 17, 64, 100, 1000, 4097, 20000])
+def test_spec_decode_form(m):
+    # the batched start-offset speculation of leaf_decode_spec_kernel equals the serial FDR loop
+    for seed in (0, 1):
+        bits = stream_bits(O.substream_seed(seed, m), 24 * m + 4096)
+        cur = BitCursor(bits)
+        want = [0] * m
+        for i in range(m - 1, 0, -1):
+            want[i] = cur.fdr(i + 1)
+        got, used, batches = spec_decode_model(m, bits)
+        assert got == want and used == cur.pos
+        for H, lanes in ((1, 32), (2, 8), (6, 4)):
+            got, used, _ = spec_decode_model(m, bits, H=H, lanes=lanes)
+            assert got == want and used == cur.pos
+
+
+def test_spec_decode_form_on_oracle_draws():
+    m = 3000
+    st = O.state_vec(O.substream_seed(7, 3), 0, 0, 0)
+    want = [0] * m
+    for i in range(m - 1, 0, -1):
+        want[i] = O.fdr(st, i + 1)
+    bits = stream_bits(O.substream_seed(7, 3), 24 * m)
+    got, _, batches = spec_decode_model(m, bits)
+    assert got == want
+    assert batches < m / 4     # several draws per batch
