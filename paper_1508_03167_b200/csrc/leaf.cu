@@ -195,26 +195,26 @@ static void launch_ws(bool fresh, unsigned blocks, const ArrayJob& J, const Expl
 // per-lane chain of 65 535 draws takes).  Bit-identical to the serial loop
 // (_kernels.py:64-93); what is speculated is only WHERE each draw starts.
 //
-// A batch is up to 32 consecutive steps s = i - lane whose first FDR
-// iteration takes the same K bits and whose second iteration (after one
-// rejection: v' = 2^K - b, c' = c - b) takes the same k1 bits -- both are
-// functions of the bound alone, constant over long runs of steps.  Lane l's
-// draw then starts at o + l*K + h*k1 when exactly h earlier draws of the
-// batch were rejected once and the rest accepted at once.  Every lane
-// evaluates its draw (first iteration and, on a rejection, the second) under
-// each hypothesis h < kSpecH from one 96-bit window of the stream; six
-// ballots per outcome class then resolve the batch without touching memory:
-// the lanes up to the first rejection under h = 0 are final, that lane's
-// second iteration accepts (the next lanes continue under h = 1) or rejects
-// again (it finishes its draw with the serial loop and the batch ends there).
-// A batch also ends when the hypotheses run out.  About 10 draws per batch
-// at full leaves (model: tests/decomp_model.py
-// spec_decode_model, checked against the serial loop on the CPU).
+// A batch is up to 16 consecutive steps s = i - d whose first FDR iteration
+// takes the same K bits and whose second iteration (after one rejection:
+// v' = 2^K - b, c' = c - b) takes the same k1 bits -- both are functions of
+// the bound alone, constant over long runs of steps (the run's lower end in
+// closed form: b > 2^(K+k1-1) / (2^(k1-1) + 1)).  Draw d of the batch then
+// starts at o + d*K + h*k1 when exactly h earlier draws of the batch were
+// rejected once and the rest accepted at once.  Lane 2d + h evaluates draw d
+// under hypothesis h in {0, 1}: the first iteration and, on a rejection, the
+// second and the third.  Three ballots (rejected once / twice / three times)
+// resolve the batch without touching memory: the draws up to the first
+// rejection under h = 0 are final; if that draw's second iteration accepts,
+// the following draws are read under h = 1 up to the next rejection, which
+// ends the batch; a draw rejected twice ends the batch there (its lane knows
+// the k2 bits of its third iteration; only after a third rejection does it
+// run the serial loop).  About 6 draws per batch at full leaves (model:
+// tests/decomp_model.py spec_decode_model, checked against the serial loop).
 constexpr int kSpecWarps = 4;
-constexpr uint32_t kSpecRing = 128;  // halves: 64 stream words per warp
+constexpr uint32_t kSpecRing = 128;    // halves: 64 stream words per warp
 constexpr uint32_t kSpecAhead = 1536;  // bits kept generated past the batch start
-constexpr int kSpecH = 6;
-static uint64_t g_spec_decode_max = 2048;  // jobs with at most this many leaves take the warp-per-leaf decode
+static uint64_t g_spec_decode_max = 1024;  // jobs with at most this many leaves take the warp-per-leaf decode (measured: 2.48 ms per leaf up to ~600 leaves, 2.95 ms at 1024, 4.0 ms at 2048 against 3.8 ms for a lane per leaf)
 
 template <bool FRESH>
 __global__ void __launch_bounds__(32 * kSpecWarps)
@@ -240,91 +240,80 @@ __global__ void __launch_bounds__(32 * kSpecWarps)
   };
   refill();
   refill();
-  uint32_t o = 0;      // bit offset of the batch's first draw
-  uint32_t i = m - 1;  // the batch's first step (bound i + 1)
+  const uint32_t d = lane >> 1, h = lane & 1;
+  const uint32_t lanebit = 1u << lane;
+  uint32_t o = 0;       // bit offset of the batch's first draw
+  uint32_t i = m - 1;   // the batch's first step (bound i + 1)
+  uint32_t run_lo = m;  // steps [run_lo, i] share (K, k1); recomputed when i drops below it
+  uint32_t K = 0, k1 = 1;
+  bool pow2 = false;  // the run is one step whose bound is a power of two
   while (i >= 1) {
-    while (o + kSpecAhead > 64 * wgen) refill();
-    const uint32_t n = min(32u, i);
-    const uint32_t s = lane < n ? i - lane : 1u, b = s + 1;
-    const uint32_t K = 32 - __clz(i);
-    const uint32_t Kl = 32 - __clz(s);
-    const uint32_t v1 = (1u << Kl) - b;  // v after one rejection; 0 when b is a power of two (never rejects)
-    uint32_t k1l = __clz(v1) - __clz(b);
-    k1l += ((v1 << (k1l & 31)) < b) ? 1u : 0u;
-    uint32_t k1 = __shfl_sync(0xffffffffu, k1l, 0);
-    uint32_t neff;
-    if ((i & (i + 1)) == 0) {  // the batch's first bound is a power of two: that step alone
-      neff = 1;
-      k1 = 1;
-    } else {
-      const uint32_t same = __ballot_sync(0xffffffffu, lane < n && Kl == K && k1l == k1);
-      neff = same == 0xffffffffu ? 32u : (uint32_t)__ffs(~same) - 1;
-    }
-    const bool live = lane < neff;
-    // the 96 stream bits from this lane's h = 0 start
-    const uint32_t off0 = o + lane * K;
-    const uint32_t hw = off0 >> 5, a = off0 & 31;
-    const uint32_t w0 = ring[hw & (kSpecRing - 1)], w1 = ring[(hw + 1) & (kSpecRing - 1)];
-    const uint32_t w2 = ring[(hw + 2) & (kSpecRing - 1)], w3 = ring[(hw + 3) & (kSpecRing - 1)];
-    const uint32_t X0 = __funnelshift_l(w1, w0, a), X1 = __funnelshift_l(w2, w1, a), X2 = __funnelshift_l(w3, w2, a);
-    uint32_t val[kSpecH], R[kSpecH], D[kSpecH];
-#pragma unroll
-    for (int h = 0; h < kSpecH; ++h) {
-      const uint32_t sh = h * k1;  // <= 64 for the hypotheses that are used
-      const uint32_t wi = sh >> 5;
-      const uint32_t hiw = wi == 0 ? X0 : (wi == 1 ? X1 : X2);
-      const uint32_t low = wi == 0 ? X1 : X2;
-      const uint32_t Y = __funnelshift_l(low, hiw, sh);
-      const uint32_t c = Y >> (32 - K);
-      const bool r1 = live && c >= b;
-      const uint32_t c2 = ((c - b) << k1) | ((Y << K) >> (32 - k1));
-      const bool r2 = r1 && c2 >= b;
-      val[h] = r1 ? c2 : c;
-      R[h] = __ballot_sync(0xffffffffu, r1);
-      D[h] = __ballot_sync(0xffffffffu, r2);
-    }
-    // resolve: hypothesis h covers the lanes from `start` to its first rejection
-    uint32_t start = 0, consumed = neff, extra = 0, myval = 0;
-    int serial_lane = -1, hs = 0;
-    bool done = false;
-#pragma unroll
-    for (int h = 0; h < kSpecH; ++h) {
-      if (!done) {
-        if (h * k1 > 64) {  // not evaluable from the window
-          consumed = start;
-          extra = h * k1;
-          done = true;
-        } else {
-          const uint32_t rm = R[h] & (0xffffffffu << start);
-          const uint32_t f = rm ? (uint32_t)__ffs(rm) - 1 : neff;
-          if (lane >= start && lane <= f) myval = val[h];
-          if (!rm) {
-            extra = h * k1;
-            done = true;
-          } else if ((D[h] >> f) & 1) {
-            serial_lane = (int)f;
-            hs = h;
-            consumed = f + 1;
-            done = true;
-          } else {
-            start = f + 1;
-            if (start == neff) {
-              extra = (h + 1) * k1;
-              done = true;
-            }
-          }
-        }
+    if (i < run_lo) {  // next run of steps with one (K, k1)
+      K = 32 - __clz(i);
+      const uint32_t bt = i + 1, vt = (1u << K) - bt;
+      pow2 = vt == 0;
+      if (pow2) {  // bound a power of two: never rejects, a run of its own
+        k1 = 1;
+        run_lo = i;
+      } else {
+        k1 = __clz(vt) - __clz(bt);
+        k1 += ((vt << k1) < bt) ? 1u : 0u;
+        run_lo = (1u << (K + k1 - 1)) / ((1u << (k1 - 1)) + 1u);  // smallest bound of the run, minus one
       }
     }
-    if (!done) {  // every hypothesis used up by single rejections
-      consumed = start;
-      extra = kSpecH * k1;
-    }
-    if (serial_lane >= 0) {
-      uint32_t e = 0;
-      if ((int)lane == serial_lane) {  // the rest of this draw's FDR loop (_kernels.py:71-82)
-        uint32_t v = (v1 << k1) - b, cc = myval - b;
-        uint32_t p = off0 + hs * k1 + K + k1;
+    while (o + kSpecAhead > 64 * wgen) refill();
+    const uint32_t n = min(16u, i - run_lo + 1);
+    const bool live = d < n;
+    const uint32_t s = live ? i - d : 1u, b = s + 1;
+    const uint32_t lm = 0xffffffffu >> (32 - 2 * n);  // lanes of the batch's draws
+    // rejection tests on the left-aligned window: c >= b  <=>  Y >= b << (32 - K), and with
+    // Z = Y - (b << (32 - K)) the second iteration's c2 = Z >> (32 - K - k1)
+    const uint32_t sh2 = 32 - K - k1;
+    const uint32_t bsh = b << (32 - K), bsh2 = b << sh2;
+    const uint32_t off = o + d * K + h * k1;
+    const uint32_t q = off >> 5;
+    const uint32_t w0 = ring[q & (kSpecRing - 1)], w1 = ring[(q + 1) & (kSpecRing - 1)];
+    const uint32_t w2 = ring[(q + 2) & (kSpecRing - 1)];
+    const uint32_t Y = __funnelshift_l(w1, w0, off);   // stream bits [off, off + 32)
+    const uint32_t Y2 = __funnelshift_l(w2, w1, off);  // [off + 32, off + 64)
+    // third iteration (after two rejections: v2 = (v' << k1) - b, k2 bits)
+    const uint32_t v2 = ((((1u << K) - b)) << k1) - b;
+    uint32_t k2 = __clz(v2) - __clz(b);
+    k2 += ((v2 << (k2 & 31)) < b) ? 1u : 0u;
+    const uint32_t t3 = K + k1;                                     // <= 32
+    const uint32_t Y3 = t3 == 32 ? Y2 : __funnelshift_l(Y2, Y, t3);  // [off + K + k1, ... + 32)
+    const uint32_t Z = Y - bsh;
+    const bool r1 = live && !pow2 && Y >= bsh;  // (b << (32 - K) wraps to 0 for a power of two)
+    const bool r2 = r1 && Z >= bsh2;
+    const uint32_t c2 = Z >> sh2;
+    const uint32_t c3 = ((c2 - b) << (k2 & 31)) | (Y3 >> ((32 - k2) & 31));
+    const bool r3 = r2 && c3 >= b;
+    uint32_t val = r2 ? c3 : (r1 ? c2 : Y >> (32 - K));
+    const uint32_t R = __ballot_sync(0xffffffffu, r1);
+    const uint32_t D = __ballot_sync(0xffffffffu, r2);
+    const uint32_t T = __ballot_sync(0xffffffffu, r3);
+    // h = 0 lanes up to the first rejection f0; then h = 1 lanes up to the next rejection f1
+    const uint32_t rm0 = R & 0x55555555u;
+    const uint32_t l0 = rm0 & (0u - rm0);   // lane (f0, 0), or 0
+    const uint32_t ab0 = 0u - (l0 << 2);    // lanes of the draws after f0 (0 when there is no f0)
+    const uint32_t rm1 = R & 0xAAAAAAAAu & ab0;
+    const uint32_t l1 = rm1 & (0u - rm1);   // lane (f1, 1), or 0
+    const uint32_t ab1 = 0u - (l1 << 1);    // lanes of the draws after f1
+    const bool dbl0 = (D & l0) != 0;
+    // lanes on the true path
+    const uint32_t path0 = 0x55555555u & ~ab0;                      // draws 0..f0 under h = 0 (all when no rejection)
+    const uint32_t path1 = dbl0 ? 0u : (0xAAAAAAAAu & ab0 & ~ab1);  // draws f0+1..f1 under h = 1
+    const uint32_t path = (path0 | path1) & lm;
+    const uint32_t dl = dbl0 ? l0 : (D & l1);  // the lane whose draw was rejected twice (it ends the batch), if any
+    const uint32_t consumed = (uint32_t)__popc(path);
+    uint32_t extra = (l0 ? k1 : 0u) + ((!dbl0 && l1) ? k1 : 0u);
+    if (dl) {
+      // bits the batch used beyond K per draw, known to that lane: its own shift, k1 and k2 --
+      // or, after a third rejection, whatever the serial loop (_kernels.py:71-82) takes
+      uint32_t e = h * k1 + k1 + k2;
+      if ((T & dl) && lanebit == dl) {
+        uint32_t v = (v2 << k2) - b, cc = c3 - b;
+        uint32_t p = off + K + k1 + k2;
         for (;;) {
           uint32_t k = __clz(v) - __clz(b);
           k += ((v << k) < b) ? 1u : 0u;
@@ -332,8 +321,8 @@ __global__ void __launch_bounds__(32 * kSpecWarps)
           if (p + 32 > 64 * wgen) {
             x = (uint32_t)(bits64_at(L.sd, p) >> 32);
           } else {
-            const uint32_t q = p >> 5;
-            x = __funnelshift_l(ring[(q + 1) & (kSpecRing - 1)], ring[q & (kSpecRing - 1)], p);
+            const uint32_t qq = p >> 5;
+            x = __funnelshift_l(ring[(qq + 1) & (kSpecRing - 1)], ring[qq & (kSpecRing - 1)], p);
           }
           cc = (cc << k) | (x >> (32 - k));
           v <<= k;
@@ -342,12 +331,12 @@ __global__ void __launch_bounds__(32 * kSpecWarps)
           cc -= b;
           v -= b;
         }
-        myval = cc;
-        e = p - off0 - K;
+        val = cc;
+        e = p - (o + (d + 1) * K);
       }
-      extra = __shfl_sync(0xffffffffu, e, serial_lane);
+      extra = __shfl_sync(0xffffffffu, e, __ffs(dl) - 1);
     }
-    if (lane < consumed) dr[s] = (uint16_t)myval;
+    if (path & lanebit) dr[s] = (uint16_t)val;
     o += consumed * K + extra;
     i -= consumed;
   }

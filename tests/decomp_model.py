@@ -266,11 +266,12 @@ def _k_of(v, b):
     return k
 
 
-def spec_decode_model(m, bits, H=6, lanes=32):
+def spec_decode_model(m, bits, H=2, lanes=16):
     """Draws j_i (i = m-1 .. 1, bound i+1) of a leaf from `bits`, decoded as
     leaf_decode_spec_kernel does: a batch = up to `lanes` consecutive steps with
     the same first-iteration width K and the same second-iteration width k1;
-    lane l evaluates its draw at o + l*K + h*k1 for h < H; the first rejection
+    draw l is evaluated at o + l*K + h*k1 for h < H (the kernel: 16 draws x 2
+    hypotheses, one per lane); the first rejection
     under hypothesis h hands the later lanes to h+1, a double rejection is
     finished serially and ends the batch.  Returns (draws, bits consumed,
     batches)."""
