@@ -104,3 +104,35 @@ def test_tensor_on_its_own_device_and_stream():
     s.synchronize()
     ref, _ = O.merge_shuffle_perm(100_000, 1000, 4)
     assert np.array_equal(x.cpu().numpy(), ref.astype(np.int32))
+
+
+@pytest.mark.parametrize("n,cutoff,dt", [(1 << 20, None, torch.int32), (3_000_001, None, torch.int64),
+                                         (300_007, 4096, torch.int32), (70_000, 65536, torch.int32),
+                                         (5000, 1000, torch.int32), (9, 2, torch.int32)])
+def test_both_leaf_decodes(n, cutoff, dt):
+    # the warp-per-leaf speculative decode (jobs of few leaves) and the lane-per-leaf decode
+    # produce the same draws: same permutation, same bit count, both equal to the oracle's
+    import ctypes
+    from paper_1508_03167_b200 import _lib
+    lib = _lib.load()
+    lib.sk_debug_set.argtypes = [ctypes.c_int, ctypes.c_int]
+    try:
+        for spec_max in (0, 1 << 30):
+            assert lib.sk_debug_set(8, spec_max) == 0
+            run(n, cutoff, 4242, dt)
+    finally:
+        lib.sk_debug_set(8, 1024)
+
+
+def test_speculative_decode_mid_stream():
+    # one long Fisher-Yates on a stream entered mid-word (prefix bits) through the warp-per-leaf decode
+    for m in (2, 3, 64, 65, 4097, 65_536):
+        x = torch.arange(m, dtype=torch.int32, device="cuda")
+        src = sk.BitSource(9)
+        src.take(29)
+        st = np.array(src.state_tuple(), dtype=np.uint64)
+        sk.fisher_yates(x, src)
+        a = np.arange(m, dtype=np.int64)
+        O.fy_range(a, 0, m, st)
+        assert np.array_equal(x.cpu().numpy().astype(np.int64), a)
+        assert tuple(int(v) for v in st) == tuple(src.state_tuple())
