@@ -403,7 +403,12 @@ def main():
             # the whole step: c+1 passes over the shard (leaves + local rounds)
             "step_passes": local_rounds + 1,
             "profiled_pass_ms_per_step": round(ms_prof / args.steps, 3),
-            "step_frac_of_roofline": round((local_rounds + 1) * alg_bytes / (peak * 1e9) * 1e3 / ms_per_step, 4)}
+            "step_frac_of_roofline": round((local_rounds + 1) * alg_bytes / (peak * 1e9) * 1e3 / ms_per_step, 4),
+            # achieved GB/s of the whole step = P * 2 * sizeof(T) * n / t, against the
+            # measured copy peak, the nominal 8 TB/s, and the one-pass floor (8 B/elem)
+            "step_achieved_gbs": round((local_rounds + 1) * alg_bytes / (ms_per_step * 1e-3) / 1e9, 1),
+            "step_frac_of_nominal_8tbs": round((local_rounds + 1) * alg_bytes / 8e12 * 1e3 / ms_per_step, 4),
+            "step_frac_of_one_pass_floor": round(alg_bytes / (peak * 1e9) * 1e3 / ms_per_step, 4)}
 
     # e2e through the public API with host buffers (pinned), H2D + D2H inside
     e2e = None
