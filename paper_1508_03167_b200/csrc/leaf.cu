@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(32 * kSpecWarps)
   auto refill = [&]() {
     const uint64_t x = leaf_word<FRESH>(L.sd, (uint64_t)wgen + lane);
     const uint32_t h = ((wgen + lane) * 2) & (kSpecRing - 1);
+    __syncwarp();  // every lane is done reading the slots this overwrites (they lie >= 2048 bits behind o)
     ring[h] = (uint32_t)(x >> 32);
     ring[h + 1] = (uint32_t)x;
     wgen += 32;
