@@ -214,7 +214,10 @@ static void launch_ws(bool fresh, unsigned blocks, const ArrayJob& J, const Expl
 constexpr int kSpecWarps = 4;
 constexpr uint32_t kSpecRing = 128;    // halves: 64 stream words per warp
 constexpr uint32_t kSpecAhead = 1536;  // bits kept generated past the batch start
-static uint64_t g_spec_decode_max = 1024;  // jobs with at most this many leaves take the warp-per-leaf decode (measured: 2.48 ms per leaf up to ~600 leaves, 2.95 ms at 1024, 4.0 ms at 2048 against 3.8 ms for a lane per leaf)
+// Jobs with at most this many leaves take the warp-per-leaf decode (measured:
+// 2.48 ms per leaf up to ~600 leaves, 2.95 ms at 1024, 4.0 ms at 2048, against
+// 3.8 ms at any count for a lane per leaf).
+static uint64_t g_spec_decode_max = 1024;
 
 template <bool FRESH>
 __global__ void __launch_bounds__(32 * kSpecWarps)
