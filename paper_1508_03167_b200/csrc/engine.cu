@@ -891,7 +891,11 @@ extern "C" {
 
 int sk_version(void) { return 1; }
 
-// Internal knobs for performance experiments (not part of the public header).
+// Internal knobs for performance experiments and tests (not part of the public
+// header): 1 = cut the leaf apply after phase k / test paths, 4 = tree merge
+// direct path, 6 = force the leaf apply's serial fallback, 7 = leaf-apply L2
+// eviction hints on/off, 8 = largest leaf count that takes the warp-per-leaf
+// speculative decode (0: always a lane per leaf).
 int sk_debug_set(int key, int value) {
   if (key == 1) { debug_set_leaf_stop(value); return 0; }
   if (key == 4) { debug_set_tree_force_direct(value); return 0; }
