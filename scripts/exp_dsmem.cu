@@ -41,6 +41,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
 
+// streaming: every thread reads kElems / kThreads / 4 coalesced 16-byte words, `reps` times
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
+    stream_kernel(int remote, uint32_t* out, long long* cycles) {
+  extern __shared__ uint32_t sdata[];
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t rank = cl.block_rank();
+  for (int i = threadIdx.x; i < kElems; i += kThreads) sdata[i] = hash32(i + rank * kElems);
+  cl.sync();
+  const uint4* src = reinterpret_cast<const uint4*>(remote ? cl.map_shared_rank(sdata, rank ^ 1) : sdata);
+  uint32_t acc = 0;
+  const long long t0 = clock64();
+  for (int rep = 0; rep < 8; ++rep) {
+#pragma unroll
+    for (int k = 0; k < kElems / 4 / kThreads; ++k) {
+      const uint4 v = src[(k * kThreads + threadIdx.x + rep * 32) & (kElems / 4 - 1)];  // (shifted per repetition)
+      acc += v.x ^ v.y ^ v.z ^ v.w ^ rep;
+    }
+    asm volatile("" ::: "memory");  // every repetition loads again
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  cl.sync();
+  out[blockIdx.x * kThreads + threadIdx.x] = acc;
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -63,6 +89,19 @@ int main() {
     printf("{\"mode\": \"%s\", \"gathers_per_cta\": %d, \"cycles\": %.0f, \"cycles_per_65536_gathers\": %.0f}\n",
            mode == 0 ? "local smem" : mode == 1 ? "peer smem (DSMEM)" : "half local, half peer",
            kThreads * kPerThread, avg, avg * 65536.0 / (kThreads * kPerThread));
+  }
+  cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int remote = 0; remote < 2; ++remote) {
+    for (int rep = 0; rep < 3; ++rep) {
+      stream_kernel<<<blocks, kThreads, smem>>>(remote, out, cyc);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("error: %s\n", cudaGetErrorString(e)); return 1; }
+    }
+    double sum = 0;
+    for (int b = 0; b < blocks; ++b) sum += (double)cyc[b];
+    const double avg = sum / blocks, bytes = 8.0 * kElems * 4;
+    printf("{\"mode\": \"coalesced 16-byte loads, %s\", \"bytes_per_cta\": %.0f, \"cycles\": %.0f, \"bytes_per_cycle_per_sm\": %.1f}\n",
+           remote ? "peer smem (DSMEM)" : "local smem", bytes, avg, bytes / avg);
   }
   return 0;
 }
