@@ -205,23 +205,38 @@ static void fork_side(cudaStream_t st, cudaStream_t ps) {
 // window chains (then lv[r].ev_chain), the tail offsets; one launch decodes
 // every pair's tail draws; per round the (dst, src) tail plan (then
 // lv[r].ev_tail).
+static cudaStream_t side_stream2();
+static int g_plan_streams = 2;  // 1: every round's plan on one side stream (debug knob)
+
 static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* d_bits, Arena& A, cudaStream_t ps) {
   const int nl = (int)lv.size();
-  for (auto& L : lv) {
+  // The rounds' plans are independent of one another until the tail draws, and
+  // their kernels are small: odd rounds go to a second side stream (forked
+  // from `ps` after the allocations, joined before the tail decode and again
+  // at the end), so the two streams fill each other's launch gaps and tails
+  // while the leaf decode holds its one warp per scheduler.
+  cudaStream_t ps2 = g_plan_streams > 1 && nl > 1 ? side_stream2() : ps;
+  std::vector<uint64_t*> csum(nl);
+  for (int i = 0; i < nl; ++i) {
+    auto& L = lv[i];
     L.rank = A.alloc<uint64_t>(L.npairs * L.sbs, ps);
     L.plans = A.alloc<PairPlan>(L.npairs, ps);
     L.chains = A.alloc<uint64_t>(tree_chain_words(L.npairs, L.tpp), ps);
     L.used = A.alloc<uint64_t>(1, ps);
+    csum[i] = A.alloc<uint64_t>(rank_scan_scratch(L.npairs, L.sbs), ps);
     CK(cudaEventCreateWithFlags(&L.ev_chain, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&L.ev_tail, cudaEventDisableTiming));
   }
-  for (auto& L : lv) {
-    uint64_t* csum = A.alloc<uint64_t>(rank_scan_scratch(L.npairs, L.sbs), ps);
-    launch_rank_tables(L.LJ, L.sbs, L.rank, csum, ps);
-    launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, ps);
-    launch_tree_chains(eb, L.plans, L.npairs, L.rank, L.tpp, L.chains, ps);
-    CK(cudaEventRecord(L.ev_chain, ps));
+  if (ps2 != ps) fork_side(ps, ps2);
+  for (int i = 0; i < nl; ++i) {
+    auto& L = lv[i];
+    cudaStream_t s = (i & 1) ? ps2 : ps;
+    launch_rank_tables(L.LJ, L.sbs, L.rank, csum[i], s);
+    launch_pair_plan(L.LJ, L.sbs, L.rank, L.plans, s);
+    launch_tree_chains(eb, L.plans, L.npairs, L.rank, L.tpp, L.chains, s);
+    CK(cudaEventRecord(L.ev_chain, s));
   }
+  if (ps2 != ps) fork_side(ps2, ps);  // the tail decode reads every round's plans
   uint64_t tot_pairs = 0;
   std::vector<uint64_t> pprefix(nl + 1, 0);
   std::vector<LevelTail> ht(nl);
@@ -241,7 +256,7 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
   poke(d_lt, ht.data(), nl * sizeof(LevelTail), ps);
   poke(d_pp, pprefix.data(), (nl + 1) * 8, ps);
   launch_tail_decode(d_lt, nl, d_pp, tot_pairs, d_bits, ps);
-  for (auto& L : lv) {
+  for (auto& L : lv) {  // (allocations first: they are ordered on `ps`)
     uint32_t hb = 1;
     while ((1ull << hb) < 2 * L.cap) ++hb;
     L.hmask = (uint32_t)((1ull << hb) - 1);
@@ -254,15 +269,22 @@ static void build_plans(std::vector<LevelBufs>& lv, int eb, unsigned long long* 
     L.dst = A.alloc<uint64_t>(2 * L.cap, ps);
     L.src = A.alloc<uint64_t>(2 * L.cap, ps);
     L.tmp = A.alloc<uint64_t>(2 * L.cap, ps);
-    CK(cudaMemsetAsync(L.hkey, 0xFF, (8ull << hb), ps));
-    CK(cudaMemsetAsync(L.hhead, 0xFF, (4ull << hb), ps));
-    CK(cudaMemsetAsync(L.keyed, 0, L.cap, ps));
-    CK(cudaMemsetAsync(L.dst, 0xFF, 2 * L.cap * 8, ps));
-    launch_tail_plan(L.plans, L.rec_key, L.rec_pair, L.used, L.cap, L.hkey, L.hhead, L.next, L.slot_of, L.hmask,
-                     L.predx, L.keyed, L.dst, L.src, ps);
-    launch_tail_chase(L.plans, L.rec_key, L.rec_pair, L.predx, L.keyed, L.used, L.cap, L.dst, L.src, ps);
-    CK(cudaEventRecord(L.ev_tail, ps));
   }
+  if (ps2 != ps) fork_side(ps, ps2);
+  for (int i = 0; i < nl; ++i) {
+    auto& L = lv[i];
+    cudaStream_t s = (i & 1) ? ps2 : ps;
+    const uint64_t hsz = (uint64_t)L.hmask + 1;
+    CK(cudaMemsetAsync(L.hkey, 0xFF, 8 * hsz, s));
+    CK(cudaMemsetAsync(L.hhead, 0xFF, 4 * hsz, s));
+    CK(cudaMemsetAsync(L.keyed, 0, L.cap, s));
+    CK(cudaMemsetAsync(L.dst, 0xFF, 2 * L.cap * 8, s));
+    launch_tail_plan(L.plans, L.rec_key, L.rec_pair, L.used, L.cap, L.hkey, L.hhead, L.next, L.slot_of, L.hmask,
+                     L.predx, L.keyed, L.dst, L.src, s);
+    launch_tail_chase(L.plans, L.rec_key, L.rec_pair, L.predx, L.keyed, L.used, L.cap, L.dst, L.src, s);
+    CK(cudaEventRecord(L.ev_tail, s));
+  }
+  if (ps2 != ps) fork_side(ps2, ps);  // callers wait for `ps` before releasing the arena
   CK(cudaGetLastError());
 }
 
@@ -277,10 +299,10 @@ static void destroy_events(std::vector<LevelBufs>& lv) {
 // Helper streams of the calling thread on the CURRENT device (a thread may
 // drive several devices in turn): plan, round and copy streams, created on
 // first use per device.
-enum HelperStream { kPlanStream = 0, kRoundStream = 1, kCopyStream = 2 };
+enum HelperStream { kPlanStream = 0, kRoundStream = 1, kCopyStream = 2, kPlanStream2 = 3 };
 constexpr int kMaxDevices = 64;
 struct HelperStreams {
-  cudaStream_t s[3][kMaxDevices] = {};
+  cudaStream_t s[4][kMaxDevices] = {};
   ~HelperStreams() {
     for (auto& row : s)
       for (cudaStream_t x : row)
@@ -299,6 +321,7 @@ static cudaStream_t helper_stream(HelperStream which) {
 }
 
 static cudaStream_t side_stream() { return helper_stream(kPlanStream); }
+static cudaStream_t side_stream2() { return helper_stream(kPlanStream2); }
 
 // Run rounds 1..c over `cur` (data currently there); the result lands in
 // `other`.  The tree merge reads every window of a CTA before writing it back
@@ -895,13 +918,15 @@ int sk_version(void) { return 1; }
 // header): 1 = cut the leaf apply after phase k / test paths, 4 = tree merge
 // direct path, 6 = force the leaf apply's serial fallback, 7 = leaf-apply L2
 // eviction hints on/off, 8 = largest leaf count that takes the warp-per-leaf
-// speculative decode (0: always a lane per leaf).
+// speculative decode (0: always a lane per leaf), 10 = side streams for the
+// rounds' plans (1 or 2).
 int sk_debug_set(int key, int value) {
   if (key == 1) { debug_set_leaf_stop(value); return 0; }
   if (key == 4) { debug_set_tree_force_direct(value); return 0; }
   if (key == 6) { debug_set_leaf_fallback(value); return 0; }
   if (key == 7) { debug_set_leaf_l2pol(value); return 0; }
   if (key == 8) { debug_set_spec_decode_max(value); return 0; }
+  if (key == 10) { g_plan_streams = value; return 0; }
   return -1;
 }
 const char* sk_last_error(void) { return g_err.c_str(); }
